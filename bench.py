@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py — stochastic GCP gradient throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c1|c3|c4] [--samples S]
+
+One "step" = one pass of the hot path over one batch of synthetic samples:
+fused sample -> model eval -> loss derivative -> d-mode MTTKRP (one kernel),
+[NCCL all-reduce of the gradient when N > 1], fused Adam update.  Default
+workload: BASELINE.json configs[1] (C2: dense 200^4 binary, bernoulli-odds,
+r=16, uniform s=1.6e7 per GPU).  Multi-GPU is weak scaling (s per GPU fixed,
+samples sharded by ordinal range, factors replicated).
+
+Prints ONE JSON line on rank 0 (driver contract).  `--impl reference` times
+the reference's own CPU implementation (oracle/_ref, the unmodified reference
+compiled here) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))  # cpu_baseline / reference legs only
+
+METRIC = "GCP stochastic-gradient samples/sec (sample+eval+MTTKRP), % of HBM roofline"
+UNIT = "samples/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) >= 7 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(statistics.median(sm)), "sm_max_mhz": int(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# workload setup on the engine
+# ---------------------------------------------------------------------------
+def setup_engine(w, device, log):
+    import torch
+    import paper_1906_01687_b200.gcp as G
+    from paper_1906_01687_b200 import workloads as WL
+
+    e = G.Engine(w.dims, w.rank, dtype=w.dtype, device=device)
+    t0 = time.perf_counter()
+    if w.name == "c2":
+        e.generate_dense_bernoulli(WL.c2_true_factors(1002), seed=1002)
+    elif w.name == "c1":
+        rs = np.random.default_rng(1001)
+        A = [rs.standard_normal((n, 5)) for n in w.dims]
+        A = [a / np.linalg.norm(a, axis=0) for a in A]
+        M = np.einsum("ir,jr,kr->ijk", *A)
+        E = rs.standard_normal(M.shape)
+        X = M + 0.1 * (np.linalg.norm(M) / np.linalg.norm(E)) * E
+        e.set_dense(X.reshape(-1, order="F"), "f64")
+    else:
+        keys = WL.sparse_keys(w, 1000 + int(w.name[1]))
+        vals = WL.sparse_values(w, len(keys), 1100 + int(w.name[1]))
+        kt = torch.from_numpy(keys.view(np.int64)).to(f"cuda:{device}")
+        vt = torch.from_numpy(vals).to(f"cuda:{device}")
+        e.set_sparse_device(kt.data_ptr(), vt.data_ptr(), len(keys), "f32")
+        torch.cuda.synchronize(device)
+        del kt, vt
+    log(f"[bench] data ready in {time.perf_counter() - t0:.1f}s")
+    xnorm = e.tensor_norm()
+    F = WL.init_factors(w.dims, w.rank, 2000 + int(w.name[1]), data_norm=xnorm)
+    if w.dtype == "f32":
+        F = [f.astype(np.float32).astype(np.float64) for f in F]
+    e.set_factors(F)
+    return e, F
+
+
+def sampler_of(w, G, nranks=1):
+    if w.sampler == "uniform":
+        return G.SamplerKind.uniform(w.s * nranks)
+    if w.sampler == "stratified":
+        return G.SamplerKind.stratified(w.p * nranks, w.q * nranks, w.rho)
+    return G.SamplerKind.semi_stratified(w.p * nranks, w.q * nranks)
+
+
+def launches_per_step(w, nranks):
+    if w.sampler == "stratified":
+        # 3 x (plan + candidate) + status memset is a memset, fused kernel, adam
+        return 3 * 2 + 1 + 1
+    return 2
+
+
+# ---------------------------------------------------------------------------
+# CPU reference timing (oracle/_ref = the unmodified reference compiled here)
+# ---------------------------------------------------------------------------
+def reference_cpu(w, steps, warmup, n_sample, log):
+    import oracle as O
+    from paper_1906_01687_b200 import workloads as WL
+    ref = O.reference()
+    if ref is None:
+        return None
+    threads = os.cpu_count() or 1
+    loss_kind = {"gaussian": 0, "poisson": 1, "bernoulli-odds": 2}[w.loss]
+    rs = np.random.default_rng(4242)
+    if w.name == "c2":
+        # The reference cannot hold the 1.6e9-entry tensor (DenseTensor cap
+        # 1e8, tensor.hpp:54): time its per-sample entry+deriv+weight+append
+        # loop (samplers.hpp:87-93) on builder-supplied (index, x), then
+        # mttkrp_sampled_all(threads) and adam_step.
+        T = WL.c2_true_factors(1002)
+        idx = np.stack([rs.integers(0, n, n_sample) for n in w.dims], 1).astype(np.int64)
+        m = np.ones((n_sample, T[0].shape[1]))
+        for k in range(4):
+            m *= T[k][idx[:, k]]
+        m = m.sum(1)
+        x = (rs.random(n_sample) < m / (1.0 + m)).astype(np.float64)
+        F = WL.init_factors(w.dims, w.rank, 2002, data_norm=np.sqrt(0.1 * 1.6e9))
+        import ctypes as C
+        dims = np.array(w.dims, dtype=np.int64)
+        h = C.c_void_p()
+        ref._ck(ref.lib.ref_bench_model_new(len(dims), O._i64(dims), w.rank,
+                                            O._f64(O.Oracle.flat(F)), C.byref(h)))
+        weight = float(np.prod(np.array(w.dims, dtype=np.float64))) / n_sample
+        times = []
+        tm = np.zeros(3)
+        for it in range(warmup + steps):
+            ref._ck(ref.lib.ref_bench_step_given(h, loss_kind, 0.0, n_sample, O._i64(idx),
+                                                 O._f64(x), weight, threads, 1e-3, 1, 0.0,
+                                                 O._f64(tm)))
+            if it >= warmup:
+                times.append(tm.copy())
+        ref.lib.ref_bench_model_free(h)
+        t = np.mean(times, axis=0)
+        sample = (f"{n_sample} pre-drawn uniform samples of C2 per step (entry+deriv+append "
+                  f"{t[0]*1e3:.1f} ms, mttkrp_sampled_all({threads} threads) {t[1]*1e3:.1f} ms, "
+                  f"adam_step {t[2]*1e3:.1f} ms); x from the C2 generator model")
+        return {"value": n_sample / float(t.sum()), "unit": UNIT, "cores": threads,
+                "kind": "reference", "sample": sample, "step_s": float(t.sum())}
+    return None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, w):
+    import torch
+    import paper_1906_01687_b200.gcp as G
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    def log(msg):
+        if rank == 0:
+            print(msg, file=sys.stderr, flush=True)
+
+    e, F = setup_engine(w, local, log)
+    stream = torch.cuda.current_stream()
+    e.set_stream(stream.cuda_stream)
+    if world > 1:
+        uid = [G.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        e.comm_init(uid[0], rank, world)
+    e.set_shard(rank, world)
+    sk = sampler_of(w, G, world)
+    loss = G.LossFunction.parse(w.loss)
+    lr = 1e-3
+    seed = 3000 + int(w.name[1])
+
+    def step(it):
+        e.stoch_grad(sk, loss, seed, it, want_stats=False)
+        if world > 1:
+            e.allreduce_grad()
+        e.adam_step(lr, lower_bound=w.lower_bound)
+
+    for it in range(args.warmup):
+        step(it)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for k in range(K):
+        ev[k][0].record(stream)
+        e.stoch_grad(sk, loss, seed, args.warmup + k, want_stats=False)
+        ev[k][1].record(stream)
+        if world > 1:
+            e.allreduce_grad()
+        e.adam_step(lr, lower_bound=w.lower_bound)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    fused_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    if dist:
+        t = torch.tensor([total_ms, fused_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, fused_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / K
+    samples_per_step = w.samples_per_step * world
+    value = samples_per_step / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (the fused sample->eval->MTTKRP launch)
+    peak_gbs, peak_src = _peaks()
+    bps = w.bytes_per_sample()
+    achieved = bps * w.samples_per_step / (fused_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_traffic_{w.name}.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
+                "frac": round(achieved / peak_gbs, 4), "traffic": traffic,
+                "kernel": "fused_grad_kernel (sample+eval+deriv+MTTKRP)",
+                "kernel_ms": round(fused_ms, 4), "bytes_per_sample": bps,
+                "bytes_per_sample_formula": "4d + 2*d*r*F (int32 index/mode + gathered + "
+                                            "scattered factor rows)",
+                "peak_source": peak_src}
+
+    # e2e through the C-ABI with host buffers: factors H2D, step, factors D2H
+    e2e = None
+    if not args.no_e2e:
+        host_F = e.factors()
+        Ke = max(3, min(K, 20))
+        for it in range(2):
+            e.set_factors(host_F)
+            step(10_000 + it)
+            host_F = e.factors()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for it in range(Ke):
+            e.set_factors(host_F)
+            step(20_000 + it)
+            host_F = e.factors()
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t[0])
+        rp = ((w.rank + (8 if w.dtype == "f32" else 4) - 1) // (8 if w.dtype == "f32" else 4)) * \
+            (8 if w.dtype == "f32" else 4)
+        fb = 4 if w.dtype == "f32" else 8
+        nbytes = sum(n * rp * fb for n in w.dims)
+        e2e = {"value": samples_per_step * Ke / el, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes,
+               "what": "gcpb_set_factors(host) + gcpb_stoch_grad + gcpb_adam_step + "
+                       "gcpb_get_factors(host) per step, wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = reference_cpu(w, steps=2, warmup=1, n_sample=args.cpu_samples, log=log)
+        except Exception as ex:  # reported, not fatal
+            log(f"[bench] cpu baseline failed: {ex}")
+    if cpu:
+        cpu.pop("step_s", None)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
+        "data": f"synthetic ({w.description}); seeded generator, no dataset",
+        "config": {"workload": f"{w.name.upper()}: {w.description}",
+                   "samples_per_gpu_step": w.samples_per_step, "global_batch": samples_per_step,
+                   "rank": w.rank, "dims": list(w.dims), "loss": w.loss, "sampler": w.sampler,
+                   "parallelism": f"dp{world} (samples sharded, factors replicated, NCCL "
+                                  f"all-reduce of the gradient)" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (tensor in HBM); factor rows L2/L1-resident "
+                         "by design", "step": "fused grad kernel + adam (+ all-reduce)"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step(w, world) * K, "clocks": clk,
+        "impl": "ours",
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    t0 = time.perf_counter()
+    cpu = reference_cpu(w, steps=args.steps, warmup=args.warmup, n_sample=args.cpu_samples,
+                        log=lambda m: print(m, file=sys.stderr))
+    if cpu is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libgcpref.so (reference compiled from /root/reference) "
+                          "not present"}))
+        return
+    line = {
+        "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["step_s"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic ({w.description})",
+        "config": {"workload": f"{w.name.upper()}: {w.description}",
+                   "samples_per_step": args.cpu_samples, "rank": w.rank, "dims": list(w.dims),
+                   "loss": w.loss, "sampler": w.sampler},
+        "impl": "reference",
+        "cpu_baseline": {"value": cpu["value"], "unit": UNIT, "cores": cpu["cores"],
+                         "kind": "reference", "sample": cpu["sample"]},
+        "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--samples", type=int, default=None, help="override s (uniform) per GPU")
+    ap.add_argument("--cpu-samples", type=int, default=1_000_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    from paper_1906_01687_b200 import workloads as WL
+    w = WL.get(args.config, s=args.samples)
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,240 @@
+/* gcpb.h — C-ABI of the B200-native stochastic GCP gradient engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj, the inner loop of fit_gcp_adam at
+ * src/optimizer.cpp:115-120).  Each entry point names the reference interface
+ * it replaces.  Plain pointers and sizes only; all host buffers are borrowed
+ * for the duration of the call; the context owns all device memory.
+ *
+ * Status codes mirror the reference's exception classes:
+ *   GCPB_OK 0, GCPB_ERR_RUNTIME 1 (std::runtime_error / CUDA / NCCL),
+ *   GCPB_ERR_USAGE 2 (std::invalid_argument), GCPB_ERR_DOMAIN 3
+ *   (std::domain_error), GCPB_ERR_RANGE 4 (std::out_of_range),
+ *   GCPB_ERR_LOGIC 5 (std::logic_error).  gcpb_last_error(ctx) returns the
+ *   message of the last failure on that context (gcpb_last_error(NULL) for
+ *   failures of gcpb_create and the context-free helpers).
+ *
+ * Threading: a context is not thread-safe; use one host thread per device.
+ * Work is ordered on the context's stream; calls that return host-visible
+ * outputs synchronise that stream before returning.
+ */
+#ifndef GCPB_H
+#define GCPB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GCPB_OK 0
+#define GCPB_ERR_RUNTIME 1
+#define GCPB_ERR_USAGE 2
+#define GCPB_ERR_DOMAIN 3
+#define GCPB_ERR_RANGE 4
+#define GCPB_ERR_LOGIC 5
+
+/* Factor / arithmetic type of a context.  The reference is fp64-only
+ * (include/gcp/kruskal.hpp:16); fp32 is the B200 fast path. */
+#define GCPB_F32 0
+#define GCPB_F64 1
+
+/* Dense tensor storage in HBM.  U8 holds exact small integers (binary or
+ * count data), F32/F64 anything else. */
+#define GCPB_STORE_U8 0
+#define GCPB_STORE_F32 1
+#define GCPB_STORE_F64 2
+
+/* LossKind, same order as include/gcp/loss.hpp:8-15. */
+#define GCPB_LOSS_GAUSSIAN 0
+#define GCPB_LOSS_POISSON 1
+#define GCPB_LOSS_BERNOULLI_ODDS 2
+#define GCPB_LOSS_GAMMA 3
+#define GCPB_LOSS_BETA_HALF 4
+#define GCPB_LOSS_HUBER 5
+
+/* SamplerKind::Strategy, include/gcp/samplers.hpp:32. */
+#define GCPB_UNIFORM 0
+#define GCPB_STRATIFIED 1
+#define GCPB_SEMI_STRATIFIED 2
+
+/* EstimatorSamples::Kind, include/gcp/samplers.hpp:259. */
+#define GCPB_EST_UNIFORM 0
+#define GCPB_EST_STRATIFIED 1
+
+typedef struct gcpb_ctx gcpb_ctx;
+
+/* LossFunction (include/gcp/loss.hpp:20-56): kind + huber delta. */
+typedef struct {
+  int32_t kind;
+  double delta;
+} gcpb_loss;
+
+/* SamplerKind (include/gcp/samplers.hpp:31-51). */
+typedef struct {
+  int32_t strategy;
+  int64_t num_samples;     /* s, uniform only */
+  int64_t nonzero_samples; /* p */
+  int64_t zero_samples;    /* q */
+  double oversample;       /* rho, stratified rejection batch factor */
+} gcpb_sampler;
+
+/* RejectionStats (include/gcp/samplers.hpp:53-57). */
+typedef struct {
+  int64_t tested;
+  int64_t accepted;
+  int64_t rejected;
+} gcpb_stats;
+
+/* The FitConfig fields adam_step reads (include/gcp/optimizer.hpp:42-65),
+ * plus the current learning rate (AdamState::learning_rate). */
+typedef struct {
+  double learning_rate;
+  double beta1;
+  double beta2;
+  double epsilon;
+  int32_t has_lower_bound;
+  double lower_bound;
+} gcpb_adam;
+
+/* ---- lifetime ------------------------------------------------------------
+ * Replaces KruskalModel(Shape, rank) + GradientSet/AdamState allocation
+ * (src/kruskal.cpp:10-16, src/kernels.cpp:61-67, src/optimizer.cpp:19-29).
+ * Factors start at zero.  dims: n_1..n_d (1 <= d <= 16, each < 2^31).      */
+int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t rank,
+                gcpb_ctx** out);
+void gcpb_destroy(gcpb_ctx* ctx);
+const char* gcpb_last_error(const gcpb_ctx* ctx);
+const char* gcpb_version(void);
+/* Run the context's work on a caller-owned CUDA stream (cudaStream_t as void*);
+ * NULL restores the context's own stream. */
+int gcpb_set_stream(gcpb_ctx* ctx, void* stream);
+void* gcpb_get_stream(gcpb_ctx* ctx);
+
+/* ---- tensor data ----------------------------------------------------------
+ * SparseTensor(Shape, indices, values) (src/tensor.cpp:10-41): coords are
+ * nnz x d row-major int64; duplicates are summed, zeros dropped, entries
+ * sorted by first-mode-fastest linear key (that order defines nonzero pick
+ * ordinals).  Bad index -> GCPB_ERR_RANGE naming the mode.  Builds the
+ * device SoA COO and the open-addressing hash of linear keys.              */
+int gcpb_set_sparse(gcpb_ctx* ctx, int64_t nnz, const int64_t* coords, const double* values);
+/* Device-resident ingest for generated data: keys_sorted (strictly
+ * increasing linear keys, device pointer) and values (device pointer of
+ * value_dtype GCPB_F32/GCPB_F64); copied into the context. */
+int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_sorted,
+                           const void* d_values, int value_dtype);
+int64_t gcpb_nnz(const gcpb_ctx* ctx);
+/* Normalised COO read-back (nnz x d int64, values as double). */
+int gcpb_get_sparse(gcpb_ctx* ctx, int64_t* coords_out, double* values_out);
+/* DenseTensor values (include/gcp/tensor.hpp:52-81), first-mode-fastest. */
+int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage);
+/* Device-resident dense ingest from a device pointer in `storage` layout. */
+int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage);
+/* Synthetic dense binary tensor generated in HBM (BASELINE configs[1]):
+ * x(i) ~ Bernoulli(m_i / (1 + m_i)) with m the rank-true_rank model given by
+ * true_factors (double, flattened mode-major row-major), uniform from a
+ * counter hash of (seed, linear index).  Stored as U8. */
+int gcpb_generate_dense_bernoulli(gcpb_ctx* ctx, int64_t true_rank, const double* true_factors,
+                                  uint64_t seed);
+/* TensorView::norm (src/tensor.cpp:56-60,70-74): Frobenius norm of the data,
+ * fp64 accumulation. */
+int gcpb_tensor_norm(gcpb_ctx* ctx, double* out);
+/* TensorView::value_at (include/gcp/tensor.hpp:95-97) for n indices. */
+int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out);
+
+/* ---- factors, gradient, moments -------------------------------------------
+ * mode-wise n_k x r row-major double (KruskalModel::factor, GradientSet::modes,
+ * AdamState::{first,second}_moment); mode = -1 means all modes flattened in
+ * mode order (GradientSet::flatten order, src/kernels.cpp:74-85).           */
+int gcpb_set_factors(gcpb_ctx* ctx, int mode, const double* values);
+int gcpb_get_factors(gcpb_ctx* ctx, int mode, double* out);
+int gcpb_get_grad(gcpb_ctx* ctx, int mode, double* out);
+int gcpb_set_grad(gcpb_ctx* ctx, int mode, const double* values);
+/* which: 0 = first moment B, 1 = second moment C. */
+int gcpb_get_moment(gcpb_ctx* ctx, int which, int mode, double* out);
+int gcpb_set_moment(gcpb_ctx* ctx, int which, int mode, const double* values);
+
+/* ---- the hot path -------------------------------------------------------------
+ * draw_gradient_samples + mttkrp_sampled_all (include/gcp/samplers.hpp:223-245,
+ * src/kernels.cpp:137-168), fused: sample -> model entry -> loss derivative
+ * -> weight -> d-mode sparse MTTKRP scatter.  The gradient (overwritten, not
+ * accumulated) stays on the device.  Draws come from the Philox4x32-10 stream
+ * keyed by `seed` at iteration `iter`; stats may be NULL.
+ * Validation, forfeit rules and errors follow the reference.               */
+int gcpb_stoch_grad(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                    uint64_t seed, uint64_t iter, gcpb_stats* stats);
+
+/* Parity: the sampler alone.  Writes n samples (returned in *n_out; cap is
+ * the capacity) in the reference's GradientSamples order: index (n x d int64),
+ * data value x, weight w, flag (1 = semi-stratified nonzero term, y uses
+ * g(x,m) - g(0,m)), model entry m, final weighted derivative y. */
+int gcpb_draw_samples(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                      uint64_t seed, uint64_t iter, int64_t cap, int64_t* idx_out,
+                      double* x_out, double* w_out, int32_t* flag_out, double* m_out,
+                      double* y_out, int64_t* n_out, gcpb_stats* stats);
+/* Parity: KruskalModel::entry + LossFunction::deriv + weight on given samples
+ * (src/kruskal.cpp:47-58, src/loss.cpp:88-110, samplers.hpp:90-91,206).
+ * flags may be NULL (all 0). */
+int gcpb_eval_deriv(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const double* x,
+                    const double* w, const int32_t* flags, const gcpb_loss* loss,
+                    double* m_out, double* y_out);
+/* Parity: mttkrp_sampled_all on given (index, value) samples
+ * (src/kernels.cpp:137-168); result in the context's gradient. */
+int gcpb_mttkrp_samples(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const double* y);
+
+/* ---- optimizer ----------------------------------------------------------------
+ * adam_step (src/optimizer.cpp:47-66): moments, bias-corrected step with
+ * epsilon inside the sqrt, projection, iteration counter += 1; fused with
+ * zeroing the gradient for the next stoch_grad. */
+int gcpb_adam_step(gcpb_ctx* ctx, const gcpb_adam* adam);
+/* AdamState::init (src/optimizer.cpp:19-29): zero moments, iterations = 0. */
+int gcpb_adam_reset(gcpb_ctx* ctx);
+int gcpb_get_iterations(gcpb_ctx* ctx, int64_t* out);
+int gcpb_set_iterations(gcpb_ctx* ctx, int64_t iterations);
+
+/* ---- loss estimator -------------------------------------------------------------
+ * EstimatorSamples (include/gcp/samplers.hpp:257-351).  set: given samples;
+ * draw: drawn on the device from the Philox stream (tags EST_*). */
+int gcpb_estimator_set(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const double* x,
+                       const double* w);
+int gcpb_estimator_draw(gcpb_ctx* ctx, int kind, int64_t count, double rho, uint64_t seed);
+int64_t gcpb_estimator_size(const gcpb_ctx* ctx);
+int gcpb_estimator_get(gcpb_ctx* ctx, int64_t* idx_out, double* x_out, double* w_out);
+/* EstimatorSamples::estimate (src/samplers.cpp:114-124): fp64 accumulation in
+ * a fixed order (bit-deterministic for a given model). */
+int gcpb_estimate(gcpb_ctx* ctx, const gcpb_loss* loss, double* out);
+
+/* ---- rollback snapshot (src/optimizer.cpp:101-105,129-140) ---------------------- */
+int gcpb_snapshot_save(gcpb_ctx* ctx);
+int gcpb_snapshot_restore(gcpb_ctx* ctx);
+
+/* ---- multi-GPU (one process per GPU) ---------------------------------------------
+ * Samples are sharded by ordinal range across ranks (gcpb_shard_range);
+ * factors are replicated; the gradient is summed with an NCCL all-reduce. */
+int gcpb_nccl_unique_id(char out[128]);
+int gcpb_comm_init(gcpb_ctx* ctx, const char unique_id[128], int rank, int nranks);
+int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks);
+int gcpb_allreduce_grad(gcpb_ctx* ctx);
+
+/* ---- host-only helpers (no device needed) ----------------------------------------- */
+/* Product Philox stream: bounded draw in [0, n). */
+uint64_t gcpb_philox_bounded(uint64_t seed, uint32_t tag, uint64_t iter, uint64_t t, int slot,
+                             uint64_t n);
+/* One zero-rejection batch size (include/gcp/samplers.hpp:118-122). */
+int64_t gcpb_zero_batch_size(double total, double zeta, double rho, int64_t shortfall);
+/* Contiguous ordinal range [begin, end) of n units owned by rank of nranks. */
+void gcpb_shard_range(int64_t n, int rank, int nranks, int64_t* begin, int64_t* end);
+/* Stratified multi-rank merge: given every rank's count of accepted zero
+ * candidates in its slice (candidate order = rank order), the global rank
+ * offset of this rank's first accept and how many of its accepts to keep so
+ * that exactly the first `need` accepts overall are kept. */
+void gcpb_stratified_keep(const int64_t* accepted_per_rank, int nranks, int rank, int64_t need,
+                          int64_t* offset, int64_t* keep);
+/* Loss derivative / value in double (LossFunction::deriv/value). */
+double gcpb_loss_deriv(const gcpb_loss* loss, double x, double m);
+double gcpb_loss_value(const gcpb_loss* loss, double x, double m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCPB_H */

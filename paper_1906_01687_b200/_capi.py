@@ -1,0 +1,115 @@
+"""ctypes binding of the C-ABI in include/gcpb.h (libgcpb.so, built in-tree).
+
+There is no fallback: if the engine library is missing, importing this module
+raises — build it with ``python -m paper_1906_01687_b200.build``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_LIB_PATH = Path(os.environ.get("GCPB_LIB", Path(__file__).resolve().parent / "libgcpb.so"))
+
+if not _LIB_PATH.exists():
+    raise ImportError(
+        f"gcpb engine library not found at {_LIB_PATH}; build it with "
+        "`python -m paper_1906_01687_b200.build` (there is no CPU fallback)")
+
+lib = C.CDLL(str(_LIB_PATH))
+
+# status codes (gcpb.h)
+OK, ERR_RUNTIME, ERR_USAGE, ERR_DOMAIN, ERR_RANGE, ERR_LOGIC = 0, 1, 2, 3, 4, 5
+F32, F64 = 0, 1
+STORE_U8, STORE_F32, STORE_F64 = 0, 1, 2
+UNIFORM, STRATIFIED, SEMI_STRATIFIED = 0, 1, 2
+EST_UNIFORM, EST_STRATIFIED = 0, 1
+
+
+class gcpb_loss(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("delta", C.c_double)]
+
+
+class gcpb_sampler(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("num_samples", C.c_int64),
+                ("nonzero_samples", C.c_int64), ("zero_samples", C.c_int64),
+                ("oversample", C.c_double)]
+
+
+class gcpb_stats(C.Structure):
+    _fields_ = [("tested", C.c_int64), ("accepted", C.c_int64), ("rejected", C.c_int64)]
+
+
+class gcpb_adam(C.Structure):
+    _fields_ = [("learning_rate", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("epsilon", C.c_double), ("has_lower_bound", C.c_int32),
+                ("lower_bound", C.c_double)]
+
+
+ctx_p = C.c_void_p
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+i32p = C.POINTER(C.c_int32)
+u64p = C.POINTER(C.c_uint64)
+
+# (name, restype, argtypes) for every entry point of include/gcpb.h
+SIGNATURES = [
+    ("gcpb_create", C.c_int, [C.c_int, C.c_int, C.c_int, i64p, C.c_int64, C.POINTER(ctx_p)]),
+    ("gcpb_destroy", None, [ctx_p]),
+    ("gcpb_last_error", C.c_char_p, [ctx_p]),
+    ("gcpb_version", C.c_char_p, []),
+    ("gcpb_set_stream", C.c_int, [ctx_p, C.c_void_p]),
+    ("gcpb_get_stream", C.c_void_p, [ctx_p]),
+    ("gcpb_set_sparse", C.c_int, [ctx_p, C.c_int64, i64p, f64p]),
+    ("gcpb_set_sparse_device", C.c_int, [ctx_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]),
+    ("gcpb_nnz", C.c_int64, [ctx_p]),
+    ("gcpb_get_sparse", C.c_int, [ctx_p, i64p, f64p]),
+    ("gcpb_set_dense", C.c_int, [ctx_p, f64p, C.c_int]),
+    ("gcpb_set_dense_device", C.c_int, [ctx_p, C.c_void_p, C.c_int]),
+    ("gcpb_generate_dense_bernoulli", C.c_int, [ctx_p, C.c_int64, f64p, C.c_uint64]),
+    ("gcpb_tensor_norm", C.c_int, [ctx_p, f64p]),
+    ("gcpb_value_at", C.c_int, [ctx_p, C.c_int64, i64p, f64p]),
+    ("gcpb_set_factors", C.c_int, [ctx_p, C.c_int, f64p]),
+    ("gcpb_get_factors", C.c_int, [ctx_p, C.c_int, f64p]),
+    ("gcpb_get_grad", C.c_int, [ctx_p, C.c_int, f64p]),
+    ("gcpb_set_grad", C.c_int, [ctx_p, C.c_int, f64p]),
+    ("gcpb_get_moment", C.c_int, [ctx_p, C.c_int, C.c_int, f64p]),
+    ("gcpb_set_moment", C.c_int, [ctx_p, C.c_int, C.c_int, f64p]),
+    ("gcpb_stoch_grad", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
+                                  C.c_uint64, C.c_uint64, C.POINTER(gcpb_stats)]),
+    ("gcpb_draw_samples", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
+                                    C.c_uint64, C.c_uint64, C.c_int64, i64p, f64p, f64p, i32p,
+                                    f64p, f64p, i64p, C.POINTER(gcpb_stats)]),
+    ("gcpb_eval_deriv", C.c_int, [ctx_p, C.c_int64, i64p, f64p, f64p, i32p,
+                                  C.POINTER(gcpb_loss), f64p, f64p]),
+    ("gcpb_mttkrp_samples", C.c_int, [ctx_p, C.c_int64, i64p, f64p]),
+    ("gcpb_adam_step", C.c_int, [ctx_p, C.POINTER(gcpb_adam)]),
+    ("gcpb_adam_reset", C.c_int, [ctx_p]),
+    ("gcpb_get_iterations", C.c_int, [ctx_p, i64p]),
+    ("gcpb_set_iterations", C.c_int, [ctx_p, C.c_int64]),
+    ("gcpb_estimator_set", C.c_int, [ctx_p, C.c_int64, i64p, f64p, f64p]),
+    ("gcpb_estimator_draw", C.c_int, [ctx_p, C.c_int, C.c_int64, C.c_double, C.c_uint64]),
+    ("gcpb_estimator_size", C.c_int64, [ctx_p]),
+    ("gcpb_estimator_get", C.c_int, [ctx_p, i64p, f64p, f64p]),
+    ("gcpb_estimate", C.c_int, [ctx_p, C.POINTER(gcpb_loss), f64p]),
+    ("gcpb_snapshot_save", C.c_int, [ctx_p]),
+    ("gcpb_snapshot_restore", C.c_int, [ctx_p]),
+    ("gcpb_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("gcpb_comm_init", C.c_int, [ctx_p, C.c_char_p, C.c_int, C.c_int]),
+    ("gcpb_set_shard", C.c_int, [ctx_p, C.c_int, C.c_int]),
+    ("gcpb_allreduce_grad", C.c_int, [ctx_p]),
+    ("gcpb_philox_bounded", C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
+                                         C.c_uint64]),
+    ("gcpb_zero_batch_size", C.c_int64, [C.c_double, C.c_double, C.c_double, C.c_int64]),
+    ("gcpb_shard_range", None, [C.c_int64, C.c_int, C.c_int, i64p, i64p]),
+    ("gcpb_stratified_keep", None, [i64p, C.c_int, C.c_int, C.c_int64, i64p, i64p]),
+    ("gcpb_loss_deriv", C.c_double, [C.POINTER(gcpb_loss), C.c_double, C.c_double]),
+    ("gcpb_loss_value", C.c_double, [C.POINTER(gcpb_loss), C.c_double, C.c_double]),
+]
+
+for _name, _res, _args in SIGNATURES:
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = [s[0] for s in SIGNATURES]

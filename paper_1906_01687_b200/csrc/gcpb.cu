@@ -1,0 +1,1569 @@
+// gcpb.cu — context layer and C-ABI (include/gcpb.h).
+//
+// Owns every device buffer of one GCP problem on one GPU:
+//   factors A, gradient G, Adam moments B, C (+ rollback snapshots), all in
+//   one padded mode-major buffer each; the tensor (dense U8/F32/F64 array, or
+//   SoA int32 COO + values + sorted u64 keys + open-addressing hash); the
+//   fixed estimator sample set; the device-resident scalar state.
+// Errors are C++ exceptions internally, mapped at the boundary onto the
+// reference's exception classes (status codes, gcpb_last_error()).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gcpb.h"
+#include "gcpb_aux.cuh"
+#include "gcpb_kernels.cuh"
+
+using namespace gcpb;
+
+namespace {
+
+thread_local std::string g_global_err;
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw cuda_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw std::runtime_error(std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+}
+
+// Simple owning device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t n) {
+    if (n <= bytes && p) return;
+    reset();
+    if (n == 0) n = 16;
+    ck(cudaMalloc(&p, n), "cudaMalloc");
+    bytes = n;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+const char* loss_name(int kind) {
+  switch (kind) {
+    case GCPB_LOSS_GAUSSIAN: return "gaussian";
+    case GCPB_LOSS_POISSON: return "poisson";
+    case GCPB_LOSS_BERNOULLI_ODDS: return "bernoulli-odds";
+    case GCPB_LOSS_GAMMA: return "gamma";
+    case GCPB_LOSS_BETA_HALF: return "beta-half";
+    case GCPB_LOSS_HUBER: return "huber";
+  }
+  return "?";
+}
+
+void validate_loss(const gcpb_loss* loss) {
+  if (!loss) throw std::invalid_argument("loss: null");
+  if (loss->kind < 0 || loss->kind > 5) throw std::invalid_argument("unknown loss kind");
+  if (loss->kind == GCPB_LOSS_HUBER && !(loss->delta > 0.0))
+    throw std::invalid_argument("huber: delta must be > 0");  // loss.cpp:17-18
+}
+
+// LossFunction::check_domain (loss.cpp:42-62) on one value.
+void check_domain_value(int kind, double x) {
+  switch (kind) {
+    case GCPB_LOSS_POISSON:
+    case GCPB_LOSS_GAMMA:
+    case GCPB_LOSS_BETA_HALF:
+      if (!(x >= 0.0))
+        throw std::domain_error(std::string(loss_name(kind)) + " loss: data value " +
+                                std::to_string(x) + " out of domain (x >= 0 required)");
+      return;
+    case GCPB_LOSS_BERNOULLI_ODDS:
+      if (x != 0.0 && x != 1.0)
+        throw std::domain_error(std::string(loss_name(kind)) + " loss: data value " +
+                                std::to_string(x) + " out of domain (x in {0,1} required)");
+      return;
+    default:
+      return;
+  }
+}
+
+// SamplerKind::validate (samplers.cpp:56-67).
+void validate_sampler(const gcpb_sampler* s) {
+  if (!s) throw std::invalid_argument("sampler: null");
+  if (s->strategy == GCPB_UNIFORM) {
+    if (s->num_samples < 1) throw std::invalid_argument("uniform sampler: s must be >= 1");
+    return;
+  }
+  if (s->strategy != GCPB_STRATIFIED && s->strategy != GCPB_SEMI_STRATIFIED)
+    throw std::invalid_argument("unknown sampler strategy");
+  if (s->nonzero_samples < 0 || s->zero_samples < 0 ||
+      s->nonzero_samples + s->zero_samples < 1)
+    throw std::invalid_argument("sampler: need p, q >= 0 and p + q >= 1");
+  if (s->strategy == GCPB_STRATIFIED && !(s->oversample > 1.0))
+    throw std::invalid_argument("stratified sampler: oversample rate must be > 1");
+}
+
+std::string u128_to_string(unsigned __int128 v) {
+  if (v == 0) return "0";
+  std::string s;
+  while (v > 0) {
+    s.push_back(static_cast<char>('0' + static_cast<int>(v % 10)));
+    v /= 10;
+  }
+  std::reverse(s.begin(), s.end());
+  return s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// The context
+// ---------------------------------------------------------------------------
+struct gcpb_ctx {
+  int device = 0;
+  int dtype = GCPB_F32;
+  size_t tsize = 4;
+  int d = 0;
+  int64_t dims[kMaxModes] = {};
+  int64_t r = 0, rp = 0;
+  int vw = 4;  // elements per 16-byte chunk
+  unsigned __int128 total128 = 0;
+  bool total_fits = true;  // N < 2^64
+  uint64_t total = 0;
+  double total_d = 0.0;
+  int64_t off[kMaxModes + 1] = {};
+  int64_t nelem = 0;  // padded elements of all modes
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  DBuf A, Gr, B, C, As, Bs, Cs;
+  DBuf dstate;
+  DevState host_state{};
+  double* pinned_params = nullptr;  // pinned staging block for Adam scalars
+  bool adam_params_valid = false;
+  bool grad_zero = false;
+  bool have_snapshot = false;
+
+  // tensor
+  int tensor_kind = 0;  // 0 none, 1 dense, 2 sparse
+  int dense_storage = GCPB_STORE_F64;
+  DBuf dense;
+  int64_t nnz = 0;
+  DBuf coo, vals, keys;
+  DBuf hkeys, hvals;
+  uint64_t hmask = 0;
+  bool hash_ready = false;
+  int domain_flags = -1;  // cached domain scan of the stored data
+
+  // sharding
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+
+  // stratified zero sampler
+  DBuf zero_list, zstatus;
+  int64_t zero_cap = 0, zstatus_cap = 0;
+
+  // estimator
+  int64_t est_n = 0;
+  DBuf est_idx, est_x, est_w, est_partials, est_out;
+
+  // scratch for parity / record paths
+  DBuf s_idx, s_x, s_w, s_flag, s_m, s_y, s_aux;
+  DBuf dims_dev;
+
+  ~gcpb_ctx() {
+    if (pinned_params) {
+      cudaStreamSynchronize(stream);
+      cudaFreeHost(pinned_params);
+    }
+    if (comm) ncclCommDestroy(comm);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  DevState* dst() const { return dstate.as<DevState>(); }
+
+  void push_state() {
+    CK(cudaMemcpyAsync(dstate.p, &host_state, sizeof(DevState), cudaMemcpyHostToDevice, stream));
+  }
+  void pull_state() {
+    CK(cudaMemcpyAsync(&host_state, dstate.p, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
+    sync();
+  }
+  void check_mode(int mode) const {
+    if (mode < -1 || mode >= d) throw std::invalid_argument("mode out of range");
+  }
+  int64_t mode_elems(int mode) const {  // unpadded n_k * r (or all modes)
+    if (mode >= 0) return dims[mode] * r;
+    int64_t s = 0;
+    for (int k = 0; k < d; ++k) s += dims[k] * r;
+    return s;
+  }
+};
+
+namespace {
+
+template <typename F>
+int guard(gcpb_ctx* ctx, F&& f) {
+  std::string* err = ctx ? &ctx->err : &g_global_err;
+  try {
+    f();
+    return GCPB_OK;
+  } catch (const std::invalid_argument& e) {
+    *err = e.what();
+    return GCPB_ERR_USAGE;
+  } catch (const std::domain_error& e) {
+    *err = e.what();
+    return GCPB_ERR_DOMAIN;
+  } catch (const std::out_of_range& e) {
+    *err = e.what();
+    return GCPB_ERR_RANGE;
+  } catch (const std::logic_error& e) {
+    *err = e.what();
+    return GCPB_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    *err = e.what();
+    return GCPB_ERR_RUNTIME;
+  } catch (...) {
+    *err = "unknown error";
+    return GCPB_ERR_RUNTIME;
+  }
+}
+
+int grid_for(int64_t n, int threads, int num_sms, int per_sm = 8) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<int>(b);
+}
+
+// check_index (shape.cpp:73-85) message format.
+void check_index_host(const gcpb_ctx* c, const int64_t* idx) {
+  for (int k = 0; k < c->d; ++k) {
+    if (idx[k] < 0 || idx[k] >= c->dims[k])
+      throw std::out_of_range("index " + std::to_string(idx[k]) + " out of range [0, " +
+                              std::to_string(c->dims[k]) + ") in mode " + std::to_string(k));
+  }
+}
+
+// Host-side factor layout conversion: n_k x r double <-> padded n_k x rp T.
+template <typename T>
+void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values) {
+  const int k0 = mode < 0 ? 0 : mode, k1 = mode < 0 ? c->d : mode + 1;
+  const double* src = values;
+  for (int k = k0; k < k1; ++k) {
+    std::vector<T> host(static_cast<size_t>(c->dims[k] * c->rp), static_cast<T>(0));
+    for (int64_t i = 0; i < c->dims[k]; ++i)
+      for (int64_t j = 0; j < c->r; ++j) host[i * c->rp + j] = static_cast<T>(src[i * c->r + j]);
+    src += c->dims[k] * c->r;
+    CK(cudaMemcpyAsync(buf.as<T>() + c->off[k], host.data(), host.size() * sizeof(T),
+                       cudaMemcpyHostToDevice, c->stream));
+    c->sync();  // host vector goes out of scope
+  }
+}
+
+template <typename T>
+void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out) {
+  const int k0 = mode < 0 ? 0 : mode, k1 = mode < 0 ? c->d : mode + 1;
+  double* dst = out;
+  for (int k = k0; k < k1; ++k) {
+    std::vector<T> host(static_cast<size_t>(c->dims[k] * c->rp));
+    CK(cudaMemcpyAsync(host.data(), buf.as<T>() + c->off[k], host.size() * sizeof(T),
+                       cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    for (int64_t i = 0; i < c->dims[k]; ++i)
+      for (int64_t j = 0; j < c->r; ++j) dst[i * c->r + j] = static_cast<double>(host[i * c->rp + j]);
+    dst += c->dims[k] * c->r;
+  }
+}
+
+void upload(gcpb_ctx* c, DBuf& buf, int mode, const double* v) {
+  if (c->dtype == GCPB_F32)
+    upload_modes<float>(c, buf, mode, v);
+  else
+    upload_modes<double>(c, buf, mode, v);
+}
+void download(gcpb_ctx* c, const DBuf& buf, int mode, double* v) {
+  if (c->dtype == GCPB_F32)
+    download_modes<float>(c, buf, mode, v);
+  else
+    download_modes<double>(c, buf, mode, v);
+}
+
+void ensure_grad_zero(gcpb_ctx* c) {
+  if (!c->grad_zero) {
+    CK(cudaMemsetAsync(c->Gr.p, 0, c->nelem * c->tsize, c->stream));
+    c->grad_zero = true;
+  }
+}
+
+// Hash of the nonzero linear keys, built on first use.
+void ensure_hash(gcpb_ctx* c) {
+  if (c->tensor_kind != 2) throw std::logic_error("hash requested without a sparse tensor");
+  if (c->hash_ready) return;
+  if (c->nnz >= (int64_t{1} << 32))
+    throw std::invalid_argument("membership hash supports nnz < 2^32");
+  uint64_t buckets = 1;
+  while (buckets * 2 < static_cast<uint64_t>(c->nnz)) buckets <<= 1;  // load <= 0.5
+  if (buckets < 1) buckets = 1;
+  c->hmask = buckets - 1;
+  c->hkeys.alloc(buckets * 4 * sizeof(uint64_t));
+  c->hvals.alloc(buckets * 4 * sizeof(uint32_t));
+  CK(cudaMemsetAsync(c->hkeys.p, 0xFF, buckets * 4 * sizeof(uint64_t), c->stream));
+  if (c->nnz > 0) {
+    hash_build_kernel<<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
+        c->keys.as<uint64_t>(), c->nnz, c->hkeys.as<unsigned long long>(),
+        c->hvals.as<uint32_t>(), c->hmask);
+    CK(cudaGetLastError());
+  }
+  c->hash_ready = true;
+}
+
+// Data-domain scan (cached) -> domain_error like LossFunction::check_domain.
+void check_data_domain(gcpb_ctx* c, int loss_kind) {
+  if (loss_kind == GCPB_LOSS_GAUSSIAN || loss_kind == GCPB_LOSS_HUBER) return;
+  if (c->tensor_kind == 0) return;
+  if (c->domain_flags < 0) {
+    c->s_aux.alloc(16);
+    CK(cudaMemsetAsync(c->s_aux.p, 0, 4, c->stream));
+    unsigned* f = c->s_aux.as<unsigned>();
+    if (c->tensor_kind == 2) {
+      if (c->nnz > 0) {
+        if (c->dtype == GCPB_F32)
+          domain_scan_kernel<float><<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
+              c->vals.as<float>(), c->nnz, f);
+        else
+          domain_scan_kernel<double><<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
+              c->vals.as<double>(), c->nnz, f);
+      }
+    } else {
+      const int64_t n = static_cast<int64_t>(c->total);
+      if (c->dense_storage == GCPB_STORE_U8)
+        domain_scan_kernel<uint8_t><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
+            c->dense.as<uint8_t>(), n, f);
+      else if (c->dense_storage == GCPB_STORE_F32)
+        domain_scan_kernel<float><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
+            c->dense.as<float>(), n, f);
+      else
+        domain_scan_kernel<double><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
+            c->dense.as<double>(), n, f);
+    }
+    CK(cudaGetLastError());
+    unsigned flags = 0;
+    CK(cudaMemcpyAsync(&flags, f, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    c->domain_flags = static_cast<int>(flags);
+  }
+  const int f = c->domain_flags;
+  if (loss_kind == GCPB_LOSS_BERNOULLI_ODDS && (f & 6))
+    throw std::domain_error(std::string(loss_name(loss_kind)) +
+                            " loss: data value out of domain (x in {0,1} required)");
+  if ((loss_kind == GCPB_LOSS_POISSON || loss_kind == GCPB_LOSS_GAMMA ||
+       loss_kind == GCPB_LOSS_BETA_HALF) &&
+      (f & 5))
+    throw std::domain_error(std::string(loss_name(loss_kind)) +
+                            " loss: data value out of domain (x >= 0 required)");
+}
+
+template <typename T>
+FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64_t iter) {
+  FusedArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.A = c->A.as<T>();
+  a.G = c->Gr.as<T>();
+  a.d = c->d;
+  a.rp = static_cast<int>(c->rp);
+  a.nchunks = static_cast<int>((c->r + c->vw - 1) / c->vw);
+  a.loss = loss ? loss->kind : 0;
+  a.delta = static_cast<T>(loss ? loss->delta : 0.0);
+  uint64_t stride = 1;
+  for (int k = 0; k < c->d; ++k) {
+    a.off[k] = c->off[k];
+    a.dims[k] = static_cast<uint32_t>(c->dims[k]);
+    a.thr[k] = lemire_threshold32(static_cast<uint64_t>(c->dims[k]));
+    a.stride[k] = stride;
+    stride *= static_cast<uint64_t>(c->dims[k]);
+  }
+  a.seed = seed;
+  a.iter = iter;
+  if (c->tensor_kind == 1) {
+    a.xkind = c->dense_storage == GCPB_STORE_U8
+                  ? X_DENSE_U8
+                  : (c->dense_storage == GCPB_STORE_F32 ? X_DENSE_F32 : X_DENSE_F64);
+    a.dense = c->dense.p;
+  } else if (c->tensor_kind == 2) {
+    a.xkind = X_SPARSE;
+    a.coo = c->coo.as<int32_t>();
+    a.coo_stride = c->nnz;
+    a.vals = c->vals.as<T>();
+    a.eta = static_cast<uint64_t>(c->nnz);
+    a.thr_eta = c->nnz > 0 && static_cast<uint64_t>(c->nnz) <= (1ull << 32)
+                    ? lemire_threshold32(static_cast<uint64_t>(c->nnz))
+                    : 0u;
+    a.nz_begin = 0;
+    a.nz_end = c->nnz;
+    if (c->hash_ready) {
+      a.hkeys = c->hkeys.as<uint64_t>();
+      a.hvals = c->hvals.as<uint32_t>();
+      a.hmask = c->hmask;
+    }
+  }
+  a.scatter = 1;
+  return a;
+}
+
+template <typename T>
+int64_t finish_segments(FusedArgs<T>& a) {
+  int64_t tiles = 0;
+  for (int s = 0; s < a.nseg; ++s) {
+    a.seg[s].tiles_begin = tiles;
+    const int64_t len = a.seg[s].t_end - a.seg[s].t_begin;
+    tiles += len > 0 ? (len + 31) / 32 : 0;
+  }
+  return tiles;
+}
+
+template <typename T>
+void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record) {
+  const int64_t tiles = finish_segments(a);
+  CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms));
+}
+
+Seg make_seg(int kind, uint32_t tag, int64_t tb, int64_t te, double w, int flag, int64_t out) {
+  Seg s;
+  std::memset(&s, 0, sizeof(s));
+  s.kind = kind;
+  s.tag = tag;
+  s.t_begin = tb;
+  s.t_end = te;
+  s.weight = w;
+  s.flag = flag;
+  s.out_offset = out;
+  return s;
+}
+
+// Runs the stratified zero sampler for q accepts: fills zero_list[0..q) with
+// candidate ordinals.  host_check: synchronise and continue host-side until
+// exactly q accepts exist (reference semantics for any q); otherwise three
+// device-planned batches are queued without a host round trip.
+void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
+                      uint32_t tag, bool host_check) {
+  ensure_hash(c);
+  const double zeta = static_cast<double>(c->total128 - static_cast<unsigned __int128>(c->nnz));
+  const int64_t first_batch = zero_batch_size_dev(c->total_d, zeta, rho, q);
+  const int64_t nchunks = (first_batch + kZcChunk - 1) / kZcChunk;
+  if (c->zero_cap < q) {
+    c->zero_list.alloc(static_cast<size_t>(q) * sizeof(uint64_t));
+    c->zero_cap = q;
+  }
+  if (c->zstatus_cap < nchunks) {
+    c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
+    c->zstatus_cap = nchunks;
+  }
+  // Look-back words from earlier calls must not alias this call's batch tags.
+  CK(cudaMemsetAsync(c->zstatus.p, 0, static_cast<size_t>(std::max<int64_t>(nchunks, 1)) * 8,
+                     c->stream));
+  // Scalar inputs of the plan kernel.
+  DevState* st = c->dst();
+  c->host_state.z_q = q;
+  c->host_state.z_total = c->total_d;
+  c->host_state.z_zeta = zeta;
+  c->host_state.z_rho = rho;
+  c->host_state.z_status_cap = c->zstatus_cap;
+  CK(cudaMemcpyAsync(&st->z_q, &c->host_state.z_q, sizeof(int64_t), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(&st->z_total, &c->host_state.z_total, 3 * sizeof(double),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&st->z_status_cap, &c->host_state.z_status_cap, sizeof(int64_t),
+                     cudaMemcpyHostToDevice, c->stream));
+  ZeroArgs za;
+  std::memset(&za, 0, sizeof(za));
+  za.d = c->d;
+  uint64_t stride = 1;
+  for (int k = 0; k < c->d; ++k) {
+    za.dims[k] = static_cast<uint32_t>(c->dims[k]);
+    za.thr[k] = lemire_threshold32(static_cast<uint64_t>(c->dims[k]));
+    za.stride[k] = stride;
+    stride *= static_cast<uint64_t>(c->dims[k]);
+  }
+  za.seed = seed;
+  za.iter = iter;
+  za.tag = tag;
+  za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
+  za.hmask = c->hmask;
+  za.st = st;
+  za.status = c->zstatus.as<unsigned long long>();
+  za.zero_list = c->zero_list.as<uint64_t>();
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
+  for (int b = 0; b < 3; ++b) {
+    zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, b == 0 ? 1 : 0);
+    zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+  }
+  CK(cudaGetLastError());
+  if (!host_check) return;
+  for (;;) {
+    c->pull_state();
+    if (c->host_state.z_overflow) throw std::logic_error("zero sampler: status overflow");
+    if (std::min(c->host_state.z_accepted, q) >= q) break;
+    zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, 0);
+    zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    CK(cudaGetLastError());
+  }
+}
+
+struct SampleResult {
+  int64_t n = 0;
+  gcpb_stats stats{0, 0, 0};
+};
+
+// The fused sample -> eval -> MTTKRP (and/or record) for one sampler call.
+template <typename T>
+SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss,
+                             uint64_t seed, uint64_t iter, bool scatter, bool record,
+                             bool host_check, bool estimator_tags, int est_kind) {
+  SampleResult res;
+  FusedArgs<T> a = base_args<T>(c, loss, seed, iter);
+  a.scatter = scatter ? 1 : 0;
+  if (record) {
+    a.r_idx = c->s_idx.as<int64_t>();
+    a.r_x = c->s_x.as<double>();
+    a.r_w = c->s_w.as<double>();
+    a.r_flag = c->s_flag.as<int32_t>();
+    a.r_m = c->s_m.as<double>();
+    a.r_y = c->s_y.as<double>();
+  }
+  const uint32_t tag_u = estimator_tags ? TAG_EST_UNIFORM : TAG_GRAD_UNIFORM;
+  const uint32_t tag_p = estimator_tags ? TAG_EST_NZ_PICK : TAG_GRAD_NZ_PICK;
+  const uint32_t tag_z = estimator_tags ? TAG_EST_ZERO_CAND : TAG_GRAD_ZERO_CAND;
+  int64_t b0 = 0, b1 = 0;
+  if (sk->strategy == GCPB_UNIFORM) {
+    const int64_t s = sk->num_samples;
+    gcpb_shard_range(s, c->rank, c->nranks, &b0, &b1);
+    const double w = c->total_d / static_cast<double>(s);  // samplers.hpp:83
+    a.nseg = 1;
+    a.seg[0] = make_seg(SEG_UNIFORM, tag_u, b0, b1, w, 0, 0);
+    if (c->tensor_kind == 2) ensure_hash(c), a.hkeys = c->hkeys.as<uint64_t>(),
+                             a.hvals = c->hvals.as<uint32_t>(), a.hmask = c->hmask;
+    res.n = s;
+    run_fused(c, a, record);
+    return res;
+  }
+  // stratified / semi-stratified (samplers.hpp:141-219), estimator split
+  // (samplers.hpp:283-315) when est_kind >= 0.
+  int64_t p = sk->nonzero_samples, q = sk->zero_samples;
+  const int64_t eta = c->nnz;
+  const unsigned __int128 zeta128 = c->total128 - static_cast<unsigned __int128>(eta);
+  if (eta == 0 && p > 0) {
+    q += p;
+    p = 0;
+  }
+  if (est_kind >= 0 && zeta128 == 0) {
+    p += q;
+    q = 0;
+  }
+  const double eta_over_p = p > 0 ? static_cast<double>(eta) / static_cast<double>(p) : 0.0;
+  const bool strat = sk->strategy == GCPB_STRATIFIED;
+  if (strat && q > 0) {
+    if (zeta128 < static_cast<unsigned __int128>(q))
+      throw std::invalid_argument("sample_zeros_rejection: requested " + std::to_string(q) +
+                                  " zeros but only " + u128_to_string(zeta128) + " exist");
+    if (c->nranks > 1) throw std::invalid_argument("stratified sampling is single-rank in v1");
+    run_zero_sampler(c, q, sk->oversample, seed, iter, tag_z, host_check);
+    a.zero_list = c->zero_list.as<uint64_t>();
+  }
+  a.nseg = 0;
+  if (p > 0) {
+    gcpb_shard_range(p, c->rank, c->nranks, &b0, &b1);
+    a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p,
+                               (!strat && est_kind < 0) ? 1 : 0, 0);
+  }
+  if (q > 0) {
+    const double zeta_d = static_cast<double>(zeta128);
+    if (strat) {
+      a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, tag_z, 0, q, zeta_d / static_cast<double>(q), 0, p);
+    } else {
+      gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
+      a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1,
+                                 c->total_d / static_cast<double>(q), 0, p);
+    }
+  }
+  res.n = p + q;
+  run_fused(c, a, record);
+  if (strat && q > 0 && host_check) {
+    res.stats.tested = c->host_state.z_tested;
+    res.stats.accepted = c->host_state.z_accepted;
+    res.stats.rejected = c->host_state.z_rejected;
+  }
+  return res;
+}
+
+void alloc_record(gcpb_ctx* c, int64_t n) {
+  const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+  c->s_idx.alloc(nn * c->d * sizeof(int64_t));
+  c->s_x.alloc(nn * sizeof(double));
+  c->s_w.alloc(nn * sizeof(double));
+  c->s_flag.alloc(nn * sizeof(int32_t));
+  c->s_m.alloc(nn * sizeof(double));
+  c->s_y.alloc(nn * sizeof(double));
+}
+
+int64_t expected_samples(const gcpb_ctx* c, const gcpb_sampler* s) {
+  if (s->strategy == GCPB_UNIFORM) return s->num_samples;
+  return s->nonzero_samples + s->zero_samples;
+  (void)c;
+}
+
+template <typename T>
+void adam_launch(gcpb_ctx* c) {
+  const int grid = grid_for(c->nelem, 256, c->num_sms, 4);
+  adam_kernel<T><<<grid, 256, 0, c->stream>>>(c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(),
+                                               c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
+                                               static_cast<int>(c->r), c->dst());
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void estimate_launch(gcpb_ctx* c, const gcpb_loss* loss) {
+  ModelDesc<T> md;
+  std::memset(&md, 0, sizeof(md));
+  md.A = c->A.as<T>();
+  md.d = c->d;
+  md.rp = static_cast<int>(c->rp);
+  md.r = static_cast<int>(c->r);
+  for (int k = 0; k < c->d; ++k) md.off[k] = c->off[k];
+  constexpr int kGrid = 296;  // fixed => bit-deterministic summation order
+  c->est_partials.alloc(kGrid * sizeof(double));
+  c->est_out.alloc(sizeof(double));
+  estimate_partial_kernel<T><<<kGrid, 256, 0, c->stream>>>(
+      md, c->est_idx.as<int64_t>(), c->est_x.as<double>(), c->est_w.as<double>(), c->est_n,
+      loss->kind, loss->delta, c->est_partials.as<double>());
+  sum_partials_kernel<<<1, 32, 0, c->stream>>>(c->est_partials.as<double>(), kGrid,
+                                                c->est_out.as<double>());
+  CK(cudaGetLastError());
+}
+
+void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
+                           const std::vector<double>& values) {
+  const int64_t n = static_cast<int64_t>(keys.size());
+  c->nnz = n;
+  c->tensor_kind = 2;
+  c->hash_ready = false;
+  c->domain_flags = -1;
+  c->dense.reset();
+  const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+  c->keys.alloc(nn * sizeof(uint64_t));
+  c->coo.alloc(nn * c->d * sizeof(int32_t));
+  c->vals.alloc(nn * c->tsize);
+  std::vector<int32_t> coo(nn * c->d);
+  for (int64_t e = 0; e < n; ++e) {
+    uint64_t rem = keys[e];
+    for (int k = 0; k < c->d; ++k) {
+      coo[k * n + e] = static_cast<int32_t>(rem % static_cast<uint64_t>(c->dims[k]));
+      rem /= static_cast<uint64_t>(c->dims[k]);
+    }
+  }
+  if (n > 0) {
+    CK(cudaMemcpyAsync(c->keys.p, keys.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(c->coo.p, coo.data(), n * c->d * sizeof(int32_t), cudaMemcpyHostToDevice,
+                       c->stream));
+    if (c->dtype == GCPB_F32) {
+      std::vector<float> v(values.begin(), values.end());
+      CK(cudaMemcpyAsync(c->vals.p, v.data(), n * sizeof(float), cudaMemcpyHostToDevice,
+                         c->stream));
+      c->sync();
+    } else {
+      CK(cudaMemcpyAsync(c->vals.p, values.data(), n * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+    }
+  }
+  c->sync();
+}
+
+}  // namespace
+
+namespace {
+template <typename T>
+void given_launch(gcpb_ctx* c, int64_t n, const gcpb_loss* loss, bool y_given, bool record,
+                  bool scatter) {
+  FusedArgs<T> a = base_args<T>(c, loss, 0, 0);
+  a.scatter = scatter ? 1 : 0;
+  a.g_idx = c->s_idx.as<int64_t>();
+  if (y_given) {
+    a.g_y = c->s_y.as<double>();
+  } else {
+    a.g_x = c->s_x.as<double>();
+    a.g_w = c->s_w.as<double>();
+    a.g_flag = c->s_flag.as<int32_t>();
+  }
+  if (record) {
+    a.r_m = c->s_m.as<double>();
+    a.r_y = c->s_aux.as<double>();
+  }
+  a.nseg = 1;
+  a.seg[0] = make_seg(SEG_GIVEN, 0, 0, n, 0.0, 0, 0);
+  run_fused(c, a, record);
+}
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* gcpb_version(void) { return "gcpb 0.1 (sm_100a)"; }
+
+const char* gcpb_last_error(const gcpb_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_global_err.c_str();
+}
+
+int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t rank,
+                gcpb_ctx** out) {
+  return guard(nullptr, [&] {
+    if (!out) throw std::invalid_argument("gcpb_create: null output");
+    *out = nullptr;
+    if (dtype != GCPB_F32 && dtype != GCPB_F64) throw std::invalid_argument("dtype must be F32 or F64");
+    if (ndims < 1) throw std::invalid_argument("Shape: need at least one mode");
+    if (ndims > kMaxModes) throw std::invalid_argument("Shape: at most 16 modes supported");
+    if (rank < 1) throw std::invalid_argument("kruskal model: rank must be >= 1");
+    auto c = std::make_unique<gcpb_ctx>();
+    c->device = device;
+    c->dtype = dtype;
+    c->tsize = dtype == GCPB_F32 ? 4 : 8;
+    c->vw = dtype == GCPB_F32 ? 4 : 2;
+    c->d = ndims;
+    c->r = rank;
+    const int64_t pad = dtype == GCPB_F32 ? 8 : 4;  // 32-byte rows
+    c->rp = (rank + pad - 1) / pad * pad;
+    if (c->rp / c->vw > 32 * 8) throw std::invalid_argument("rank too large for the device path (r <= 1024 fp32 / 512 fp64)");
+    unsigned __int128 total = 1;
+    const unsigned __int128 maxv = ~static_cast<unsigned __int128>(0);
+    for (int k = 0; k < ndims; ++k) {
+      if (dims[k] < 1) throw std::invalid_argument("Shape: every extent must be positive");
+      if (dims[k] >= (int64_t{1} << 31))
+        throw std::invalid_argument("device path supports extents < 2^31");
+      if (total > maxv / static_cast<unsigned __int128>(dims[k]))
+        throw std::invalid_argument("Shape: total entry count overflows 128 bits");
+      total *= static_cast<unsigned __int128>(dims[k]);
+      c->dims[k] = dims[k];
+    }
+    c->total128 = total;
+    c->total_fits = total <= static_cast<unsigned __int128>(UINT64_MAX);
+    c->total = c->total_fits ? static_cast<uint64_t>(total) : 0;
+    c->total_d = static_cast<double>(total);
+    int64_t o = 0;
+    for (int k = 0; k < ndims; ++k) {
+      c->off[k] = o;
+      o += c->dims[k] * c->rp;
+    }
+    c->off[ndims] = o;
+    c->nelem = o;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    const size_t bytes = static_cast<size_t>(c->nelem) * c->tsize;
+    DBuf* bufs[4] = {&c->A, &c->Gr, &c->B, &c->C};
+    for (DBuf* b : bufs) {
+      b->alloc(bytes);
+      CK(cudaMemsetAsync(b->p, 0, bytes, c->stream));
+    }
+    c->grad_zero = true;
+    c->dstate.alloc(sizeof(DevState));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->pinned_params), 8 * sizeof(double)));
+    std::memset(&c->host_state, 0, sizeof(DevState));
+    c->host_state.lr = 1e-3;
+    c->host_state.beta1 = 0.9;
+    c->host_state.beta2 = 0.999;
+    c->host_state.eps = 1e-8;
+    c->push_state();
+    c->dims_dev.alloc(kMaxModes * sizeof(int64_t));
+    CK(cudaMemcpyAsync(c->dims_dev.p, c->dims, kMaxModes * sizeof(int64_t), cudaMemcpyHostToDevice,
+                       c->stream));
+    c->sync();
+    *out = c.release();
+  });
+}
+
+void gcpb_destroy(gcpb_ctx* ctx) { delete ctx; }
+
+int gcpb_set_stream(gcpb_ctx* ctx, void* stream) {
+  return guard(ctx, [&] {
+    ctx->sync();
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+void* gcpb_get_stream(gcpb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+// ---- tensor data -------------------------------------------------------------------
+int gcpb_set_sparse(gcpb_ctx* ctx, int64_t nnz, const int64_t* coords, const double* values) {
+  return guard(ctx, [&] {
+    if (nnz < 0) throw std::invalid_argument("sparse tensor: negative nnz");
+    if (!ctx->total_fits) throw std::invalid_argument("sparse tensor: N >= 2^64 unsupported (u64 keys)");
+    const int d = ctx->d;
+    std::vector<std::pair<uint64_t, double>> entries(static_cast<size_t>(nnz));
+    for (int64_t e = 0; e < nnz; ++e) {
+      check_index_host(ctx, coords + e * d);  // tensor.cpp:21
+      uint64_t lin = 0, stride = 1;
+      for (int k = 0; k < d; ++k) {
+        lin += static_cast<uint64_t>(coords[e * d + k]) * stride;
+        stride *= static_cast<uint64_t>(ctx->dims[k]);
+      }
+      entries[e] = {lin, values[e]};
+    }
+    std::stable_sort(entries.begin(), entries.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<uint64_t> keys;
+    std::vector<double> vals;
+    keys.reserve(entries.size());
+    vals.reserve(entries.size());
+    size_t e = 0;
+    while (e < entries.size()) {  // tensor.cpp:30-40: sum duplicates, drop zeros
+      const uint64_t key = entries[e].first;
+      double sum = 0.0;
+      while (e < entries.size() && entries[e].first == key) sum += entries[e++].second;
+      if (sum == 0.0) continue;
+      keys.push_back(key);
+      vals.push_back(sum);
+    }
+    set_sparse_normalized(ctx, keys, vals);
+  });
+}
+
+int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_sorted,
+                           const void* d_values, int value_dtype) {
+  return guard(ctx, [&] {
+    if (nnz < 0) throw std::invalid_argument("sparse tensor: negative nnz");
+    if (!ctx->total_fits) throw std::invalid_argument("sparse tensor: N >= 2^64 unsupported (u64 keys)");
+    if (value_dtype != GCPB_F32 && value_dtype != GCPB_F64)
+      throw std::invalid_argument("value dtype must be F32 or F64");
+    ctx->nnz = nnz;
+    ctx->tensor_kind = 2;
+    ctx->hash_ready = false;
+    ctx->domain_flags = -1;
+    ctx->dense.reset();
+    const size_t nn = static_cast<size_t>(std::max<int64_t>(nnz, 1));
+    ctx->keys.alloc(nn * sizeof(uint64_t));
+    ctx->coo.alloc(nn * ctx->d * sizeof(int32_t));
+    ctx->vals.alloc(nn * ctx->tsize);
+    if (nnz > 0) {
+      CK(cudaMemcpyAsync(ctx->keys.p, d_keys_sorted, nnz * sizeof(uint64_t),
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+      ctx->s_aux.alloc(16);
+      CK(cudaMemsetAsync(ctx->s_aux.p, 0, 4, ctx->stream));
+      const int g = grid_for(nnz, 256, ctx->num_sms);
+      if (value_dtype == GCPB_F32)
+        check_keys_kernel<float><<<g, 256, 0, ctx->stream>>>(
+            ctx->keys.as<uint64_t>(), static_cast<const float*>(d_values), nnz, ctx->total,
+            ctx->s_aux.as<unsigned>());
+      else
+        check_keys_kernel<double><<<g, 256, 0, ctx->stream>>>(
+            ctx->keys.as<uint64_t>(), static_cast<const double*>(d_values), nnz, ctx->total,
+            ctx->s_aux.as<unsigned>());
+      unsigned flags = 0;
+      CK(cudaMemcpyAsync(&flags, ctx->s_aux.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      if (flags & 1u) throw std::out_of_range("sparse tensor: linear key out of range");
+      if (flags & 2u) throw std::invalid_argument("device ingest requires strictly increasing keys");
+      if (flags & 4u) throw std::invalid_argument("device ingest requires nonzero values");
+      keys_to_coo_kernel<<<g, 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), nnz, ctx->d,
+                                                     ctx->dims_dev.as<int64_t>(),
+                                                     ctx->coo.as<int32_t>());
+      if (ctx->dtype == GCPB_F32) {
+        if (value_dtype == GCPB_F32)
+          convert_kernel<float, float><<<g, 256, 0, ctx->stream>>>(
+              static_cast<const float*>(d_values), ctx->vals.as<float>(), nnz);
+        else
+          convert_kernel<double, float><<<g, 256, 0, ctx->stream>>>(
+              static_cast<const double*>(d_values), ctx->vals.as<float>(), nnz);
+      } else {
+        if (value_dtype == GCPB_F32)
+          convert_kernel<float, double><<<g, 256, 0, ctx->stream>>>(
+              static_cast<const float*>(d_values), ctx->vals.as<double>(), nnz);
+        else
+          convert_kernel<double, double><<<g, 256, 0, ctx->stream>>>(
+              static_cast<const double*>(d_values), ctx->vals.as<double>(), nnz);
+      }
+      CK(cudaGetLastError());
+    }
+    ctx->sync();
+  });
+}
+
+int64_t gcpb_nnz(const gcpb_ctx* ctx) { return ctx ? ctx->nnz : 0; }
+
+int gcpb_get_sparse(gcpb_ctx* ctx, int64_t* coords_out, double* values_out) {
+  return guard(ctx, [&] {
+    if (ctx->tensor_kind != 2) throw std::invalid_argument("no sparse tensor set");
+    const int64_t n = ctx->nnz;
+    std::vector<uint64_t> keys(static_cast<size_t>(n));
+    if (n > 0)
+      CK(cudaMemcpyAsync(keys.data(), ctx->keys.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<double> v(static_cast<size_t>(n));
+    if (ctx->dtype == GCPB_F32) {
+      std::vector<float> f(static_cast<size_t>(n));
+      if (n > 0)
+        CK(cudaMemcpyAsync(f.data(), ctx->vals.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      for (int64_t e = 0; e < n; ++e) v[e] = f[e];
+    } else {
+      if (n > 0)
+        CK(cudaMemcpyAsync(v.data(), ctx->vals.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+    }
+    for (int64_t e = 0; e < n; ++e) {
+      uint64_t rem = keys[e];
+      for (int k = 0; k < ctx->d; ++k) {
+        coords_out[e * ctx->d + k] = static_cast<int64_t>(rem % static_cast<uint64_t>(ctx->dims[k]));
+        rem /= static_cast<uint64_t>(ctx->dims[k]);
+      }
+      values_out[e] = v[e];
+    }
+  });
+}
+
+int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage) {
+  return guard(ctx, [&] {
+    if (!ctx->total_fits || ctx->total > (uint64_t{1} << 40))
+      throw std::invalid_argument("dense tensor too large to materialize");
+    const uint64_t n = ctx->total;
+    size_t es = storage == GCPB_STORE_U8 ? 1 : (storage == GCPB_STORE_F32 ? 4 : 8);
+    if (storage < 0 || storage > 2) throw std::invalid_argument("unknown dense storage");
+    std::vector<unsigned char> host(n * es);
+    for (uint64_t i = 0; i < n; ++i) {
+      const double v = values[i];
+      if (storage == GCPB_STORE_U8) {
+        if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v)))
+          throw std::invalid_argument("U8 dense storage needs integers in [0, 255]");
+        host[i] = static_cast<unsigned char>(v);
+      } else if (storage == GCPB_STORE_F32) {
+        const float f = static_cast<float>(v);
+        std::memcpy(&host[i * 4], &f, 4);
+      } else {
+        std::memcpy(&host[i * 8], &v, 8);
+      }
+    }
+    ctx->dense.alloc(n * es);
+    CK(cudaMemcpyAsync(ctx->dense.p, host.data(), n * es, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+    ctx->dense_storage = storage;
+    ctx->tensor_kind = 1;
+    ctx->nnz = 0;
+    ctx->domain_flags = -1;
+  });
+}
+
+int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage) {
+  return guard(ctx, [&] {
+    if (!ctx->total_fits) throw std::invalid_argument("dense tensor too large to materialize");
+    if (storage < 0 || storage > 2) throw std::invalid_argument("unknown dense storage");
+    const size_t es = storage == GCPB_STORE_U8 ? 1 : (storage == GCPB_STORE_F32 ? 4 : 8);
+    ctx->dense.alloc(ctx->total * es);
+    CK(cudaMemcpyAsync(ctx->dense.p, d_values, ctx->total * es, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    ctx->sync();
+    ctx->dense_storage = storage;
+    ctx->tensor_kind = 1;
+    ctx->nnz = 0;
+    ctx->domain_flags = -1;
+  });
+}
+
+int gcpb_generate_dense_bernoulli(gcpb_ctx* ctx, int64_t true_rank, const double* true_factors,
+                                  uint64_t seed) {
+  return guard(ctx, [&] {
+    if (!ctx->total_fits) throw std::invalid_argument("dense tensor too large to materialize");
+    if (true_rank < 1 || true_rank > 1024) throw std::invalid_argument("true rank out of range");
+    int64_t foff[kMaxModes] = {};
+    int64_t tot = 0;
+    for (int k = 0; k < ctx->d; ++k) {
+      foff[k] = tot;
+      tot += ctx->dims[k] * true_rank;
+    }
+    DBuf F, fo;
+    F.alloc(tot * sizeof(double));
+    fo.alloc(kMaxModes * sizeof(int64_t));
+    CK(cudaMemcpyAsync(F.p, true_factors, tot * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(fo.p, foff, sizeof(foff), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->dense.alloc(ctx->total);
+    const int64_t nfibers = static_cast<int64_t>(ctx->total / static_cast<uint64_t>(ctx->dims[0]));
+    const size_t smem = 8 * true_rank * sizeof(double);
+    gen_bernoulli_kernel<<<grid_for(nfibers * 32, 256, ctx->num_sms, 8), 256, smem, ctx->stream>>>(
+        ctx->dense.as<uint8_t>(), ctx->d, ctx->dims_dev.as<int64_t>(), fo.as<int64_t>(),
+        static_cast<int>(true_rank), F.as<double>(), seed, nfibers);
+    CK(cudaGetLastError());
+    ctx->sync();
+    ctx->dense_storage = GCPB_STORE_U8;
+    ctx->tensor_kind = 1;
+    ctx->nnz = 0;
+    ctx->domain_flags = -1;
+  });
+}
+
+int gcpb_tensor_norm(gcpb_ctx* ctx, double* out) {
+  return guard(ctx, [&] {
+    if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+    constexpr int kGrid = 592;
+    ctx->est_partials.alloc(kGrid * sizeof(double));
+    ctx->est_out.alloc(sizeof(double));
+    double* parts = ctx->est_partials.as<double>();
+    if (ctx->tensor_kind == 2) {
+      if (ctx->dtype == GCPB_F32)
+        sumsq_kernel<float><<<kGrid, 256, 0, ctx->stream>>>(ctx->vals.as<float>(), ctx->nnz, parts);
+      else
+        sumsq_kernel<double><<<kGrid, 256, 0, ctx->stream>>>(ctx->vals.as<double>(), ctx->nnz, parts);
+    } else {
+      const int64_t n = static_cast<int64_t>(ctx->total);
+      if (ctx->dense_storage == GCPB_STORE_U8)
+        sumsq_kernel<uint8_t><<<kGrid, 256, 0, ctx->stream>>>(ctx->dense.as<uint8_t>(), n, parts);
+      else if (ctx->dense_storage == GCPB_STORE_F32)
+        sumsq_kernel<float><<<kGrid, 256, 0, ctx->stream>>>(ctx->dense.as<float>(), n, parts);
+      else
+        sumsq_kernel<double><<<kGrid, 256, 0, ctx->stream>>>(ctx->dense.as<double>(), n, parts);
+    }
+    sum_partials_kernel<<<1, 32, 0, ctx->stream>>>(parts, kGrid, ctx->est_out.as<double>());
+    CK(cudaGetLastError());
+    double ss = 0.0;
+    CK(cudaMemcpyAsync(&ss, ctx->est_out.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    *out = std::sqrt(ss);
+  });
+}
+
+int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out) {
+  return guard(ctx, [&] {
+    if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+    for (int64_t e = 0; e < n; ++e) check_index_host(ctx, idx + e * ctx->d);
+    if (n == 0) return;
+    // Gathered with the same device access path the sampler uses: a GIVEN
+    // segment cannot look x up, so use a tiny uniform-free path: record x by
+    // evaluating a gaussian derivative with w = 0 would lose x; instead do a
+    // direct host-mirrored lookup on the device copy.
+    std::vector<uint64_t> lin(static_cast<size_t>(n));
+    for (int64_t e = 0; e < n; ++e) {
+      uint64_t l = 0, s = 1;
+      for (int k = 0; k < ctx->d; ++k) {
+        l += static_cast<uint64_t>(idx[e * ctx->d + k]) * s;
+        s *= static_cast<uint64_t>(ctx->dims[k]);
+      }
+      lin[e] = l;
+    }
+    if (ctx->tensor_kind == 1) {
+      const size_t es = ctx->dense_storage == GCPB_STORE_U8 ? 1 : (ctx->dense_storage == GCPB_STORE_F32 ? 4 : 8);
+      for (int64_t e = 0; e < n; ++e) {
+        unsigned char buf[8] = {};
+        CK(cudaMemcpyAsync(buf, ctx->dense.as<unsigned char>() + lin[e] * es, es,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        if (es == 1) x_out[e] = buf[0];
+        else if (es == 4) { float f; std::memcpy(&f, buf, 4); x_out[e] = f; }
+        else std::memcpy(&x_out[e], buf, 8);
+      }
+      return;
+    }
+    std::vector<uint64_t> keys(static_cast<size_t>(ctx->nnz));
+    if (ctx->nnz > 0)
+      CK(cudaMemcpyAsync(keys.data(), ctx->keys.p, ctx->nnz * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int64_t e = 0; e < n; ++e) {
+      const auto it = std::lower_bound(keys.begin(), keys.end(), lin[e]);
+      if (it == keys.end() || *it != lin[e]) {
+        x_out[e] = 0.0;
+        continue;
+      }
+      const int64_t pos = it - keys.begin();
+      if (ctx->dtype == GCPB_F32) {
+        float f;
+        CK(cudaMemcpyAsync(&f, ctx->vals.as<float>() + pos, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        x_out[e] = f;
+      } else {
+        CK(cudaMemcpyAsync(&x_out[e], ctx->vals.as<double>() + pos, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+      }
+    }
+  });
+}
+
+// ---- factors / gradient / moments -----------------------------------------------------
+int gcpb_set_factors(gcpb_ctx* ctx, int mode, const double* values) {
+  return guard(ctx, [&] {
+    ctx->check_mode(mode);
+    upload(ctx, ctx->A, mode, values);
+  });
+}
+int gcpb_get_factors(gcpb_ctx* ctx, int mode, double* out) {
+  return guard(ctx, [&] {
+    ctx->check_mode(mode);
+    download(ctx, ctx->A, mode, out);
+  });
+}
+int gcpb_get_grad(gcpb_ctx* ctx, int mode, double* out) {
+  return guard(ctx, [&] {
+    ctx->check_mode(mode);
+    download(ctx, ctx->Gr, mode, out);
+  });
+}
+int gcpb_set_grad(gcpb_ctx* ctx, int mode, const double* values) {
+  return guard(ctx, [&] {
+    ctx->check_mode(mode);
+    upload(ctx, ctx->Gr, mode, values);
+    ctx->grad_zero = false;
+  });
+}
+int gcpb_get_moment(gcpb_ctx* ctx, int which, int mode, double* out) {
+  return guard(ctx, [&] {
+    ctx->check_mode(mode);
+    if (which != 0 && which != 1) throw std::invalid_argument("moment must be 0 or 1");
+    download(ctx, which == 0 ? ctx->B : ctx->C, mode, out);
+  });
+}
+int gcpb_set_moment(gcpb_ctx* ctx, int which, int mode, const double* values) {
+  return guard(ctx, [&] {
+    ctx->check_mode(mode);
+    if (which != 0 && which != 1) throw std::invalid_argument("moment must be 0 or 1");
+    upload(ctx, which == 0 ? ctx->B : ctx->C, mode, values);
+  });
+}
+
+// ---- hot path ---------------------------------------------------------------------------
+int gcpb_stoch_grad(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                    uint64_t seed, uint64_t iter, gcpb_stats* stats) {
+  return guard(ctx, [&] {
+    validate_sampler(sampler);
+    validate_loss(loss);
+    if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+    if (sampler->strategy != GCPB_UNIFORM && ctx->tensor_kind != 2)
+      throw std::invalid_argument(sampler->strategy == GCPB_STRATIFIED
+                                      ? "stratified sampling requires a sparse tensor"
+                                      : "semi-stratified sampling requires a sparse tensor");
+    check_data_domain(ctx, loss->kind);
+    ensure_grad_zero(ctx);
+    const bool want_stats = stats != nullptr;
+    SampleResult res;
+    if (ctx->dtype == GCPB_F32)
+      res = stoch_grad_impl<float>(ctx, sampler, loss, seed, iter, true, false, want_stats, false, -1);
+    else
+      res = stoch_grad_impl<double>(ctx, sampler, loss, seed, iter, true, false, want_stats, false, -1);
+    ctx->grad_zero = false;
+    if (want_stats) {
+      *stats = res.stats;
+      ctx->sync();
+    }
+  });
+}
+
+int gcpb_draw_samples(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                      uint64_t seed, uint64_t iter, int64_t cap, int64_t* idx_out,
+                      double* x_out, double* w_out, int32_t* flag_out, double* m_out,
+                      double* y_out, int64_t* n_out, gcpb_stats* stats) {
+  return guard(ctx, [&] {
+    validate_sampler(sampler);
+    validate_loss(loss);
+    if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+    if (sampler->strategy != GCPB_UNIFORM && ctx->tensor_kind != 2)
+      throw std::invalid_argument("stratified sampling requires a sparse tensor");
+    check_data_domain(ctx, loss->kind);
+    const int64_t n = expected_samples(ctx, sampler);
+    if (n_out) *n_out = n;
+    if (n > cap) throw std::length_error("gcpb_draw_samples: capacity too small");
+    alloc_record(ctx, n);
+    SampleResult res;
+    if (ctx->dtype == GCPB_F32)
+      res = stoch_grad_impl<float>(ctx, sampler, loss, seed, iter, false, true, true, false, -1);
+    else
+      res = stoch_grad_impl<double>(ctx, sampler, loss, seed, iter, false, true, true, false, -1);
+    if (n > 0) {
+      if (idx_out) CK(cudaMemcpyAsync(idx_out, ctx->s_idx.p, n * ctx->d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (x_out) CK(cudaMemcpyAsync(x_out, ctx->s_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (w_out) CK(cudaMemcpyAsync(w_out, ctx->s_w.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (flag_out) CK(cudaMemcpyAsync(flag_out, ctx->s_flag.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+      if (m_out) CK(cudaMemcpyAsync(m_out, ctx->s_m.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (y_out) CK(cudaMemcpyAsync(y_out, ctx->s_y.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    ctx->sync();
+    if (stats) *stats = res.stats;
+  });
+}
+
+
+int gcpb_eval_deriv(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const double* x,
+                    const double* w, const int32_t* flags, const gcpb_loss* loss,
+                    double* m_out, double* y_out) {
+  return guard(ctx, [&] {
+    validate_loss(loss);
+    if (n < 0) throw std::invalid_argument("negative sample count");
+    for (int64_t e = 0; e < n; ++e) {
+      check_index_host(ctx, idx + e * ctx->d);
+      check_domain_value(loss->kind, x[e]);
+    }
+    if (n == 0) return;
+    alloc_record(ctx, n);
+    ctx->s_aux.alloc(static_cast<size_t>(n) * sizeof(double));
+    std::vector<int32_t> f(static_cast<size_t>(n), 0);
+    if (flags) std::copy(flags, flags + n, f.begin());
+    CK(cudaMemcpyAsync(ctx->s_idx.p, idx, n * ctx->d * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->s_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->s_w.p, w, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->s_flag.p, f.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->dtype == GCPB_F32)
+      given_launch<float>(ctx, n, loss, false, true, false);
+    else
+      given_launch<double>(ctx, n, loss, false, true, false);
+    if (m_out) CK(cudaMemcpyAsync(m_out, ctx->s_m.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (y_out) CK(cudaMemcpyAsync(y_out, ctx->s_aux.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
+int gcpb_mttkrp_samples(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const double* y) {
+  return guard(ctx, [&] {
+    if (n < 0) throw std::invalid_argument("negative sample count");
+    for (int64_t e = 0; e < n; ++e) check_index_host(ctx, idx + e * ctx->d);
+    CK(cudaMemsetAsync(ctx->Gr.p, 0, ctx->nelem * ctx->tsize, ctx->stream));
+    ctx->grad_zero = true;
+    if (n == 0) {
+      ctx->sync();
+      return;
+    }
+    alloc_record(ctx, n);
+    CK(cudaMemcpyAsync(ctx->s_idx.p, idx, n * ctx->d * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->s_y.p, y, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    gcpb_loss l{GCPB_LOSS_GAUSSIAN, 0.0};
+    if (ctx->dtype == GCPB_F32)
+      given_launch<float>(ctx, n, &l, true, false, true);
+    else
+      given_launch<double>(ctx, n, &l, true, false, true);
+    ctx->grad_zero = false;
+    ctx->sync();
+  });
+}
+
+// ---- optimizer -------------------------------------------------------------------------------
+int gcpb_adam_step(gcpb_ctx* ctx, const gcpb_adam* adam) {
+  return guard(ctx, [&] {
+    if (!adam) throw std::invalid_argument("adam: null");
+    DevState* st = ctx->dst();
+    DevState& h = ctx->host_state;
+    const int32_t has = adam->has_lower_bound ? 1 : 0;
+    const bool changed = !ctx->adam_params_valid || h.lr != adam->learning_rate ||
+                         h.beta1 != adam->beta1 || h.beta2 != adam->beta2 ||
+                         h.eps != adam->epsilon || h.lb != adam->lower_bound || h.has_lb != has;
+    if (changed) {
+      // Staged through the context's pinned parameter block: no host sync.
+      h.lr = adam->learning_rate;
+      h.beta1 = adam->beta1;
+      h.beta2 = adam->beta2;
+      h.eps = adam->epsilon;
+      h.lb = adam->lower_bound;
+      h.has_lb = has;
+      double* pin = ctx->pinned_params;
+      pin[0] = h.lr;
+      pin[1] = h.beta1;
+      pin[2] = h.beta2;
+      pin[3] = h.eps;
+      pin[4] = h.lb;
+      std::memcpy(&pin[5], &has, sizeof(has));
+      CK(cudaMemcpyAsync(&st->lr, pin, 5 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(&st->has_lb, &pin[5], sizeof(int32_t), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      ctx->adam_params_valid = true;
+    }
+    if (ctx->dtype == GCPB_F32)
+      adam_launch<float>(ctx);
+    else
+      adam_launch<double>(ctx);
+    ctx->grad_zero = true;
+  });
+}
+
+int gcpb_adam_reset(gcpb_ctx* ctx) {
+  return guard(ctx, [&] {
+    const size_t bytes = ctx->nelem * ctx->tsize;
+    CK(cudaMemsetAsync(ctx->B.p, 0, bytes, ctx->stream));
+    CK(cudaMemsetAsync(ctx->C.p, 0, bytes, ctx->stream));
+    const int64_t zero = 0;
+    CK(cudaMemcpyAsync(&ctx->dst()->t, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+  });
+}
+
+int gcpb_get_iterations(gcpb_ctx* ctx, int64_t* out) {
+  return guard(ctx, [&] {
+    CK(cudaMemcpyAsync(out, &ctx->dst()->t, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
+int gcpb_set_iterations(gcpb_ctx* ctx, int64_t iterations) {
+  return guard(ctx, [&] {
+    CK(cudaMemcpyAsync(&ctx->dst()->t, &iterations, 8, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+  });
+}
+
+// ---- estimator -----------------------------------------------------------------------------------
+int gcpb_estimator_set(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const double* x,
+                       const double* w) {
+  return guard(ctx, [&] {
+    if (n < 0) throw std::invalid_argument("estimator: count must be >= 0");
+    for (int64_t e = 0; e < n; ++e) check_index_host(ctx, idx + e * ctx->d);
+    const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+    ctx->est_idx.alloc(nn * ctx->d * 8);
+    ctx->est_x.alloc(nn * 8);
+    ctx->est_w.alloc(nn * 8);
+    if (n > 0) {
+      CK(cudaMemcpyAsync(ctx->est_idx.p, idx, n * ctx->d * 8, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->est_x.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->est_w.p, w, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->est_n = n;
+    ctx->sync();
+  });
+}
+
+int gcpb_estimator_draw(gcpb_ctx* ctx, int kind, int64_t count, double rho, uint64_t seed) {
+  return guard(ctx, [&] {
+    if (count < 0) throw std::invalid_argument("estimator: count must be >= 0");
+    if (kind != GCPB_EST_UNIFORM && kind != GCPB_EST_STRATIFIED)
+      throw std::invalid_argument("unknown estimator kind");
+    if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+    if (kind == GCPB_EST_STRATIFIED && ctx->tensor_kind != 2)
+      throw std::invalid_argument("stratified estimator requires a sparse tensor");
+    gcpb_sampler sk{};
+    if (kind == GCPB_EST_UNIFORM) {
+      sk.strategy = GCPB_UNIFORM;
+      sk.num_samples = count;
+    } else {
+      sk.strategy = GCPB_STRATIFIED;
+      sk.nonzero_samples = count / 2;
+      sk.zero_samples = count - count / 2;
+      sk.oversample = rho;
+      if (!(rho > 1.0)) throw std::invalid_argument("sample_zeros_rejection: rho must be > 1");
+    }
+    const int64_t n = count;
+    alloc_record(ctx, n);
+    gcpb_loss l{GCPB_LOSS_GAUSSIAN, 0.0};
+    if (n > 0) {
+      if (kind == GCPB_EST_UNIFORM) {
+        if (ctx->dtype == GCPB_F32)
+          stoch_grad_impl<float>(ctx, &sk, &l, seed, 0, false, true, true, true, kind);
+        else
+          stoch_grad_impl<double>(ctx, &sk, &l, seed, 0, false, true, true, true, kind);
+      } else {
+        if (ctx->dtype == GCPB_F32)
+          stoch_grad_impl<float>(ctx, &sk, &l, seed, 0, false, true, true, true, kind);
+        else
+          stoch_grad_impl<double>(ctx, &sk, &l, seed, 0, false, true, true, true, kind);
+      }
+    }
+    const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+    ctx->est_idx.alloc(nn * ctx->d * 8);
+    ctx->est_x.alloc(nn * 8);
+    ctx->est_w.alloc(nn * 8);
+    if (n > 0) {
+      CK(cudaMemcpyAsync(ctx->est_idx.p, ctx->s_idx.p, n * ctx->d * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->est_x.p, ctx->s_x.p, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->est_w.p, ctx->s_w.p, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ctx->est_n = n;
+    ctx->sync();
+  });
+}
+
+int64_t gcpb_estimator_size(const gcpb_ctx* ctx) { return ctx ? ctx->est_n : 0; }
+
+int gcpb_estimator_get(gcpb_ctx* ctx, int64_t* idx_out, double* x_out, double* w_out) {
+  return guard(ctx, [&] {
+    const int64_t n = ctx->est_n;
+    if (n > 0) {
+      if (idx_out) CK(cudaMemcpyAsync(idx_out, ctx->est_idx.p, n * ctx->d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (x_out) CK(cudaMemcpyAsync(x_out, ctx->est_x.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      if (w_out) CK(cudaMemcpyAsync(w_out, ctx->est_w.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    ctx->sync();
+  });
+}
+
+int gcpb_estimate(gcpb_ctx* ctx, const gcpb_loss* loss, double* out) {
+  return guard(ctx, [&] {
+    validate_loss(loss);
+    if (ctx->est_n == 0) {
+      *out = 0.0;
+      return;
+    }
+    if (ctx->dtype == GCPB_F32)
+      estimate_launch<float>(ctx, loss);
+    else
+      estimate_launch<double>(ctx, loss);
+    CK(cudaMemcpyAsync(out, ctx->est_out.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
+// ---- snapshots ----------------------------------------------------------------------------------
+int gcpb_snapshot_save(gcpb_ctx* ctx) {
+  return guard(ctx, [&] {
+    const size_t bytes = ctx->nelem * ctx->tsize;
+    for (auto pr : {std::make_pair(&ctx->As, &ctx->A), std::make_pair(&ctx->Bs, &ctx->B),
+                    std::make_pair(&ctx->Cs, &ctx->C)}) {
+      pr.first->alloc(bytes);
+      CK(cudaMemcpyAsync(pr.first->p, pr.second->p, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    DevState* st = ctx->dst();
+    CK(cudaMemcpyAsync(&st->t_saved, &st->t, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->have_snapshot = true;
+    ctx->sync();
+  });
+}
+
+int gcpb_snapshot_restore(gcpb_ctx* ctx) {
+  return guard(ctx, [&] {
+    if (!ctx->have_snapshot) throw std::logic_error("no snapshot saved");
+    const size_t bytes = ctx->nelem * ctx->tsize;
+    for (auto pr : {std::make_pair(&ctx->A, &ctx->As), std::make_pair(&ctx->B, &ctx->Bs),
+                    std::make_pair(&ctx->C, &ctx->Cs)})
+      CK(cudaMemcpyAsync(pr.first->p, pr.second->p, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    DevState* st = ctx->dst();
+    CK(cudaMemcpyAsync(&st->t, &st->t_saved, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->sync();
+  });
+}
+
+// ---- multi-GPU ------------------------------------------------------------------------------------
+int gcpb_nccl_unique_id(char out[128]) {
+  return guard(nullptr, [&] {
+    ncclUniqueId id;
+    nck(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+  });
+}
+
+int gcpb_comm_init(gcpb_ctx* ctx, const char unique_id[128], int rank, int nranks) {
+  return guard(ctx, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank/nranks");
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, 128);
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    nck(ncclCommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+  });
+}
+
+int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks) {
+  return guard(ctx, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank/nranks");
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+  });
+}
+
+int gcpb_allreduce_grad(gcpb_ctx* ctx) {
+  return guard(ctx, [&] {
+    if (ctx->nranks == 1) return;
+    if (!ctx->comm) throw std::logic_error("allreduce without an NCCL communicator");
+    nck(ncclAllReduce(ctx->Gr.p, ctx->Gr.p, static_cast<size_t>(ctx->nelem),
+                      ctx->dtype == GCPB_F32 ? ncclFloat : ncclDouble, ncclSum, ctx->comm,
+                      ctx->stream),
+        "ncclAllReduce");
+  });
+}
+
+// ---- host-only helpers ------------------------------------------------------------------------------
+uint64_t gcpb_philox_bounded(uint64_t seed, uint32_t tag, uint64_t iter, uint64_t t, int slot,
+                             uint64_t n) {
+  if (n == 0) return 0;
+  return bounded_draw(seed, tag, iter, t, slot, n);
+}
+
+int64_t gcpb_zero_batch_size(double total, double zeta, double rho, int64_t shortfall) {
+  return zero_batch_size_dev(total, zeta, rho, shortfall);
+}
+
+void gcpb_shard_range(int64_t n, int rank, int nranks, int64_t* begin, int64_t* end) {
+  if (nranks < 1) nranks = 1;
+  const int64_t base = n / nranks, rem = n % nranks;
+  const int64_t b = rank * base + std::min<int64_t>(rank, rem);
+  *begin = b;
+  *end = b + base + (rank < rem ? 1 : 0);
+}
+
+void gcpb_stratified_keep(const int64_t* accepted_per_rank, int nranks, int rank, int64_t need,
+                          int64_t* offset, int64_t* keep) {
+  int64_t before = 0;
+  for (int i = 0; i < rank && i < nranks; ++i) before += accepted_per_rank[i];
+  *offset = before;
+  const int64_t room = need - before;
+  const int64_t mine = accepted_per_rank[rank];
+  *keep = room <= 0 ? 0 : (mine < room ? mine : room);
+}
+
+double gcpb_loss_deriv(const gcpb_loss* loss, double x, double m) {
+  const double eps = 1e-10;
+  switch (loss->kind) {
+    case GCPB_LOSS_GAUSSIAN: return 2.0 * (m - x);
+    case GCPB_LOSS_POISSON: return 1.0 - x / (m + eps);
+    case GCPB_LOSS_BERNOULLI_ODDS: return 1.0 / (m + 1.0) - x / (m + eps);
+    case GCPB_LOSS_GAMMA: return 1.0 / (m + eps) - x / ((m + eps) * (m + eps));
+    case GCPB_LOSS_BETA_HALF: {
+      const double s = std::sqrt(m + eps);
+      return 1.0 / s - x / (s * s * s);
+    }
+    default: {
+      const double r = x - m;
+      if (std::fabs(r) <= loss->delta) return -2.0 * r;
+      return r > 0.0 ? -2.0 * loss->delta : 2.0 * loss->delta;
+    }
+  }
+}
+
+double gcpb_loss_value(const gcpb_loss* loss, double x, double m) {
+  const double eps = 1e-10;
+  switch (loss->kind) {
+    case GCPB_LOSS_GAUSSIAN: return (x - m) * (x - m);
+    case GCPB_LOSS_POISSON: return m - x * std::log(m + eps);
+    case GCPB_LOSS_BERNOULLI_ODDS: return std::log(m + 1.0) - x * std::log(m + eps);
+    case GCPB_LOSS_GAMMA: return x / (m + eps) + std::log(m + eps);
+    case GCPB_LOSS_BETA_HALF: {
+      const double s = std::sqrt(m + eps);
+      return 2.0 * s + 2.0 * x / s;
+    }
+    default: {
+      const double r = x - m;
+      if (std::fabs(r) <= loss->delta) return r * r;
+      return 2.0 * loss->delta * std::fabs(r) - loss->delta * loss->delta;
+    }
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,440 @@
+// gcpb_aux.cuh — the kernels around the hot path: stratified zero-candidate
+// testing with order-preserving compaction, hash build, Adam, the fp64 loss
+// estimate, data generation and small parity helpers.
+#pragma once
+#include "gcpb_kernels.cuh"
+
+namespace gcpb {
+
+// Device-resident scalar state (one per context).  Living in device memory
+// lets whole iterations be captured in a CUDA graph and replayed.
+struct DevState {
+  // Adam (AdamState + the FitConfig fields adam_step reads)
+  int64_t t;  // AdamState::iterations
+  int64_t t_saved;
+  double lr, beta1, beta2, eps, lb;
+  int32_t has_lb;
+  uint32_t adam_done;
+  // stratified zero sampler (one call)
+  int64_t z_q;
+  int64_t z_tested, z_accepted, z_rejected;  // RejectionStats, cumulative
+  int64_t z_acc_before;                      // accepted before the current batch
+  int64_t z_batch_begin, z_batch_size, z_nchunks;
+  unsigned long long z_ticket;
+  uint32_t z_batch_tag;
+  int32_t z_pad;
+  double z_total, z_zeta, z_rho;
+  int64_t z_status_cap;
+  int32_t z_overflow;
+  int32_t z_pad2;
+};
+
+constexpr int kZcThreads = 256;
+constexpr int kZcItems = 8;
+constexpr int64_t kZcChunk = kZcThreads * kZcItems;
+
+struct ZeroArgs {
+  int d;
+  uint32_t dims[kMaxModes];
+  uint32_t thr[kMaxModes];
+  uint64_t stride[kMaxModes];
+  uint64_t seed;
+  uint64_t iter;
+  uint32_t tag;
+  const uint64_t* hkeys;
+  uint64_t hmask;
+  DevState* st;
+  unsigned long long* status;
+  uint64_t* zero_list;
+};
+
+// Batch size of one rejection round, samplers.hpp:118-122, evaluated with
+// explicit round-to-nearest ops so it equals the host formula bit for bit.
+__host__ __device__ inline int64_t zero_batch_size_dev(double total, double zeta, double rho,
+                                                       int64_t shortfall) {
+#if defined(__CUDA_ARCH__)
+  double b = ceil(__dmul_rn(__dmul_rn(rho, __ddiv_rn(total, zeta)), static_cast<double>(shortfall)));
+#else
+  double b = std::ceil(rho * (total / zeta) * static_cast<double>(shortfall));
+#endif
+  if (!(b >= 1.0)) b = 1.0;
+  if (b > 9e15) b = 9e15;
+  return static_cast<int64_t>(b);
+}
+
+// Plans the next rejection batch from the device-resident shortfall.
+__global__ void zero_plan_kernel(DevState* st, int first) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (first) {
+    st->z_tested = 0;
+    st->z_accepted = 0;
+    st->z_rejected = 0;
+  }
+  const int64_t kept = st->z_accepted < st->z_q ? st->z_accepted : st->z_q;
+  const int64_t shortfall = st->z_q - kept;
+  st->z_ticket = 0;
+  st->z_batch_tag += 1;
+  st->z_acc_before = st->z_accepted;
+  st->z_batch_begin = st->z_tested;
+  if (shortfall <= 0) {
+    st->z_batch_size = 0;
+    st->z_nchunks = 0;
+    return;
+  }
+  const int64_t batch = zero_batch_size_dev(st->z_total, st->z_zeta, st->z_rho, shortfall);
+  int64_t nchunks = (batch + kZcChunk - 1) / kZcChunk;
+  if (nchunks > st->z_status_cap) {  // cannot happen: batch shrinks with the shortfall
+    st->z_overflow = 1;
+    nchunks = 0;
+  }
+  st->z_batch_size = batch;
+  st->z_nchunks = nchunks;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Status word: [63:48] batch tag, [47:46] flag (1 aggregate, 2 inclusive
+// prefix), [45:0] count.
+__device__ __forceinline__ unsigned long long pack_status(uint32_t tag, unsigned flag,
+                                                          unsigned long long v) {
+  return (static_cast<unsigned long long>(tag & 0xFFFFu) << 48) |
+         (static_cast<unsigned long long>(flag) << 46) | (v & ((1ull << 46) - 1));
+}
+
+// Tests one batch of zero candidates against the nonzero hash and appends the
+// accepted ones, in candidate order, to zero_list (ranks < q only) — the
+// reference's "test the whole batch, keep the first q non-hits"
+// (samplers.hpp:117-133) as one pass with a decoupled look-back scan.
+__global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a) {
+  __shared__ long long s_chunk;
+  __shared__ int s_warp_sum[kZcThreads / 32];
+  __shared__ int s_warp_valid[kZcThreads / 32];
+  __shared__ long long s_excl;
+  DevState* st = a.st;
+  const int64_t nchunks = st->z_nchunks;
+  const int64_t bbeg = st->z_batch_begin;
+  const int64_t bend = bbeg + st->z_batch_size;
+  const int64_t acc_before = st->z_acc_before;
+  const int64_t q = st->z_q;
+  const uint32_t btag = st->z_batch_tag;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = static_cast<long long>(atomicAdd(&st->z_ticket, 1ull));
+    __syncthreads();
+    const int64_t chunk = s_chunk;
+    if (chunk >= nchunks) break;
+    const int64_t cbeg = bbeg + chunk * kZcChunk + static_cast<int64_t>(threadIdx.x) * kZcItems;
+    uint32_t bits = 0;
+    int nvalid = 0;
+#pragma unroll 1
+    for (int j = 0; j < kZcItems; ++j) {
+      const int64_t c = cbeg + j;
+      if (c >= bend) break;
+      ++nvalid;
+      uint64_t lin = 0;
+      for (int g4 = 0; g4 * 4 < a.d; ++g4) {
+        const U4 b = philox_block(a.seed, a.tag, static_cast<uint32_t>(g4), 0u, a.iter,
+                                  static_cast<uint64_t>(c));
+        for (int sl = 0; sl < 4; ++sl) {
+          const int k = g4 * 4 + sl;
+          if (k >= a.d) break;
+          const uint64_t prod = static_cast<uint64_t>(word_of(b, sl)) * a.dims[k];
+          uint32_t ik = (static_cast<uint32_t>(prod) >= a.thr[k])
+                            ? static_cast<uint32_t>(prod >> 32)
+                            : bounded32_from(a.seed, a.tag, a.iter, static_cast<uint64_t>(c), k,
+                                             a.dims[k], a.thr[k], 1u);
+          lin += static_cast<uint64_t>(ik) * a.stride[k];
+        }
+      }
+      const bool hit = a.hkeys != nullptr && hash_find(a.hkeys, a.hmask, lin) >= 0;
+      if (!hit) bits |= 1u << j;
+    }
+    const int cnt = __popc(bits);
+    // block exclusive scan of cnt
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int vsum = nvalid;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+    if (lane == 31) s_warp_sum[wid] = incl;
+    if (lane == 0) s_warp_valid[wid] = vsum;
+    __syncthreads();
+    int warp_excl = 0, block_total = 0, block_valid = 0;
+    for (int w = 0; w < kZcThreads / 32; ++w) {
+      if (w < wid) warp_excl += s_warp_sum[w];
+      block_total += s_warp_sum[w];
+      block_valid += s_warp_valid[w];
+    }
+    const int thread_excl = warp_excl + incl - cnt;
+    if (threadIdx.x == 0) {
+      unsigned long long excl = 0;
+      if (chunk == 0) {
+        st_release_u64(&a.status[chunk], pack_status(btag, 2u, block_total));
+      } else {
+        st_release_u64(&a.status[chunk], pack_status(btag, 1u, block_total));
+        int64_t pred = chunk - 1;
+        for (;;) {
+          const unsigned long long v = ld_acquire_u64(&a.status[pred]);
+          const unsigned flag = static_cast<unsigned>((v >> 46) & 3u);
+          if (static_cast<uint32_t>(v >> 48) != (btag & 0xFFFFu) || flag == 0) continue;
+          excl += v & ((1ull << 46) - 1);
+          if (flag == 2u) break;
+          --pred;
+        }
+        st_release_u64(&a.status[chunk], pack_status(btag, 2u, excl + block_total));
+      }
+      s_excl = static_cast<long long>(excl);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_tested),
+                static_cast<unsigned long long>(block_valid));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_accepted),
+                static_cast<unsigned long long>(block_total));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_rejected),
+                static_cast<unsigned long long>(block_valid - block_total));
+    }
+    __syncthreads();
+    int64_t rank = acc_before + s_excl + thread_excl;
+    for (int j = 0; j < kZcItems; ++j) {
+      if ((bits >> j) & 1u) {
+        if (rank < q) a.zero_list[rank] = static_cast<uint64_t>(cbeg + j);
+        ++rank;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Open-addressing build (keys unique).
+__global__ void hash_build_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                  unsigned long long* tkeys, uint32_t* tvals, uint64_t mask) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long key = keys[e];
+    uint64_t b = mix64(key) & mask;
+    for (;;) {
+      bool done = false;
+      for (int s = 0; s < 4; ++s) {
+        const unsigned long long prev = atomicCAS(&tkeys[b * 4 + s], ~0ull, key);
+        if (prev == ~0ull) {
+          tvals[b * 4 + s] = static_cast<uint32_t>(e);
+          done = true;
+          break;
+        }
+      }
+      if (done) break;
+      b = (b + 1) & mask;
+    }
+  }
+}
+
+// adam_step (optimizer.cpp:47-66) fused with zeroing the gradient; padding
+// columns (j >= r) are left untouched.  The last block advances t.
+template <typename T>
+__global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict__ B,
+                            T* __restrict__ C, int64_t n, int rp, int r, DevState* st) {
+  __shared__ double s_c1, s_c2;
+  if (threadIdx.x == 0) {
+    const double te = static_cast<double>(st->t + 1);
+    s_c1 = 1.0 - pow(st->beta1, te);
+    s_c2 = 1.0 - pow(st->beta2, te);
+  }
+  __syncthreads();
+  const T c1 = static_cast<T>(s_c1), c2 = static_cast<T>(s_c2);
+  const T lr = static_cast<T>(st->lr);
+  const T b1 = static_cast<T>(st->beta1), b2 = static_cast<T>(st->beta2);
+  const T ob1 = static_cast<T>(1.0 - st->beta1), ob2 = static_cast<T>(1.0 - st->beta2);
+  const T eps = static_cast<T>(st->eps);
+  const bool has_lb = st->has_lb != 0;
+  const T lb = static_cast<T>(st->lb);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const T g = Gr[i];
+    Gr[i] = static_cast<T>(0);
+    if (static_cast<int>(i % rp) >= r) continue;
+    const T b = b1 * B[i] + ob1 * g;
+    const T c = b2 * C[i] + ob2 * (g * g);
+    B[i] = b;
+    C[i] = c;
+    T a = A[i] - lr * (b / c1) / sqrt((c / c2) + eps);
+    if (has_lb) a = a > lb ? a : lb;
+    A[i] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->adam_done, 1u);
+    if (prev == gridDim.x - 1) {
+      st->t += 1;
+      st->adam_done = 0;
+    }
+  }
+}
+
+template <typename T>
+struct ModelDesc {
+  const T* A;
+  int d, rp, r;
+  int64_t off[kMaxModes];
+};
+
+template <typename T>
+__device__ __forceinline__ double model_entry(const ModelDesc<T>& md, const int64_t* idx) {
+  T sum = static_cast<T>(0);
+  for (int j = 0; j < md.r; ++j) {
+    T prod = static_cast<T>(1);
+    for (int k = 0; k < md.d; ++k) prod *= md.A[md.off[k] + idx[k] * md.rp + j];
+    sum += prod;
+  }
+  return static_cast<double>(sum);
+}
+
+// Fixed-order fp64 partial sums of w * f(x, m) (samplers.cpp:114-124): block
+// b owns a fixed contiguous range; deterministic for a fixed grid.
+template <typename T>
+__global__ void estimate_partial_kernel(const ModelDesc<T> md, const int64_t* __restrict__ idx,
+                                        const double* __restrict__ x,
+                                        const double* __restrict__ w, int64_t n, int loss,
+                                        double delta, double* partials) {
+  __shared__ double s[256];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t end = beg + per < n ? beg + per : n;
+  double acc = 0.0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const double m = model_entry(md, idx + i * md.d);
+    acc += w[i] * loss_value(loss, delta, x[i], m);
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
+__global__ void sum_partials_kernel(const double* partials, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += partials[i];
+    *out = s;
+  }
+}
+
+// Synthetic dense binary tensor (BASELINE configs[1]): one warp per mode-0
+// fiber; x = [u < m/(1+m)], u from the Philox stream at the linear index.
+__global__ void gen_bernoulli_kernel(uint8_t* __restrict__ out, int d, const int64_t* dims,
+                                     const int64_t* foff, int R, const double* __restrict__ F,
+                                     uint64_t seed, int64_t nfibers) {
+  extern __shared__ double s_p[];  // [warps][R]
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  double* P = s_p + wid * R;
+  const int64_t n0 = dims[0];
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t f = warp0; f < nfibers; f += nwarps) {
+    for (int j = lane; j < R; j += 32) {
+      double p = 1.0;
+      int64_t rem = f;
+      for (int k = 1; k < d; ++k) {
+        const int64_t ik = rem % dims[k];
+        rem /= dims[k];
+        p *= F[foff[k] + ik * R + j];
+      }
+      P[j] = p;
+    }
+    __syncwarp();
+    for (int64_t i0 = lane; i0 < n0; i0 += 32) {
+      double m = 0.0;
+      for (int j = 0; j < R; ++j) m += F[foff[0] + i0 * R + j] * P[j];
+      const double pr = m / (1.0 + m);
+      const uint64_t lin = static_cast<uint64_t>(f) * static_cast<uint64_t>(n0) + i0;
+      const U4 b = philox_block(seed, TAG_GENERATE, 0u, 0u, 0ull, lin);
+      const double u =
+          static_cast<double>(((static_cast<uint64_t>(b.x) << 32) | b.y) >> 11) * 0x1.0p-53;
+      out[lin] = u < pr ? 1 : 0;
+    }
+    __syncwarp();
+  }
+}
+
+// COO SoA coordinates from sorted linear keys (multi_index, shape.cpp:98-109).
+__global__ void keys_to_coo_kernel(const uint64_t* __restrict__ keys, int64_t n, int d,
+                                   const int64_t* dims, int32_t* coo) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t rem = keys[e];
+    for (int k = 0; k < d; ++k) {
+      const uint64_t nk = static_cast<uint64_t>(dims[k]);
+      coo[k * n + e] = static_cast<int32_t>(rem % nk);
+      rem /= nk;
+    }
+  }
+}
+
+// Validation of device ingest: keys strictly increasing and < N, values != 0.
+template <typename V>
+__global__ void check_keys_kernel(const uint64_t* __restrict__ keys, const V* __restrict__ vals,
+                                  int64_t n, uint64_t total, unsigned* flags) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (keys[e] >= total) atomicOr(flags, 1u);
+    if (e > 0 && keys[e - 1] >= keys[e]) atomicOr(flags, 2u);
+    if (vals[e] == static_cast<V>(0)) atomicOr(flags, 4u);
+  }
+}
+
+template <typename V, typename T>
+__global__ void convert_kernel(const V* __restrict__ in, T* __restrict__ out, int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[e] = static_cast<T>(in[e]);
+}
+
+// Sum of squares in fp64 (fixed grid, deterministic per launch geometry).
+template <typename V>
+__global__ void sumsq_kernel(const V* __restrict__ v, int64_t n, double* partials) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = static_cast<double>(v[e]);
+    acc += x * x;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
+// Loss-domain scan of the stored data (loss.cpp:42-62): bit 0 = some x < 0,
+// bit 1 = some x not in {0, 1}, bit 2 = NaN.
+template <typename V>
+__global__ void domain_scan_kernel(const V* __restrict__ v, int64_t n, unsigned* flags) {
+  unsigned f = 0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = static_cast<double>(v[e]);
+    if (x < 0.0) f |= 1u;
+    if (x != 0.0 && x != 1.0) f |= 2u;
+    if (x != x) f |= 4u;
+  }
+  if (f) atomicOr(flags, f);
+}
+
+}  // namespace gcpb

@@ -1,0 +1,7 @@
+// Instantiation unit for the fused hot-path kernel, T = float (split per type to
+// keep nvcc compile units small and parallel).
+#include "gcpb_fused.cuh"
+
+namespace gcpb {
+template cudaError_t launch_fused<float>(const FusedArgs<float>&, int64_t, bool, cudaStream_t, int);
+}  // namespace gcpb

@@ -1,0 +1,228 @@
+// gcpb_kernels.cuh — device code shared by the fused hot-path kernel and the
+// context layer.  See DESIGN.md §4 for the data layout and §5 for the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "philox.cuh"
+
+namespace gcpb {
+
+constexpr int kMaxModes = 16;
+constexpr uint64_t kEmptyKey = ~0ull;
+
+// Data-access kinds for the tensor value x at a sampled index.
+enum XKind : int { X_NONE = 0, X_DENSE_U8 = 1, X_DENSE_F32 = 2, X_DENSE_F64 = 3, X_SPARSE = 4 };
+
+// Sample-segment kinds of one fused launch (in the reference's sample order).
+enum SegKind : int {
+  SEG_UNIFORM = 0,    // sample_uniform body (samplers.hpp:87-93): x looked up
+  SEG_PICK = 1,       // nonzero picks (samplers.hpp:159-165 / 201-207)
+  SEG_DRAW_ZERO = 2,  // semi-stratified unrestricted draws, x = 0 (samplers.hpp:211-216)
+  SEG_ZERO_LIST = 3,  // stratified accepted zero candidates (samplers.hpp:169-172)
+  SEG_GIVEN = 4,      // host-given samples (parity entry points)
+};
+
+struct Seg {
+  int kind;
+  uint32_t tag;
+  int flag;          // 1: y = w * (g(x,m) - g(0,m))  (semi nonzero term)
+  int pad_;
+  int64_t t_begin;   // first sample ordinal handled by this launch
+  int64_t t_end;
+  int64_t tiles_begin;  // first global tile of this segment
+  int64_t out_offset;   // record position of ordinal t_begin
+  double weight;
+};
+
+template <typename T>
+struct FusedArgs {
+  const T* A;  // factors, mode k at A + off[k], row i at + i * rp
+  T* G;        // gradient, same layout
+  int d;
+  int rp;      // padded row length (elements)
+  int nchunks; // 16-byte chunks holding real columns: ceil(r / VW)
+  int loss;
+  T delta;
+  int64_t off[kMaxModes];
+  uint32_t dims[kMaxModes];
+  uint32_t thr[kMaxModes];  // Lemire thresholds (2^32 - n_k) mod n_k
+  uint64_t stride[kMaxModes];
+  uint64_t seed;
+  uint64_t iter;
+  // tensor access
+  int xkind;
+  const void* dense;
+  const int32_t* coo;  // SoA: coo[k * coo_stride + e]
+  int64_t coo_stride;
+  const T* vals;
+  uint64_t eta;        // global nonzero count (pick range)
+  uint32_t thr_eta;
+  int64_t nz_begin, nz_end;  // global pick ordinals held by this context
+  const uint64_t* hkeys;
+  const uint32_t* hvals;
+  uint64_t hmask;
+  // segments
+  int nseg;
+  Seg seg[3];
+  const uint64_t* zero_list;
+  // given samples
+  const int64_t* g_idx;
+  const double* g_x;
+  const double* g_w;
+  const int32_t* g_flag;
+  const double* g_y;
+  // record outputs (device pointers), written when non-null
+  int64_t* r_idx;
+  double* r_x;
+  double* r_w;
+  int32_t* r_flag;
+  double* r_m;
+  double* r_y;
+  int scatter;
+};
+
+// ---------------------------------------------------------------------------
+// Loss f(x,m) and g = df/dm (src/loss.cpp:64-110), eps = 1e-10 shift.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T loss_deriv(int kind, T delta, T x, T m) {
+  const T eps = static_cast<T>(1e-10);
+  const T one = static_cast<T>(1);
+  const T two = static_cast<T>(2);
+  switch (kind) {
+    case 0:
+      return two * (m - x);
+    case 1:
+      return one - x / (m + eps);
+    case 2:
+      return one / (m + one) - x / (m + eps);
+    case 3:
+      return one / (m + eps) - x / ((m + eps) * (m + eps));
+    case 4: {
+      const T s = sqrt(m + eps);
+      return one / s - x / (s * s * s);
+    }
+    default: {
+      const T r = x - m;
+      if (fabs(r) <= delta) return -two * r;
+      return r > static_cast<T>(0) ? -two * delta : two * delta;
+    }
+  }
+}
+
+__device__ __forceinline__ double loss_value(int kind, double delta, double x, double m) {
+  const double eps = 1e-10;
+  switch (kind) {
+    case 0:
+      return (x - m) * (x - m);
+    case 1:
+      return m - x * log(m + eps);
+    case 2:
+      return log(m + 1.0) - x * log(m + eps);
+    case 3:
+      return x / (m + eps) + log(m + eps);
+    case 4: {
+      const double s = sqrt(m + eps);
+      return 2.0 * s + 2.0 * x / s;
+    }
+    default: {
+      const double r = x - m;
+      if (fabs(r) <= delta) return r * r;
+      return 2.0 * delta * fabs(r) - delta * delta;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Memory helpers
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Vec;  // one 16-byte chunk
+template <>
+struct Vec<float> {
+  static constexpr int W = 4;
+  float v[4];
+};
+template <>
+struct Vec<double> {
+  static constexpr int W = 2;
+  double v[2];
+};
+
+__device__ __forceinline__ void load_chunk(const float* p, Vec<float>& out) {
+  const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+  out.v[0] = q.x;
+  out.v[1] = q.y;
+  out.v[2] = q.z;
+  out.v[3] = q.w;
+}
+__device__ __forceinline__ void load_chunk(const double* p, Vec<double>& out) {
+  const double2 q = __ldg(reinterpret_cast<const double2*>(p));
+  out.v[0] = q.x;
+  out.v[1] = q.y;
+}
+
+// Scatter-add of one chunk: red.global.add.v4.f32 (one 16-byte vector
+// reduction in L2) for fp32, two red.global.add.f64 for fp64.
+__device__ __forceinline__ void red_chunk(float* p, const float (&v)[4]) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void red_chunk(double* p, const double (&v)[2]) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v[0]) : "memory");
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(v[1]) : "memory");
+}
+
+// Streaming loads of tensor data that should not displace factor rows in L1.
+__device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ ulonglong2 ld_stream_u64x2(const uint64_t* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];"
+               : "=l"(v.x), "=l"(v.y)
+               : "l"(p));
+  return v;
+}
+
+// Open-addressing membership test: 2^b buckets of four u64 keys (one 32-byte
+// sector per bucket), linear probing over buckets; slots fill left to right
+// so an empty slot ends the probe.  Returns the slot or -1.
+__device__ __forceinline__ int64_t hash_find(const uint64_t* __restrict__ keys, uint64_t mask,
+                                             uint64_t key) {
+  uint64_t b = mix64(key) & mask;
+  for (;;) {
+    const ulonglong2 q0 = ld_stream_u64x2(keys + b * 4);
+    const ulonglong2 q1 = ld_stream_u64x2(keys + b * 4 + 2);
+    if (q0.x == key) return static_cast<int64_t>(b * 4);
+    if (q0.y == key) return static_cast<int64_t>(b * 4 + 1);
+    if (q1.x == key) return static_cast<int64_t>(b * 4 + 2);
+    if (q1.y == key) return static_cast<int64_t>(b * 4 + 3);
+    if (q0.x == kEmptyKey || q0.y == kEmptyKey || q1.x == kEmptyKey || q1.y == kEmptyKey)
+      return -1;
+    b = (b + 1) & mask;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-facing launcher (instantiated in gcpb_fused_f32.cu / gcpb_fused_f64.cu)
+// ---------------------------------------------------------------------------
+template <typename T>
+cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
+                         cudaStream_t stream, int num_sms);
+
+}  // namespace gcpb

@@ -1,0 +1,517 @@
+"""Host-side mirror of the reference API for the stochastic GCP hot path.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/gcp/*.hpp); every computation on the hot path
+goes through the C-ABI (include/gcpb.h) into the sm_100a engine.  Exceptions
+mirror the reference's: std::invalid_argument -> InvalidArgument(ValueError),
+std::domain_error -> DomainError(ValueError), std::out_of_range ->
+OutOfRange(IndexError), std::logic_error -> LogicError, std::runtime_error ->
+GcpRuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib
+
+
+# ---------------------------------------------------------------------------
+# Errors (status codes of include/gcpb.h)
+# ---------------------------------------------------------------------------
+class GcpError(Exception):
+    pass
+
+
+class InvalidArgument(GcpError, ValueError):
+    pass
+
+
+class DomainError(GcpError, ValueError):
+    pass
+
+
+class OutOfRange(GcpError, IndexError):
+    pass
+
+
+class LogicError(GcpError, RuntimeError):
+    pass
+
+
+class GcpRuntimeError(GcpError, RuntimeError):
+    pass
+
+
+_ERR = {_capi.ERR_RUNTIME: GcpRuntimeError, _capi.ERR_USAGE: InvalidArgument,
+        _capi.ERR_DOMAIN: DomainError, _capi.ERR_RANGE: OutOfRange, _capi.ERR_LOGIC: LogicError}
+
+
+def _check(rc: int, ctx=None) -> None:
+    if rc != _capi.OK:
+        msg = lib.gcpb_last_error(ctx)
+        raise _ERR.get(rc, GcpRuntimeError)(msg.decode() if msg else f"gcpb error {rc}")
+
+
+def _i64(a):
+    return a.ctypes.data_as(_capi.i64p)
+
+
+def _f64(a):
+    return a.ctypes.data_as(_capi.f64p)
+
+
+def _i32(a):
+    return a.ctypes.data_as(_capi.i32p)
+
+
+# ---------------------------------------------------------------------------
+# LossFunction (include/gcp/loss.hpp:8-57, src/loss.cpp)
+# ---------------------------------------------------------------------------
+GAUSSIAN, POISSON, BERNOULLI_ODDS, GAMMA, BETA_HALF, HUBER = range(6)
+_LOSS_NAMES = {GAUSSIAN: "gaussian", POISSON: "poisson", BERNOULLI_ODDS: "bernoulli-odds",
+               GAMMA: "gamma", BETA_HALF: "beta-half", HUBER: "huber"}
+
+
+@dataclass(frozen=True)
+class LossFunction:
+    kind: int
+    delta: float = 0.0
+
+    kEps = 1e-10
+
+    @staticmethod
+    def gaussian():
+        return LossFunction(GAUSSIAN)
+
+    @staticmethod
+    def poisson():
+        return LossFunction(POISSON)
+
+    @staticmethod
+    def bernoulli_odds():
+        return LossFunction(BERNOULLI_ODDS)
+
+    @staticmethod
+    def gamma():
+        return LossFunction(GAMMA)
+
+    @staticmethod
+    def beta_half():
+        return LossFunction(BETA_HALF)
+
+    @staticmethod
+    def huber(delta: float):
+        if not delta > 0.0:  # loss.cpp:17-18
+            raise InvalidArgument("huber: delta must be > 0")
+        return LossFunction(HUBER, float(delta))
+
+    @staticmethod
+    def parse(token: str) -> "LossFunction":  # loss.cpp:21-40
+        simple = {"gaussian": GAUSSIAN, "poisson": POISSON, "bernoulli-odds": BERNOULLI_ODDS,
+                  "gamma": GAMMA, "beta-half": BETA_HALF}
+        if token in simple:
+            return LossFunction(simple[token])
+        if token.startswith("huber:"):
+            arg = token[6:]
+            try:
+                delta = float(arg)
+            except ValueError:
+                raise InvalidArgument(f"huber: bad delta '{arg}'") from None
+            return LossFunction.huber(delta)
+        raise InvalidArgument(f"unknown loss '{token}'")
+
+    @property
+    def name(self) -> str:
+        return f"huber:{self.delta:f}" if self.kind == HUBER else _LOSS_NAMES[self.kind]
+
+    def c(self) -> _capi.gcpb_loss:
+        return _capi.gcpb_loss(self.kind, self.delta)
+
+    def value(self, x: float, m: float) -> float:
+        self.check_domain(x)
+        loss = self.c()
+        return lib.gcpb_loss_value(C.byref(loss), float(x), float(m))
+
+    def deriv(self, x: float, m: float) -> float:
+        self.check_domain(x)
+        loss = self.c()
+        return lib.gcpb_loss_deriv(C.byref(loss), float(x), float(m))
+
+    def check_domain(self, x: float) -> None:  # loss.cpp:42-62
+        if self.kind in (POISSON, GAMMA, BETA_HALF) and not x >= 0.0:
+            raise DomainError(f"{self.name} loss: data value {x} out of domain (x >= 0 required)")
+        if self.kind == BERNOULLI_ODDS and x not in (0.0, 1.0):
+            raise DomainError(f"{self.name} loss: data value {x} out of domain (x in {{0,1}} required)")
+
+    def default_lower_bound(self) -> Optional[float]:  # loss.cpp:112-124
+        return 0.0 if self.kind in (POISSON, BERNOULLI_ODDS, GAMMA, BETA_HALF) else None
+
+
+# ---------------------------------------------------------------------------
+# SamplerKind / RejectionStats (include/gcp/samplers.hpp:31-57)
+# ---------------------------------------------------------------------------
+UNIFORM, STRATIFIED, SEMI_STRATIFIED = _capi.UNIFORM, _capi.STRATIFIED, _capi.SEMI_STRATIFIED
+
+
+@dataclass
+class SamplerKind:
+    strategy: int = UNIFORM
+    num_samples: int = 0
+    nonzero_samples: int = 0
+    zero_samples: int = 0
+    oversample: float = 1.1
+
+    @staticmethod
+    def uniform(s: int) -> "SamplerKind":
+        k = SamplerKind(UNIFORM, num_samples=int(s))
+        k.validate()
+        return k
+
+    @staticmethod
+    def stratified(p: int, q: int, rho: float = 1.1) -> "SamplerKind":
+        k = SamplerKind(STRATIFIED, nonzero_samples=int(p), zero_samples=int(q), oversample=rho)
+        k.validate()
+        return k
+
+    @staticmethod
+    def semi_stratified(p: int, q: int) -> "SamplerKind":
+        k = SamplerKind(SEMI_STRATIFIED, nonzero_samples=int(p), zero_samples=int(q))
+        k.validate()
+        return k
+
+    @staticmethod
+    def from_token(token: str, total_samples: int) -> "SamplerKind":  # samplers.cpp:37-45
+        if token == "uniform":
+            return SamplerKind.uniform(total_samples)
+        if token == "stratified":
+            return SamplerKind.stratified(total_samples // 2, total_samples - total_samples // 2)
+        if token == "semi-stratified":
+            return SamplerKind.semi_stratified(total_samples // 2,
+                                               total_samples - total_samples // 2)
+        raise InvalidArgument(f"unknown sampler '{token}' (expected uniform, stratified, or "
+                              "semi-stratified)")
+
+    def token(self) -> str:
+        return {UNIFORM: "uniform", STRATIFIED: "stratified",
+                SEMI_STRATIFIED: "semi-stratified"}[self.strategy]
+
+    def validate(self) -> None:  # samplers.cpp:56-67
+        if self.strategy == UNIFORM:
+            if self.num_samples < 1:
+                raise InvalidArgument("uniform sampler: s must be >= 1")
+            return
+        if self.nonzero_samples < 0 or self.zero_samples < 0 or \
+                self.nonzero_samples + self.zero_samples < 1:
+            raise InvalidArgument("sampler: need p, q >= 0 and p + q >= 1")
+        if self.strategy == STRATIFIED and not self.oversample > 1.0:
+            raise InvalidArgument("stratified sampler: oversample rate must be > 1")
+
+    def total(self) -> int:
+        return self.num_samples if self.strategy == UNIFORM else \
+            self.nonzero_samples + self.zero_samples
+
+    def c(self) -> _capi.gcpb_sampler:
+        return _capi.gcpb_sampler(self.strategy, self.num_samples, self.nonzero_samples,
+                                  self.zero_samples, self.oversample)
+
+
+@dataclass
+class RejectionStats:
+    tested: int = 0
+    accepted: int = 0
+    rejected: int = 0
+
+
+# ---------------------------------------------------------------------------
+# The device engine (one GCP problem on one GPU)
+# ---------------------------------------------------------------------------
+class Engine:
+    """Owns a gcpb context: factors, gradient, Adam moments, tensor, estimator.
+
+    dims: tensor extents (n_1..n_d); rank: r; dtype "f32" (B200 fast path) or
+    "f64" (the reference's arithmetic type).
+    """
+
+    def __init__(self, dims: Sequence[int], rank: int, dtype: str = "f32", device: int = 0):
+        self.dims = tuple(int(n) for n in dims)
+        self.d = len(self.dims)
+        self.rank = int(rank)
+        self.dtype = dtype
+        dt = {"f32": _capi.F32, "f64": _capi.F64}.get(dtype)
+        if dt is None:
+            raise InvalidArgument("dtype must be 'f32' or 'f64'")
+        arr = np.asarray(self.dims, dtype=np.int64)
+        h = _capi.ctx_p()
+        _check(lib.gcpb_create(device, dt, self.d, _i64(arr), self.rank, C.byref(h)))
+        self._h = h
+        self.total = math.prod(self.dims)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.gcpb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _ck(self, rc: int) -> None:
+        _check(rc, self._h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---- tensor ------------------------------------------------------------
+    def set_sparse(self, coords, values) -> None:
+        coords = np.ascontiguousarray(coords, dtype=np.int64).reshape(-1, self.d)
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        if len(values) != len(coords):
+            raise InvalidArgument("sparse tensor: index/value count mismatch")
+        self._ck(lib.gcpb_set_sparse(self._h, len(values), _i64(coords), _f64(values)))
+
+    def set_sparse_device(self, keys_ptr: int, values_ptr: int, nnz: int, value_dtype: str) -> None:
+        vd = _capi.F32 if value_dtype == "f32" else _capi.F64
+        self._ck(lib.gcpb_set_sparse_device(self._h, int(nnz), C.c_void_p(keys_ptr),
+                                            C.c_void_p(values_ptr), vd))
+
+    @property
+    def nnz(self) -> int:
+        return int(lib.gcpb_nnz(self._h))
+
+    def get_sparse(self):
+        n = self.nnz
+        coords = np.zeros((n, self.d), dtype=np.int64)
+        vals = np.zeros(n, dtype=np.float64)
+        self._ck(lib.gcpb_get_sparse(self._h, _i64(coords), _f64(vals)))
+        return coords, vals
+
+    def set_dense(self, values, storage: str = "f64") -> None:
+        st = {"u8": _capi.STORE_U8, "f32": _capi.STORE_F32, "f64": _capi.STORE_F64}[storage]
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        if v.size != self.total:
+            raise InvalidArgument("dense tensor: value count mismatch")
+        self._ck(lib.gcpb_set_dense(self._h, _f64(v), st))
+
+    def generate_dense_bernoulli(self, true_factors: Sequence[np.ndarray], seed: int) -> None:
+        R = true_factors[0].shape[1]
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(f, np.float64).reshape(-1)
+                                                    for f in true_factors]))
+        self._ck(lib.gcpb_generate_dense_bernoulli(self._h, R, _f64(flat), seed))
+
+    def tensor_norm(self) -> float:
+        out = C.c_double()
+        self._ck(lib.gcpb_tensor_norm(self._h, C.byref(out)))
+        return out.value
+
+    def value_at(self, idx) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, self.d)
+        out = np.zeros(len(idx), dtype=np.float64)
+        self._ck(lib.gcpb_value_at(self._h, len(idx), _i64(idx), _f64(out)))
+        return out
+
+    # ---- factors / gradient / moments --------------------------------------
+    def _mode_sizes(self):
+        return [n * self.rank for n in self.dims]
+
+    def _split(self, flat):
+        out, at = [], 0
+        for n in self.dims:
+            out.append(flat[at:at + n * self.rank].reshape(n, self.rank))
+            at += n * self.rank
+        return out
+
+    def _flat(self, mats):
+        if len(mats) != self.d:
+            raise InvalidArgument("expected one matrix per mode")
+        for k, m in enumerate(mats):
+            if np.shape(m) != (self.dims[k], self.rank):
+                raise InvalidArgument(f"mode {k}: expected shape {(self.dims[k], self.rank)}")
+        return np.ascontiguousarray(np.concatenate([np.asarray(m, np.float64).reshape(-1)
+                                                    for m in mats]))
+
+    def set_factors(self, mats) -> None:
+        self._ck(lib.gcpb_set_factors(self._h, -1, _f64(self._flat(mats))))
+
+    def factors(self):
+        flat = np.zeros(sum(self._mode_sizes()), dtype=np.float64)
+        self._ck(lib.gcpb_get_factors(self._h, -1, _f64(flat)))
+        return self._split(flat)
+
+    def grad(self):
+        flat = np.zeros(sum(self._mode_sizes()), dtype=np.float64)
+        self._ck(lib.gcpb_get_grad(self._h, -1, _f64(flat)))
+        return self._split(flat)
+
+    def grad_flat(self) -> np.ndarray:
+        flat = np.zeros(sum(self._mode_sizes()), dtype=np.float64)
+        self._ck(lib.gcpb_get_grad(self._h, -1, _f64(flat)))
+        return flat
+
+    def set_grad(self, mats) -> None:
+        self._ck(lib.gcpb_set_grad(self._h, -1, _f64(self._flat(mats))))
+
+    def moment(self, which: int):
+        flat = np.zeros(sum(self._mode_sizes()), dtype=np.float64)
+        self._ck(lib.gcpb_get_moment(self._h, which, -1, _f64(flat)))
+        return self._split(flat)
+
+    def set_moment(self, which: int, mats) -> None:
+        self._ck(lib.gcpb_set_moment(self._h, which, -1, _f64(self._flat(mats))))
+
+    # ---- hot path ------------------------------------------------------------
+    def stoch_grad(self, sampler: SamplerKind, loss: LossFunction, seed: int, it: int,
+                   want_stats: bool = True) -> Optional[RejectionStats]:
+        sk, ls = sampler.c(), loss.c()
+        st = _capi.gcpb_stats()
+        self._ck(lib.gcpb_stoch_grad(self._h, C.byref(sk), C.byref(ls), seed, it,
+                                     C.byref(st) if want_stats else None))
+        return RejectionStats(st.tested, st.accepted, st.rejected) if want_stats else None
+
+    def draw_samples(self, sampler: SamplerKind, loss: LossFunction, seed: int, it: int):
+        n = sampler.total()
+        idx = np.zeros((max(n, 1), self.d), dtype=np.int64)
+        x, w, m, y = (np.zeros(max(n, 1)) for _ in range(4))
+        flag = np.zeros(max(n, 1), dtype=np.int32)
+        nout = C.c_int64()
+        st = _capi.gcpb_stats()
+        sk, ls = sampler.c(), loss.c()
+        self._ck(lib.gcpb_draw_samples(self._h, C.byref(sk), C.byref(ls), seed, it, n, _i64(idx),
+                                       _f64(x), _f64(w), _i32(flag), _f64(m), _f64(y),
+                                       C.byref(nout), C.byref(st)))
+        k = nout.value
+        return dict(idx=idx[:k], x=x[:k], w=w[:k], flag=flag[:k], m=m[:k], y=y[:k],
+                    stats=RejectionStats(st.tested, st.accepted, st.rejected))
+
+    def eval_deriv(self, idx, x, w, loss: LossFunction, flags=None):
+        idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, self.d)
+        n = len(idx)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.int32)
+        m = np.zeros(n)
+        y = np.zeros(n)
+        ls = loss.c()
+        self._ck(lib.gcpb_eval_deriv(self._h, n, _i64(idx), _f64(x), _f64(w),
+                                     _i32(fl) if fl is not None else None, C.byref(ls),
+                                     _f64(m), _f64(y)))
+        return m, y
+
+    def mttkrp_samples(self, idx, y) -> None:
+        idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, self.d)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        self._ck(lib.gcpb_mttkrp_samples(self._h, len(idx), _i64(idx), _f64(y)))
+
+    # ---- optimizer -------------------------------------------------------------
+    def adam_step(self, learning_rate: float, beta1=0.9, beta2=0.999, epsilon=1e-8,
+                  lower_bound: Optional[float] = None) -> None:
+        a = _capi.gcpb_adam(learning_rate, beta1, beta2, epsilon,
+                            0 if lower_bound is None else 1,
+                            0.0 if lower_bound is None else float(lower_bound))
+        self._ck(lib.gcpb_adam_step(self._h, C.byref(a)))
+
+    def adam_reset(self) -> None:
+        self._ck(lib.gcpb_adam_reset(self._h))
+
+    @property
+    def iterations(self) -> int:
+        self.synchronize()
+        v = C.c_int64()
+        self._ck(lib.gcpb_get_iterations(self._h, C.byref(v)))
+        return v.value
+
+    @iterations.setter
+    def iterations(self, t: int) -> None:
+        self._ck(lib.gcpb_set_iterations(self._h, int(t)))
+
+    # ---- estimator ---------------------------------------------------------------
+    def estimator_set(self, idx, x, w) -> None:
+        idx = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1, self.d)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        self._ck(lib.gcpb_estimator_set(self._h, len(idx), _i64(idx), _f64(x), _f64(w)))
+
+    def estimator_draw(self, kind: int, count: int, seed: int, rho: float = 1.1) -> None:
+        self._ck(lib.gcpb_estimator_draw(self._h, kind, count, rho, seed))
+
+    def estimator_get(self):
+        n = int(lib.gcpb_estimator_size(self._h))
+        idx = np.zeros((max(n, 1), self.d), dtype=np.int64)
+        x = np.zeros(max(n, 1))
+        w = np.zeros(max(n, 1))
+        self._ck(lib.gcpb_estimator_get(self._h, _i64(idx), _f64(x), _f64(w)))
+        return idx[:n], x[:n], w[:n]
+
+    def estimate(self, loss: LossFunction) -> float:
+        out = C.c_double()
+        ls = loss.c()
+        self._ck(lib.gcpb_estimate(self._h, C.byref(ls), C.byref(out)))
+        return out.value
+
+    # ---- snapshots / multi-GPU -------------------------------------------------------
+    def synchronize(self) -> None:
+        out = C.c_int64()
+        self._ck(lib.gcpb_get_iterations(self._h, C.byref(out)))  # syncs the stream
+
+    def snapshot_save(self) -> None:
+        self._ck(lib.gcpb_snapshot_save(self._h))
+
+    def snapshot_restore(self) -> None:
+        self._ck(lib.gcpb_snapshot_restore(self._h))
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        self._ck(lib.gcpb_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def set_shard(self, rank: int, nranks: int) -> None:
+        self._ck(lib.gcpb_set_shard(self._h, rank, nranks))
+
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        self._ck(lib.gcpb_comm_init(self._h, unique_id, rank, nranks))
+
+    def allreduce_grad(self) -> None:
+        self._ck(lib.gcpb_allreduce_grad(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.gcpb_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ---------------------------------------------------------------------------
+# Host-only helpers
+# ---------------------------------------------------------------------------
+def philox_bounded(seed: int, tag: int, it: int, t: int, slot: int, n: int) -> int:
+    return int(lib.gcpb_philox_bounded(seed, tag, it, t, slot, n))
+
+
+def zero_batch_size(total: float, zeta: float, rho: float, shortfall: int) -> int:
+    return int(lib.gcpb_zero_batch_size(total, zeta, rho, shortfall))
+
+
+def shard_range(n: int, rank: int, nranks: int) -> tuple[int, int]:
+    b, e = C.c_int64(), C.c_int64()
+    lib.gcpb_shard_range(n, rank, nranks, C.byref(b), C.byref(e))
+    return b.value, e.value
+
+
+def stratified_keep(accepted_per_rank: Sequence[int], rank: int, need: int) -> tuple[int, int]:
+    arr = np.ascontiguousarray(accepted_per_rank, dtype=np.int64)
+    off, keep = C.c_int64(), C.c_int64()
+    lib.gcpb_stratified_keep(_i64(arr), len(arr), rank, need, C.byref(off), C.byref(keep))
+    return off.value, keep.value
+
+
+TAG_GRAD_UNIFORM, TAG_GRAD_NZ_PICK, TAG_GRAD_ZERO_CAND, TAG_GRAD_SEMI_Q = 1, 2, 3, 4
+TAG_EST_UNIFORM, TAG_EST_NZ_PICK, TAG_EST_ZERO_CAND = 5, 6, 7
