@@ -217,7 +217,10 @@ def run_ours(args, w):
             print(msg, file=sys.stderr, flush=True)
 
     e, F = setup_engine(w, local, log)
-    stream = torch.cuda.current_stream()
+    # A dedicated stream shared by the engine and the CUDA events (the legacy
+    # default stream would not order against the engine's non-blocking one).
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     e.set_stream(stream.cuda_stream)
     if world > 1:
         uid = [G.nccl_unique_id() if rank == 0 else None]
