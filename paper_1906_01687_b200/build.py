@@ -22,8 +22,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "_build"
-LIB = PKG / "libgcpb.so"
+OBJ = PKG / os.environ.get("GCPB_OBJDIR", "_build")
+LIB = Path(os.environ.get("GCPB_LIB", PKG / "libgcpb.so"))
 REFERENCE = Path("/root/reference/proj")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
@@ -56,7 +56,8 @@ def _compile(src: str, force: bool) -> tuple[str, bool]:
         deps.append(ROOT / "include" / "gcpb.h")
     if not force and not _stale(o, deps):
         return src, False
-    cmd = [NVCC, *NVFLAGS, "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
+    extra = os.environ.get("GCPB_NVFLAGS", "").split()
+    cmd = [NVCC, *NVFLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

@@ -162,6 +162,10 @@ struct gcpb_ctx {
   std::string err;
 
   DBuf A, Gr, B, C, As, Bs, Cs;
+  DBuf Grep;            // privatized gradient replicas (L2-resident), zero at rest
+  int nrep = 1;         // replicas used by the current call
+  int nrep_cap = 1;     // replicas allocated
+  int64_t rep_stride = 0;
   DBuf dstate;
   DevState host_state{};
   double* pinned_params = nullptr;  // pinned staging block for Adam scalars
@@ -174,7 +178,8 @@ struct gcpb_ctx {
   int dense_storage = GCPB_STORE_F64;
   DBuf dense;
   int64_t nnz = 0;
-  DBuf coo, vals, keys;
+  DBuf nzrec, vals, keys;  // AoS nonzero records, values, sorted linear keys
+  int rec_words = 4;
   DBuf hkeys, hvals;
   uint64_t hmask = 0;
   bool hash_ready = false;
@@ -397,6 +402,8 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   std::memset(&a, 0, sizeof(a));
   a.A = c->A.as<T>();
   a.G = c->Gr.as<T>();
+  a.nrep = 1;
+  a.rep_stride = c->rep_stride;
   a.d = c->d;
   a.rp = static_cast<int>(c->rp);
   a.nchunks = static_cast<int>((c->r + c->vw - 1) / c->vw);
@@ -419,8 +426,8 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     a.dense = c->dense.p;
   } else if (c->tensor_kind == 2) {
     a.xkind = X_SPARSE;
-    a.coo = c->coo.as<int32_t>();
-    a.coo_stride = c->nnz;
+    a.nzrec = c->nzrec.as<uint32_t>();
+    a.rec_words = c->rec_words;
     a.vals = c->vals.as<T>();
     a.eta = static_cast<uint64_t>(c->nnz);
     a.thr_eta = c->nnz > 0 && static_cast<uint64_t>(c->nnz) <= (1ull << 32)
@@ -449,10 +456,37 @@ int64_t finish_segments(FusedArgs<T>& a) {
   return tiles;
 }
 
+// Replicas worth using for a scatter of n samples: contention scales with the
+// updates per 16-byte gradient chunk; one replica per ~4 updates per chunk,
+// capped by what is allocated (GCPB_REPLICAS forces the count).
+int replicas_for(const gcpb_ctx* c, int64_t n) {
+  if (c->nrep_cap < 2) return 1;
+  static const int forced = [] {
+    const char* e = getenv("GCPB_REPLICAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return std::min(forced, c->nrep_cap);
+  const int64_t chunks = std::max<int64_t>(1, c->nelem / c->vw);
+  const int64_t want = n / (4 * chunks);
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, c->nrep_cap)));
+}
+
 template <typename T>
 void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record) {
   const int64_t tiles = finish_segments(a);
+  if (a.scatter) {
+    int64_t n = 0;
+    for (int s = 0; s < a.nseg; ++s) n += std::max<int64_t>(0, a.seg[s].t_end - a.seg[s].t_begin);
+    c->nrep = replicas_for(c, n);
+    a.nrep = c->nrep;
+    a.G = c->nrep > 1 ? c->Grep.as<T>() : c->Gr.as<T>();
+  }
   CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms));
+  if (a.scatter && c->nrep > 1) {
+    grad_reduce_kernel<T><<<grid_for(c->nelem, 256, c->num_sms, 4), 256, 0, c->stream>>>(
+        c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride);
+    CK(cudaGetLastError());
+  }
 }
 
 Seg make_seg(int kind, uint32_t tag, int64_t tb, int64_t te, double w, int flag, int64_t out) {
@@ -668,6 +702,13 @@ void estimate_launch(gcpb_ctx* c, const gcpb_loss* loss) {
   CK(cudaGetLastError());
 }
 
+int record_words(int d, size_t tsize) {
+  const int need = static_cast<int>(tsize / 4) + d;
+  int w = 4;
+  while (w < need) w <<= 1;
+  return w;
+}
+
 void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
                            const std::vector<double>& values) {
   const int64_t n = static_cast<int64_t>(keys.size());
@@ -676,39 +717,33 @@ void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
   c->hash_ready = false;
   c->domain_flags = -1;
   c->dense.reset();
+  c->rec_words = record_words(c->d, c->tsize);
   const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
   c->keys.alloc(nn * sizeof(uint64_t));
-  c->coo.alloc(nn * c->d * sizeof(int32_t));
+  c->nzrec.alloc(nn * c->rec_words * sizeof(uint32_t));
   c->vals.alloc(nn * c->tsize);
-  std::vector<int32_t> coo(nn * c->d);
-  for (int64_t e = 0; e < n; ++e) {
-    uint64_t rem = keys[e];
-    for (int k = 0; k < c->d; ++k) {
-      coo[k * n + e] = static_cast<int32_t>(rem % static_cast<uint64_t>(c->dims[k]));
-      rem /= static_cast<uint64_t>(c->dims[k]);
-    }
-  }
   if (n > 0) {
+    DBuf dv;
+    dv.alloc(n * sizeof(double));
     CK(cudaMemcpyAsync(c->keys.p, keys.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice,
                        c->stream));
-    CK(cudaMemcpyAsync(c->coo.p, coo.data(), n * c->d * sizeof(int32_t), cudaMemcpyHostToDevice,
+    CK(cudaMemcpyAsync(dv.p, values.data(), n * sizeof(double), cudaMemcpyHostToDevice,
                        c->stream));
-    if (c->dtype == GCPB_F32) {
-      std::vector<float> v(values.begin(), values.end());
-      CK(cudaMemcpyAsync(c->vals.p, v.data(), n * sizeof(float), cudaMemcpyHostToDevice,
-                         c->stream));
-      c->sync();
-    } else {
-      CK(cudaMemcpyAsync(c->vals.p, values.data(), n * sizeof(double), cudaMemcpyHostToDevice,
-                         c->stream));
-    }
+    const int g = grid_for(n, 256, c->num_sms);
+    if (c->dtype == GCPB_F32)
+      keys_to_records_kernel<double, float><<<g, 256, 0, c->stream>>>(
+          c->keys.as<uint64_t>(), dv.as<double>(), n, c->d, c->dims_dev.as<int64_t>(),
+          c->nzrec.as<uint32_t>(), c->rec_words, c->vals.as<float>());
+    else
+      keys_to_records_kernel<double, double><<<g, 256, 0, c->stream>>>(
+          c->keys.as<uint64_t>(), dv.as<double>(), n, c->d, c->dims_dev.as<int64_t>(),
+          c->nzrec.as<uint32_t>(), c->rec_words, c->vals.as<double>());
+    CK(cudaGetLastError());
+    c->sync();
   }
   c->sync();
 }
 
-}  // namespace
-
-namespace {
 template <typename T>
 void given_launch(gcpb_ctx* c, int64_t n, const gcpb_loss* loss, bool y_given, bool record,
                   bool scatter) {
@@ -730,6 +765,7 @@ void given_launch(gcpb_ctx* c, int64_t n, const gcpb_loss* loss, bool y_given, b
   a.seg[0] = make_seg(SEG_GIVEN, 0, 0, n, 0.0, 0, 0);
   run_fused(c, a, record);
 }
+
 }  // namespace
 
 // ===========================================================================
@@ -795,6 +831,24 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
       CK(cudaMemsetAsync(b->p, 0, bytes, c->stream));
     }
     c->grad_zero = true;
+    // Privatized gradient replicas: the scatter of a small gradient (e.g. C2's
+    // 51 KB) otherwise funnels every red.global into a few hundred L2 sectors,
+    // where the L2 atomic units serialise per address.  Up to 32 replicas are
+    // allocated when they fit in 16 MB of L2; each call uses as many as its
+    // contention warrants (replicas_for()).
+    {
+      const int64_t rs = (c->nelem + 63) / 64 * 64;
+      int64_t cap = static_cast<int64_t>(16) * 1024 * 1024 / std::max<int64_t>(1, rs * c->tsize);
+      cap = std::min<int64_t>(cap, 32);
+      if (const char* ev = getenv("GCPB_REPLICAS")) cap = std::max(1, atoi(ev));
+      if (cap >= 2) {
+        c->nrep_cap = static_cast<int>(cap);
+        c->rep_stride = rs;
+        c->Grep.alloc(static_cast<size_t>(rs) * cap * c->tsize);
+        CK(cudaMemsetAsync(c->Grep.p, 0, static_cast<size_t>(rs) * cap * c->tsize, c->stream));
+      }
+    }
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);  // random gathers: 32-byte sectors
     c->dstate.alloc(sizeof(DevState));
     CK(cudaMallocHost(reinterpret_cast<void**>(&c->pinned_params), 8 * sizeof(double)));
     std::memset(&c->host_state, 0, sizeof(DevState));
@@ -870,8 +924,9 @@ int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_so
     ctx->domain_flags = -1;
     ctx->dense.reset();
     const size_t nn = static_cast<size_t>(std::max<int64_t>(nnz, 1));
+    ctx->rec_words = record_words(ctx->d, ctx->tsize);
     ctx->keys.alloc(nn * sizeof(uint64_t));
-    ctx->coo.alloc(nn * ctx->d * sizeof(int32_t));
+    ctx->nzrec.alloc(nn * ctx->rec_words * sizeof(uint32_t));
     ctx->vals.alloc(nn * ctx->tsize);
     if (nnz > 0) {
       CK(cudaMemcpyAsync(ctx->keys.p, d_keys_sorted, nnz * sizeof(uint64_t),
@@ -893,23 +948,27 @@ int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_so
       if (flags & 1u) throw std::out_of_range("sparse tensor: linear key out of range");
       if (flags & 2u) throw std::invalid_argument("device ingest requires strictly increasing keys");
       if (flags & 4u) throw std::invalid_argument("device ingest requires nonzero values");
-      keys_to_coo_kernel<<<g, 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), nnz, ctx->d,
-                                                     ctx->dims_dev.as<int64_t>(),
-                                                     ctx->coo.as<int32_t>());
+      const int64_t* dd = ctx->dims_dev.as<int64_t>();
+      uint32_t* rec = ctx->nzrec.as<uint32_t>();
+      const uint64_t* kk = ctx->keys.as<uint64_t>();
       if (ctx->dtype == GCPB_F32) {
         if (value_dtype == GCPB_F32)
-          convert_kernel<float, float><<<g, 256, 0, ctx->stream>>>(
-              static_cast<const float*>(d_values), ctx->vals.as<float>(), nnz);
+          keys_to_records_kernel<float, float><<<g, 256, 0, ctx->stream>>>(
+              kk, static_cast<const float*>(d_values), nnz, ctx->d, dd, rec, ctx->rec_words,
+              ctx->vals.as<float>());
         else
-          convert_kernel<double, float><<<g, 256, 0, ctx->stream>>>(
-              static_cast<const double*>(d_values), ctx->vals.as<float>(), nnz);
+          keys_to_records_kernel<double, float><<<g, 256, 0, ctx->stream>>>(
+              kk, static_cast<const double*>(d_values), nnz, ctx->d, dd, rec, ctx->rec_words,
+              ctx->vals.as<float>());
       } else {
         if (value_dtype == GCPB_F32)
-          convert_kernel<float, double><<<g, 256, 0, ctx->stream>>>(
-              static_cast<const float*>(d_values), ctx->vals.as<double>(), nnz);
+          keys_to_records_kernel<float, double><<<g, 256, 0, ctx->stream>>>(
+              kk, static_cast<const float*>(d_values), nnz, ctx->d, dd, rec, ctx->rec_words,
+              ctx->vals.as<double>());
         else
-          convert_kernel<double, double><<<g, 256, 0, ctx->stream>>>(
-              static_cast<const double*>(d_values), ctx->vals.as<double>(), nnz);
+          keys_to_records_kernel<double, double><<<g, 256, 0, ctx->stream>>>(
+              kk, static_cast<const double*>(d_values), nnz, ctx->d, dd, rec, ctx->rec_words,
+              ctx->vals.as<double>());
       }
       CK(cudaGetLastError());
     }

@@ -281,6 +281,22 @@ __global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict
   }
 }
 
+// G = sum of the nrep privatized gradient replicas; replicas re-zeroed.
+template <typename T>
+__global__ void grad_reduce_kernel(T* __restrict__ G, T* __restrict__ reps, int64_t n,
+                                   int nrep, int64_t stride) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    T s = static_cast<T>(0);
+    for (int r = 0; r < nrep; ++r) {
+      T* p = reps + r * stride + i;
+      s += *p;
+      *p = static_cast<T>(0);
+    }
+    G[i] = s;
+  }
+}
+
 template <typename T>
 struct ModelDesc {
   const T* A;
@@ -370,17 +386,29 @@ __global__ void gen_bernoulli_kernel(uint8_t* __restrict__ out, int d, const int
   }
 }
 
-// COO SoA coordinates from sorted linear keys (multi_index, shape.cpp:98-109).
-__global__ void keys_to_coo_kernel(const uint64_t* __restrict__ keys, int64_t n, int d,
-                                   const int64_t* dims, int32_t* coo) {
+// Nonzero records from sorted linear keys (multi_index, shape.cpp:98-109) and
+// values: [value (T) | coords u32 x d | zero pad] of rec_words words each.
+template <typename V, typename T>
+__global__ void keys_to_records_kernel(const uint64_t* __restrict__ keys,
+                                       const V* __restrict__ vals_in, int64_t n, int d,
+                                       const int64_t* dims, uint32_t* rec, int rec_words,
+                                       T* vals_out) {
+  constexpr int VWD = sizeof(T) / 4;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t* r = rec + e * rec_words;
+    const T v = static_cast<T>(vals_in[e]);
+    vals_out[e] = v;
+    uint32_t vw[2] = {0u, 0u};
+    memcpy(vw, &v, sizeof(T));
+    for (int w = 0; w < VWD; ++w) r[w] = vw[w];
     uint64_t rem = keys[e];
     for (int k = 0; k < d; ++k) {
       const uint64_t nk = static_cast<uint64_t>(dims[k]);
-      coo[k * n + e] = static_cast<int32_t>(rem % nk);
+      r[VWD + k] = static_cast<uint32_t>(rem % nk);
       rem /= nk;
     }
+    for (int w = VWD + d; w < rec_words; ++w) r[w] = 0u;
   }
 }
 

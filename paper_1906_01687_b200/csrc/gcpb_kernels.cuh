@@ -38,7 +38,9 @@ struct Seg {
 template <typename T>
 struct FusedArgs {
   const T* A;  // factors, mode k at A + off[k], row i at + i * rp
-  T* G;        // gradient, same layout
+  T* G;        // gradient (or nrep privatized replicas), same layout
+  int nrep;          // gradient replicas: block b accumulates into replica b % nrep
+  int64_t rep_stride;  // elements between replicas
   int d;
   int rp;      // padded row length (elements)
   int nchunks; // 16-byte chunks holding real columns: ceil(r / VW)
@@ -53,8 +55,8 @@ struct FusedArgs {
   // tensor access
   int xkind;
   const void* dense;
-  const int32_t* coo;  // SoA: coo[k * coo_stride + e]
-  int64_t coo_stride;
+  const uint32_t* nzrec;  // AoS nonzero records: [value (T) | coords (u32 x d) | pad]
+  int rec_words;          // words per record: 4, 8, 16 or 32 (16..128 bytes)
   const T* vals;
   uint64_t eta;        // global nonzero count (pick range)
   uint32_t thr_eta;
