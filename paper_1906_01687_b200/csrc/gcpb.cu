@@ -820,6 +820,8 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
     }
     c->off[ndims] = o;
     c->nelem = o;
+    if (o >= (int64_t{1} << 31))
+      throw std::invalid_argument("factor matrices exceed 2^31 padded elements (device path)");
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
