@@ -106,7 +106,8 @@ def setup_engine(w, device, log):
     e = G.Engine(w.dims, w.rank, dtype=w.dtype, device=device)
     t0 = time.perf_counter()
     if w.name == "c2":
-        e.generate_dense_bernoulli(WL.c2_true_factors(1002), seed=1002)
+        e.generate_dense_bernoulli(WL.c2_true_factors(1002), seed=1002,
+                                   storage=os.environ.get("GCPB_C2_STORAGE", "bit"))
     elif w.name == "c1":
         rs = np.random.default_rng(1001)
         A = [rs.standard_normal((n, 5)) for n in w.dims]

@@ -44,6 +44,8 @@ extern "C" {
 #define GCPB_STORE_U8 0
 #define GCPB_STORE_F32 1
 #define GCPB_STORE_F64 2
+/* Binary data, one bit per entry: bit (lin & 31) of u32 word lin >> 5. */
+#define GCPB_STORE_BIT 3
 
 /* LossKind, same order as include/gcp/loss.hpp:8-15. */
 #define GCPB_LOSS_GAUSSIAN 0
@@ -133,9 +135,10 @@ int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage);
 /* Synthetic dense binary tensor generated in HBM (BASELINE configs[1]):
  * x(i) ~ Bernoulli(m_i / (1 + m_i)) with m the rank-true_rank model given by
  * true_factors (double, flattened mode-major row-major), uniform from a
- * counter hash of (seed, linear index).  Stored as U8. */
+ * counter hash of (seed, linear index).  storage: GCPB_STORE_U8 or
+ * GCPB_STORE_BIT (same values). */
 int gcpb_generate_dense_bernoulli(gcpb_ctx* ctx, int64_t true_rank, const double* true_factors,
-                                  uint64_t seed);
+                                  uint64_t seed, int storage);
 /* TensorView::norm (src/tensor.cpp:56-60,70-74): Frobenius norm of the data,
  * fp64 accumulation. */
 int gcpb_tensor_norm(gcpb_ctx* ctx, double* out);

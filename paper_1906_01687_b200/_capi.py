@@ -21,7 +21,7 @@ lib = C.CDLL(str(_LIB_PATH))
 # status codes (gcpb.h)
 OK, ERR_RUNTIME, ERR_USAGE, ERR_DOMAIN, ERR_RANGE, ERR_LOGIC = 0, 1, 2, 3, 4, 5
 F32, F64 = 0, 1
-STORE_U8, STORE_F32, STORE_F64 = 0, 1, 2
+STORE_U8, STORE_F32, STORE_F64, STORE_BIT = 0, 1, 2, 3
 UNIFORM, STRATIFIED, SEMI_STRATIFIED = 0, 1, 2
 EST_UNIFORM, EST_STRATIFIED = 0, 1
 
@@ -66,7 +66,7 @@ SIGNATURES = [
     ("gcpb_get_sparse", C.c_int, [ctx_p, i64p, f64p]),
     ("gcpb_set_dense", C.c_int, [ctx_p, f64p, C.c_int]),
     ("gcpb_set_dense_device", C.c_int, [ctx_p, C.c_void_p, C.c_int]),
-    ("gcpb_generate_dense_bernoulli", C.c_int, [ctx_p, C.c_int64, f64p, C.c_uint64]),
+    ("gcpb_generate_dense_bernoulli", C.c_int, [ctx_p, C.c_int64, f64p, C.c_uint64, C.c_int]),
     ("gcpb_tensor_norm", C.c_int, [ctx_p, f64p]),
     ("gcpb_value_at", C.c_int, [ctx_p, C.c_int64, i64p, f64p]),
     ("gcpb_set_factors", C.c_int, [ctx_p, C.c_int, f64p]),

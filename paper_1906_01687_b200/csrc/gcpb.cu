@@ -137,6 +137,17 @@ std::string u128_to_string(unsigned __int128 v) {
   return s;
 }
 
+// Bytes of dense storage for n entries.
+size_t dense_bytes(int storage, uint64_t n) {
+  switch (storage) {
+    case GCPB_STORE_U8: return n;
+    case GCPB_STORE_F32: return n * 4;
+    case GCPB_STORE_F64: return n * 8;
+    case GCPB_STORE_BIT: return (n + 31) / 32 * 4;
+  }
+  throw std::invalid_argument("unknown dense storage");
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -369,7 +380,9 @@ void check_data_domain(gcpb_ctx* c, int loss_kind) {
       }
     } else {
       const int64_t n = static_cast<int64_t>(c->total);
-      if (c->dense_storage == GCPB_STORE_U8)
+      if (c->dense_storage == GCPB_STORE_BIT)
+        ;  // values are 0/1 by construction
+      else if (c->dense_storage == GCPB_STORE_U8)
         domain_scan_kernel<uint8_t><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
             c->dense.as<uint8_t>(), n, f);
       else if (c->dense_storage == GCPB_STORE_F32)
@@ -420,9 +433,11 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   a.seed = seed;
   a.iter = iter;
   if (c->tensor_kind == 1) {
-    a.xkind = c->dense_storage == GCPB_STORE_U8
-                  ? X_DENSE_U8
-                  : (c->dense_storage == GCPB_STORE_F32 ? X_DENSE_F32 : X_DENSE_F64);
+    a.xkind = c->dense_storage == GCPB_STORE_BIT
+                  ? X_DENSE_BIT
+                  : (c->dense_storage == GCPB_STORE_U8
+                         ? X_DENSE_U8
+                         : (c->dense_storage == GCPB_STORE_F32 ? X_DENSE_F32 : X_DENSE_F64));
     a.dense = c->dense.p;
   } else if (c->tensor_kind == 2) {
     a.xkind = X_SPARSE;
@@ -1015,24 +1030,31 @@ int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage) {
     if (!ctx->total_fits || ctx->total > (uint64_t{1} << 40))
       throw std::invalid_argument("dense tensor too large to materialize");
     const uint64_t n = ctx->total;
-    size_t es = storage == GCPB_STORE_U8 ? 1 : (storage == GCPB_STORE_F32 ? 4 : 8);
-    if (storage < 0 || storage > 2) throw std::invalid_argument("unknown dense storage");
-    std::vector<unsigned char> host(n * es);
+    const size_t bytes = dense_bytes(storage, n);
+    std::vector<unsigned char> host(bytes, 0);
     for (uint64_t i = 0; i < n; ++i) {
       const double v = values[i];
-      if (storage == GCPB_STORE_U8) {
-        if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v)))
-          throw std::invalid_argument("U8 dense storage needs integers in [0, 255]");
-        host[i] = static_cast<unsigned char>(v);
-      } else if (storage == GCPB_STORE_F32) {
-        const float f = static_cast<float>(v);
-        std::memcpy(&host[i * 4], &f, 4);
-      } else {
-        std::memcpy(&host[i * 8], &v, 8);
+      switch (storage) {
+        case GCPB_STORE_U8:
+          if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v)))
+            throw std::invalid_argument("U8 dense storage needs integers in [0, 255]");
+          host[i] = static_cast<unsigned char>(v);
+          break;
+        case GCPB_STORE_BIT:
+          if (v != 0.0 && v != 1.0) throw std::invalid_argument("BIT dense storage needs 0/1 data");
+          if (v == 1.0) host[i >> 3] |= static_cast<unsigned char>(1u << (i & 7));
+          break;
+        case GCPB_STORE_F32: {
+          const float f = static_cast<float>(v);
+          std::memcpy(&host[i * 4], &f, 4);
+          break;
+        }
+        default:
+          std::memcpy(&host[i * 8], &v, 8);
       }
     }
-    ctx->dense.alloc(n * es);
-    CK(cudaMemcpyAsync(ctx->dense.p, host.data(), n * es, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->dense.alloc(bytes);
+    CK(cudaMemcpyAsync(ctx->dense.p, host.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
     ctx->sync();
     ctx->dense_storage = storage;
     ctx->tensor_kind = 1;
@@ -1044,11 +1066,9 @@ int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage) {
 int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage) {
   return guard(ctx, [&] {
     if (!ctx->total_fits) throw std::invalid_argument("dense tensor too large to materialize");
-    if (storage < 0 || storage > 2) throw std::invalid_argument("unknown dense storage");
-    const size_t es = storage == GCPB_STORE_U8 ? 1 : (storage == GCPB_STORE_F32 ? 4 : 8);
-    ctx->dense.alloc(ctx->total * es);
-    CK(cudaMemcpyAsync(ctx->dense.p, d_values, ctx->total * es, cudaMemcpyDeviceToDevice,
-                       ctx->stream));
+    const size_t bytes = dense_bytes(storage, ctx->total);
+    ctx->dense.alloc(bytes);
+    CK(cudaMemcpyAsync(ctx->dense.p, d_values, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
     ctx->sync();
     ctx->dense_storage = storage;
     ctx->tensor_kind = 1;
@@ -1058,10 +1078,12 @@ int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage) {
 }
 
 int gcpb_generate_dense_bernoulli(gcpb_ctx* ctx, int64_t true_rank, const double* true_factors,
-                                  uint64_t seed) {
+                                  uint64_t seed, int storage) {
   return guard(ctx, [&] {
     if (!ctx->total_fits) throw std::invalid_argument("dense tensor too large to materialize");
     if (true_rank < 1 || true_rank > 1024) throw std::invalid_argument("true rank out of range");
+    if (storage != GCPB_STORE_U8 && storage != GCPB_STORE_BIT)
+      throw std::invalid_argument("binary generator stores U8 or BIT");
     int64_t foff[kMaxModes] = {};
     int64_t tot = 0;
     for (int k = 0; k < ctx->d; ++k) {
@@ -1073,15 +1095,24 @@ int gcpb_generate_dense_bernoulli(gcpb_ctx* ctx, int64_t true_rank, const double
     fo.alloc(kMaxModes * sizeof(int64_t));
     CK(cudaMemcpyAsync(F.p, true_factors, tot * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(fo.p, foff, sizeof(foff), cudaMemcpyHostToDevice, ctx->stream));
-    ctx->dense.alloc(ctx->total);
-    const int64_t nfibers = static_cast<int64_t>(ctx->total / static_cast<uint64_t>(ctx->dims[0]));
-    const size_t smem = 8 * true_rank * sizeof(double);
-    gen_bernoulli_kernel<<<grid_for(nfibers * 32, 256, ctx->num_sms, 8), 256, smem, ctx->stream>>>(
-        ctx->dense.as<uint8_t>(), ctx->d, ctx->dims_dev.as<int64_t>(), fo.as<int64_t>(),
-        static_cast<int>(true_rank), F.as<double>(), seed, nfibers);
+    ctx->dense.alloc(dense_bytes(storage, ctx->total));
+    if (storage == GCPB_STORE_U8) {
+      const int64_t nfibers = static_cast<int64_t>(ctx->total / static_cast<uint64_t>(ctx->dims[0]));
+      const size_t smem = 8 * true_rank * sizeof(double);
+      gen_bernoulli_kernel<<<grid_for(nfibers * 32, 256, ctx->num_sms, 8), 256, smem,
+                             ctx->stream>>>(ctx->dense.as<uint8_t>(), ctx->d,
+                                            ctx->dims_dev.as<int64_t>(), fo.as<int64_t>(),
+                                            static_cast<int>(true_rank), F.as<double>(), seed,
+                                            nfibers);
+    } else {
+      const int64_t nwords = static_cast<int64_t>((ctx->total + 31) / 32);
+      gen_bernoulli_bits_kernel<<<grid_for(nwords, 256, ctx->num_sms, 16), 256, 0, ctx->stream>>>(
+          ctx->dense.as<uint32_t>(), ctx->d, ctx->dims_dev.as<int64_t>(), fo.as<int64_t>(),
+          static_cast<int>(true_rank), F.as<double>(), seed, ctx->total);
+    }
     CK(cudaGetLastError());
     ctx->sync();
-    ctx->dense_storage = GCPB_STORE_U8;
+    ctx->dense_storage = storage;
     ctx->tensor_kind = 1;
     ctx->nnz = 0;
     ctx->domain_flags = -1;
@@ -1102,7 +1133,10 @@ int gcpb_tensor_norm(gcpb_ctx* ctx, double* out) {
         sumsq_kernel<double><<<kGrid, 256, 0, ctx->stream>>>(ctx->vals.as<double>(), ctx->nnz, parts);
     } else {
       const int64_t n = static_cast<int64_t>(ctx->total);
-      if (ctx->dense_storage == GCPB_STORE_U8)
+      if (ctx->dense_storage == GCPB_STORE_BIT)
+        popcount_kernel<<<kGrid, 256, 0, ctx->stream>>>(ctx->dense.as<uint32_t>(), (n + 31) / 32,
+                                                        parts);
+      else if (ctx->dense_storage == GCPB_STORE_U8)
         sumsq_kernel<uint8_t><<<kGrid, 256, 0, ctx->stream>>>(ctx->dense.as<uint8_t>(), n, parts);
       else if (ctx->dense_storage == GCPB_STORE_F32)
         sumsq_kernel<float><<<kGrid, 256, 0, ctx->stream>>>(ctx->dense.as<float>(), n, parts);
@@ -1123,10 +1157,7 @@ int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out) {
     if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
     for (int64_t e = 0; e < n; ++e) check_index_host(ctx, idx + e * ctx->d);
     if (n == 0) return;
-    // Gathered with the same device access path the sampler uses: a GIVEN
-    // segment cannot look x up, so use a tiny uniform-free path: record x by
-    // evaluating a gaussian derivative with w = 0 would lose x; instead do a
-    // direct host-mirrored lookup on the device copy.
+    if (ctx->tensor_kind == 2) ensure_hash(ctx);
     std::vector<uint64_t> lin(static_cast<size_t>(n));
     for (int64_t e = 0; e < n; ++e) {
       uint64_t l = 0, s = 1;
@@ -1136,40 +1167,30 @@ int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out) {
       }
       lin[e] = l;
     }
-    if (ctx->tensor_kind == 1) {
-      const size_t es = ctx->dense_storage == GCPB_STORE_U8 ? 1 : (ctx->dense_storage == GCPB_STORE_F32 ? 4 : 8);
-      for (int64_t e = 0; e < n; ++e) {
-        unsigned char buf[8] = {};
-        CK(cudaMemcpyAsync(buf, ctx->dense.as<unsigned char>() + lin[e] * es, es,
-                           cudaMemcpyDeviceToHost, ctx->stream));
-        ctx->sync();
-        if (es == 1) x_out[e] = buf[0];
-        else if (es == 4) { float f; std::memcpy(&f, buf, 4); x_out[e] = f; }
-        else std::memcpy(&x_out[e], buf, 8);
-      }
-      return;
-    }
-    std::vector<uint64_t> keys(static_cast<size_t>(ctx->nnz));
-    if (ctx->nnz > 0)
-      CK(cudaMemcpyAsync(keys.data(), ctx->keys.p, ctx->nnz * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    DBuf dl, dx;
+    dl.alloc(n * 8);
+    dx.alloc(n * 8);
+    CK(cudaMemcpyAsync(dl.p, lin.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    int xkind = X_SPARSE;
+    if (ctx->tensor_kind == 1)
+      xkind = ctx->dense_storage == GCPB_STORE_BIT
+                  ? X_DENSE_BIT
+                  : (ctx->dense_storage == GCPB_STORE_U8
+                         ? X_DENSE_U8
+                         : (ctx->dense_storage == GCPB_STORE_F32 ? X_DENSE_F32 : X_DENSE_F64));
+    if (ctx->dtype == GCPB_F32)
+      value_at_kernel<float><<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+          dl.as<uint64_t>(), n, xkind, ctx->dense.p, ctx->vals.as<float>(),
+          ctx->hash_ready ? ctx->hkeys.as<uint64_t>() : nullptr, ctx->hvals.as<uint32_t>(),
+          ctx->hmask, dx.as<double>());
+    else
+      value_at_kernel<double><<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+          dl.as<uint64_t>(), n, xkind, ctx->dense.p, ctx->vals.as<double>(),
+          ctx->hash_ready ? ctx->hkeys.as<uint64_t>() : nullptr, ctx->hvals.as<uint32_t>(),
+          ctx->hmask, dx.as<double>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(x_out, dx.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
-    for (int64_t e = 0; e < n; ++e) {
-      const auto it = std::lower_bound(keys.begin(), keys.end(), lin[e]);
-      if (it == keys.end() || *it != lin[e]) {
-        x_out[e] = 0.0;
-        continue;
-      }
-      const int64_t pos = it - keys.begin();
-      if (ctx->dtype == GCPB_F32) {
-        float f;
-        CK(cudaMemcpyAsync(&f, ctx->vals.as<float>() + pos, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        ctx->sync();
-        x_out[e] = f;
-      } else {
-        CK(cudaMemcpyAsync(&x_out[e], ctx->vals.as<double>() + pos, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        ctx->sync();
-      }
-    }
   });
 }
 

@@ -386,6 +386,90 @@ __global__ void gen_bernoulli_kernel(uint8_t* __restrict__ out, int d, const int
   }
 }
 
+// Same tensor as gen_bernoulli_kernel, bit-packed: thread per 32-entry word.
+__global__ void gen_bernoulli_bits_kernel(uint32_t* __restrict__ out, int d, const int64_t* dims,
+                                          const int64_t* foff, int R,
+                                          const double* __restrict__ F, uint64_t seed,
+                                          uint64_t total) {
+  const uint64_t nwords = (total + 31) / 32;
+  for (uint64_t wi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; wi < nwords;
+       wi += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t bits = 0;
+    for (int j = 0; j < 32; ++j) {
+      const uint64_t lin = wi * 32 + j;
+      if (lin >= total) break;
+      const int64_t n0 = dims[0];
+      const int64_t i0 = static_cast<int64_t>(lin % static_cast<uint64_t>(n0));
+      const int64_t f = static_cast<int64_t>(lin / static_cast<uint64_t>(n0));
+      double m = 0.0;
+      for (int r = 0; r < R; ++r) {
+        double p = 1.0;
+        int64_t rem = f;
+        for (int k = 1; k < d; ++k) {
+          const int64_t ik = rem % dims[k];
+          rem /= dims[k];
+          p *= F[foff[k] + ik * R + r];
+        }
+        m += F[foff[0] + i0 * R + r] * p;
+      }
+      const double pr = m / (1.0 + m);
+      const U4 b = philox_block(seed, TAG_GENERATE, 0u, 0u, 0ull, lin);
+      const double u =
+          static_cast<double>(((static_cast<uint64_t>(b.x) << 32) | b.y) >> 11) * 0x1.0p-53;
+      if (u < pr) bits |= 1u << j;
+    }
+    out[wi] = bits;
+  }
+}
+
+__global__ void popcount_kernel(const uint32_t* __restrict__ w, int64_t n, double* partials) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    acc += __popc(w[e]);
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
+// TensorView::value_at on the device copy (parity helper).
+template <typename T>
+__global__ void value_at_kernel(const uint64_t* __restrict__ lin, int64_t n, int xkind,
+                                const void* dense, const T* vals, const uint64_t* hkeys,
+                                const uint32_t* hvals, uint64_t hmask, double* out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t l = lin[e];
+    double x = 0.0;
+    switch (xkind) {
+      case X_DENSE_BIT:
+        x = (static_cast<const uint32_t*>(dense)[l >> 5] >> (l & 31u)) & 1u;
+        break;
+      case X_DENSE_U8:
+        x = static_cast<const uint8_t*>(dense)[l];
+        break;
+      case X_DENSE_F32:
+        x = static_cast<const float*>(dense)[l];
+        break;
+      case X_DENSE_F64:
+        x = static_cast<const double*>(dense)[l];
+        break;
+      default: {
+        if (hkeys) {
+          const int64_t slot = hash_find(hkeys, hmask, l);
+          if (slot >= 0) x = static_cast<double>(vals[hvals[slot]]);
+        }
+      }
+    }
+    out[e] = x;
+  }
+}
+
 // Nonzero records from sorted linear keys (multi_index, shape.cpp:98-109) and
 // values: [value (T) | coords u32 x d | zero pad] of rec_words words each.
 template <typename V, typename T>

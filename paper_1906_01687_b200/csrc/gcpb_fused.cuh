@@ -144,6 +144,11 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
       for (int k = 0; k < DM; ++k)
         if (EXACT || k < d) lin += static_cast<uint64_t>(ik[k]) * a.stride[k];
       switch (a.xkind) {
+        case X_DENSE_BIT: {
+          const uint32_t w = ld_stream_u32(static_cast<const uint32_t*>(a.dense) + (lin >> 5));
+          s.x = static_cast<T>((w >> (lin & 31u)) & 1u);
+          break;
+        }
         case X_DENSE_U8:
           s.x = static_cast<T>(ld_stream_u8(static_cast<const uint8_t*>(a.dense) + lin));
           break;

@@ -12,7 +12,14 @@ constexpr int kMaxModes = 16;
 constexpr uint64_t kEmptyKey = ~0ull;
 
 // Data-access kinds for the tensor value x at a sampled index.
-enum XKind : int { X_NONE = 0, X_DENSE_U8 = 1, X_DENSE_F32 = 2, X_DENSE_F64 = 3, X_SPARSE = 4 };
+enum XKind : int {
+  X_NONE = 0,
+  X_DENSE_U8 = 1,
+  X_DENSE_F32 = 2,
+  X_DENSE_F64 = 3,
+  X_SPARSE = 4,
+  X_DENSE_BIT = 5
+};
 
 // Sample-segment kinds of one fused launch (in the reference's sample order).
 enum SegKind : int {
@@ -181,6 +188,11 @@ __device__ __forceinline__ void red_chunk(double* p, const double (&v)[2]) {
 __device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
   uint16_t v;
   asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ float ld_stream_f32(const float* p) {

@@ -298,17 +298,20 @@ class Engine:
         return coords, vals
 
     def set_dense(self, values, storage: str = "f64") -> None:
-        st = {"u8": _capi.STORE_U8, "f32": _capi.STORE_F32, "f64": _capi.STORE_F64}[storage]
+        st = {"u8": _capi.STORE_U8, "f32": _capi.STORE_F32, "f64": _capi.STORE_F64,
+              "bit": _capi.STORE_BIT}[storage]
         v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
         if v.size != self.total:
             raise InvalidArgument("dense tensor: value count mismatch")
         self._ck(lib.gcpb_set_dense(self._h, _f64(v), st))
 
-    def generate_dense_bernoulli(self, true_factors: Sequence[np.ndarray], seed: int) -> None:
+    def generate_dense_bernoulli(self, true_factors: Sequence[np.ndarray], seed: int,
+                                 storage: str = "bit") -> None:
         R = true_factors[0].shape[1]
         flat = np.ascontiguousarray(np.concatenate([np.asarray(f, np.float64).reshape(-1)
                                                     for f in true_factors]))
-        self._ck(lib.gcpb_generate_dense_bernoulli(self._h, R, _f64(flat), seed))
+        st = {"u8": _capi.STORE_U8, "bit": _capi.STORE_BIT}[storage]
+        self._ck(lib.gcpb_generate_dense_bernoulli(self._h, R, _f64(flat), seed, st))
 
     def tensor_norm(self) -> float:
         out = C.c_double()

@@ -436,3 +436,37 @@ def test_sharded_samples_sum_to_single_rank_gradient():
         e.stoch_grad(sk, lf, 3, 1)
         total += e.grad_flat()
     assert O.rel_error(total, want) <= 1e-12
+
+
+def test_bit_and_byte_storage_agree(orc):
+    """BIT-packed and U8 storage of the same generated binary tensor give the
+    same values and the same gradient; set_dense('bit') matches the oracle."""
+    g = G()
+    rs = np.random.default_rng(12)
+    dims, R, r = (33, 17, 9, 5), 3, 6
+    T = [rs.uniform(0, 1, (n, R)) for n in dims]
+    F = [rs.uniform(0.05, 1.0, (n, r)) for n in dims]
+    eb = g.Engine(dims, r, dtype="f64")
+    eu = g.Engine(dims, r, dtype="f64")
+    eb.generate_dense_bernoulli(T, seed=5, storage="bit")
+    eu.generate_dense_bernoulli(T, seed=5, storage="u8")
+    idx = np.stack([rs.integers(0, n, 4000) for n in dims], 1)
+    xb, xu = eb.value_at(idx), eu.value_at(idx)
+    assert np.array_equal(xb, xu) and set(np.unique(xb)) <= {0.0, 1.0} and xb.sum() > 0
+    assert eb.tensor_norm() == pytest.approx(eu.tensor_norm(), rel=1e-15)
+    for e in (eb, eu):
+        e.set_factors(F)
+        e.stoch_grad(g.SamplerKind.uniform(5000), g.LossFunction.bernoulli_odds(), 3, 1)
+    assert O.rel_error(eb.grad_flat(), eu.grad_flat()) <= 1e-12
+    # host-packed bits against the oracle
+    dense = (rs.random(int(np.prod(dims))) < 0.2).astype(float)
+    e = g.Engine(dims, r, dtype="f32")
+    e.set_dense(dense, "bit")
+    F32 = _as_dtype(F, "f32")
+    e.set_factors(F32)
+    e.stoch_grad(g.SamplerKind.uniform(3000), g.LossFunction.bernoulli_odds(), 8, 2)
+    rc, want = orc.draw_gradient_samples(O.Tensor(dims, dense=dense), r, F32, 2, 0.0, 0, 3000, 0,
+                                         0, 1.1, orc.source(1, seed=8, it=2))
+    assert rc == 0
+    grad = orc.mttkrp(dims, r, F32, want["idx"], want["y"])
+    assert O.rel_error(e.grad_flat(), grad) <= TOL["f32"]
