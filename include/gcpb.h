@@ -195,6 +195,60 @@ int gcpb_adam_reset(gcpb_ctx* ctx);
 int gcpb_get_iterations(gcpb_ctx* ctx, int64_t* out);
 int gcpb_set_iterations(gcpb_ctx* ctx, int64_t iterations);
 
+/* ---- device-resident iterations -----------------------------------------------
+ * One iteration of the epoch loop body (src/optimizer.cpp:116-119):
+ * stoch_grad + [all-reduce when sharded] + adam_step, with the gradient-replica
+ * reduction folded into the Adam update.  No host synchronisation. */
+int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss, uint64_t seed,
+              uint64_t iter, const gcpb_adam* adam);
+/* n iterations iter0 .. iter0+n-1 replayed as one CUDA graph (captured once per
+ * sampler/loss/seed/n configuration; the draw-stream iteration and Adam's
+ * counter advance on the device).  Equivalent to n calls of gcpb_step.  For
+ * the stratified sampler the rejection batches are planned on the device
+ * (three per iteration); a shortfall is reported as GCPB_ERR_RUNTIME by the
+ * next synchronising call. */
+int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                   uint64_t seed, uint64_t iter0, int64_t n, const gcpb_adam* adam);
+/* Wait for queued device work and report deferred device-side failures. */
+int gcpb_synchronize(gcpb_ctx* ctx);
+
+/* ---- fit driver -------------------------------------------------------------------
+ * fit_gcp_adam (src/optimizer.cpp:68-158) with the epoch loop on the device:
+ * factors start as the reference's init (RngStream(seed).split("init") uniform
+ * draws, rescaled to ||X||, kruskal.cpp:33-45,85-93) unless keep_factors;
+ * the fixed estimator set and the gradient draws come from the Philox stream
+ * keyed by RngStream(seed).split("estimator"/"gradients"); each epoch is
+ * epoch_iters graph-replayed iterations; accept when F <= best, else roll back
+ * factors, moments and counter, decay the rate, count a bad epoch. */
+typedef struct {
+  gcpb_sampler sampler;
+  double learning_rate; /* alpha_0 */
+  double beta1, beta2, epsilon;
+  int64_t epoch_iters;
+  int64_t max_bad_epochs;
+  double decay;
+  int32_t lower_bound_mode; /* 0: the loss's default bound, 1: lower_bound, 2: none */
+  double lower_bound;
+  int64_t estimator_samples;
+  int32_t estimator_kind; /* -1: stratified if sparse, uniform if dense */
+  int64_t max_epochs;
+  uint64_t seed;
+  int32_t keep_factors; /* 1: start from the factors already set */
+} gcpb_fit_config;
+
+/* FitTraceRecord (include/gcp/optimizer.hpp:30-36). */
+typedef struct {
+  int64_t epoch;
+  double loss_estimate;
+  double learning_rate;
+  double seconds;
+  int32_t accepted;
+} gcpb_trace_record;
+
+int gcpb_fit_gcp_adam(gcpb_ctx* ctx, const gcpb_loss* loss, const gcpb_fit_config* cfg,
+                      gcpb_trace_record* trace, int64_t trace_cap, int64_t* n_trace,
+                      double* final_estimate);
+
 /* ---- loss estimator -------------------------------------------------------------
  * EstimatorSamples (include/gcp/samplers.hpp:257-351).  set: given samples;
  * draw: drawn on the device from the Philox stream (tags EST_*). */

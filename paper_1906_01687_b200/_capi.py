@@ -46,6 +46,20 @@ class gcpb_adam(C.Structure):
                 ("lower_bound", C.c_double)]
 
 
+class gcpb_fit_config(C.Structure):
+    _fields_ = [("sampler", gcpb_sampler), ("learning_rate", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("epsilon", C.c_double), ("epoch_iters", C.c_int64),
+                ("max_bad_epochs", C.c_int64), ("decay", C.c_double),
+                ("lower_bound_mode", C.c_int32), ("lower_bound", C.c_double),
+                ("estimator_samples", C.c_int64), ("estimator_kind", C.c_int32),
+                ("max_epochs", C.c_int64), ("seed", C.c_uint64), ("keep_factors", C.c_int32)]
+
+
+class gcpb_trace_record(C.Structure):
+    _fields_ = [("epoch", C.c_int64), ("loss_estimate", C.c_double),
+                ("learning_rate", C.c_double), ("seconds", C.c_double), ("accepted", C.c_int32)]
+
+
 ctx_p = C.c_void_p
 i64p = C.POINTER(C.c_int64)
 f64p = C.POINTER(C.c_double)
@@ -87,6 +101,13 @@ SIGNATURES = [
     ("gcpb_adam_reset", C.c_int, [ctx_p]),
     ("gcpb_get_iterations", C.c_int, [ctx_p, i64p]),
     ("gcpb_set_iterations", C.c_int, [ctx_p, C.c_int64]),
+    ("gcpb_step", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss), C.c_uint64,
+                            C.c_uint64, C.POINTER(gcpb_adam)]),
+    ("gcpb_run_steps", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
+                                 C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(gcpb_adam)]),
+    ("gcpb_synchronize", C.c_int, [ctx_p]),
+    ("gcpb_fit_gcp_adam", C.c_int, [ctx_p, C.POINTER(gcpb_loss), C.POINTER(gcpb_fit_config),
+                                    C.POINTER(gcpb_trace_record), C.c_int64, i64p, f64p]),
     ("gcpb_estimator_set", C.c_int, [ctx_p, C.c_int64, i64p, f64p, f64p]),
     ("gcpb_estimator_draw", C.c_int, [ctx_p, C.c_int, C.c_int64, C.c_double, C.c_uint64]),
     ("gcpb_estimator_size", C.c_int64, [ctx_p]),

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -23,6 +24,7 @@
 #include "../../include/gcpb.h"
 #include "gcpb_aux.cuh"
 #include "gcpb_kernels.cuh"
+#include "rngstream.h"
 
 using namespace gcpb;
 
@@ -196,13 +198,18 @@ struct gcpb_ctx {
   bool hash_ready = false;
   int domain_flags = -1;  // cached domain scan of the stored data
 
+  // graph-replayed iterations (gcpb_run_steps)
+  cudaGraphExec_t graph_exec = nullptr;
+  std::string graph_key;
+  int64_t tensor_version = 0;
+
   // sharding
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
 
   // stratified zero sampler
   DBuf zero_list, zstatus;
-  int64_t zero_cap = 0, zstatus_cap = 0;
+  int64_t zero_cap = 0, zstatus_cap = 0, z_nchunks_first = 0;
 
   // estimator
   int64_t est_n = 0;
@@ -213,6 +220,7 @@ struct gcpb_ctx {
   DBuf dims_dev;
 
   ~gcpb_ctx() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (pinned_params) {
       cudaStreamSynchronize(stream);
       cudaFreeHost(pinned_params);
@@ -487,7 +495,7 @@ int replicas_for(const gcpb_ctx* c, int64_t n) {
 }
 
 template <typename T>
-void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record) {
+void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   const int64_t tiles = finish_segments(a);
   if (a.scatter) {
     int64_t n = 0;
@@ -497,7 +505,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record) {
     a.G = c->nrep > 1 ? c->Grep.as<T>() : c->Gr.as<T>();
   }
   CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms));
-  if (a.scatter && c->nrep > 1) {
+  if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
     grad_reduce_kernel<T><<<grid_for(c->nelem, 256, c->num_sms, 4), 256, 0, c->stream>>>(
         c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride);
     CK(cudaGetLastError());
@@ -517,12 +525,9 @@ Seg make_seg(int kind, uint32_t tag, int64_t tb, int64_t te, double w, int flag,
   return s;
 }
 
-// Runs the stratified zero sampler for q accepts: fills zero_list[0..q) with
-// candidate ordinals.  host_check: synchronise and continue host-side until
-// exactly q accepts exist (reference semantics for any q); otherwise three
-// device-planned batches are queued without a host round trip.
-void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
-                      uint32_t tag, bool host_check) {
+// Sizes the zero-sampler buffers and uploads its per-call scalars (q, N, zeta,
+// rho).  Kept out of graph capture (pageable-memory copies).
+void prepare_zero_sampler(gcpb_ctx* c, int64_t q, double rho) {
   ensure_hash(c);
   const double zeta = static_cast<double>(c->total128 - static_cast<unsigned __int128>(c->nnz));
   const int64_t first_batch = zero_batch_size_dev(c->total_d, zeta, rho, q);
@@ -535,10 +540,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
     c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
     c->zstatus_cap = nchunks;
   }
-  // Look-back words from earlier calls must not alias this call's batch tags.
-  CK(cudaMemsetAsync(c->zstatus.p, 0, static_cast<size_t>(std::max<int64_t>(nchunks, 1)) * 8,
-                     c->stream));
-  // Scalar inputs of the plan kernel.
+  c->z_nchunks_first = nchunks;
   DevState* st = c->dst();
   c->host_state.z_q = q;
   c->host_state.z_total = c->total_d;
@@ -551,6 +553,23 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
                      cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&st->z_status_cap, &c->host_state.z_status_cap, sizeof(int64_t),
                      cudaMemcpyHostToDevice, c->stream));
+}
+
+enum ZeroMode { ZERO_HOST_CHECK = 0, ZERO_DEVICE_ONLY = 1, ZERO_CAPTURE = 2 };
+
+// Runs the stratified zero sampler for q accepts: fills zero_list[0..q) with
+// candidate ordinals.  Three device-planned batches are queued without a host
+// round trip; ZERO_HOST_CHECK then synchronises and continues host-side until
+// exactly q accepts exist (reference semantics for any q); ZERO_CAPTURE (graph
+// mode, prepared beforehand) only counts shortfalls on the device.
+void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
+                      const uint64_t* iter_base, uint32_t tag, int mode) {
+  if (mode != ZERO_CAPTURE) prepare_zero_sampler(c, q, rho);
+  const int64_t nchunks = c->z_nchunks_first;
+  // Look-back words from earlier calls must not alias this call's batch tags.
+  CK(cudaMemsetAsync(c->zstatus.p, 0, static_cast<size_t>(std::max<int64_t>(nchunks, 1)) * 8,
+                     c->stream));
+  DevState* st = c->dst();
   ZeroArgs za;
   std::memset(&za, 0, sizeof(za));
   za.d = c->d;
@@ -563,6 +582,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   }
   za.seed = seed;
   za.iter = iter;
+  za.iter_base = iter_base;
   za.tag = tag;
   za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
   za.hmask = c->hmask;
@@ -575,7 +595,12 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
     zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
   }
   CK(cudaGetLastError());
-  if (!host_check) return;
+  if (mode == ZERO_CAPTURE) {
+    zero_check_kernel<<<1, 1, 0, c->stream>>>(st);
+    CK(cudaGetLastError());
+    return;
+  }
+  if (mode != ZERO_HOST_CHECK) return;
   for (;;) {
     c->pull_state();
     if (c->host_state.z_overflow) throw std::logic_error("zero sampler: status overflow");
@@ -595,9 +620,13 @@ struct SampleResult {
 template <typename T>
 SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss,
                              uint64_t seed, uint64_t iter, bool scatter, bool record,
-                             bool host_check, bool estimator_tags, int est_kind) {
+                             bool host_check, bool estimator_tags, int est_kind,
+                             const uint64_t* iter_base = nullptr, bool fold = false,
+                             int zero_mode = -1) {
   SampleResult res;
   FusedArgs<T> a = base_args<T>(c, loss, seed, iter);
+  a.iter_base = iter_base;
+  if (zero_mode < 0) zero_mode = host_check ? ZERO_HOST_CHECK : ZERO_DEVICE_ONLY;
   a.scatter = scatter ? 1 : 0;
   if (record) {
     a.r_idx = c->s_idx.as<int64_t>();
@@ -620,7 +649,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     if (c->tensor_kind == 2) ensure_hash(c), a.hkeys = c->hkeys.as<uint64_t>(),
                              a.hvals = c->hvals.as<uint32_t>(), a.hmask = c->hmask;
     res.n = s;
-    run_fused(c, a, record);
+    run_fused(c, a, record, fold);
     return res;
   }
   // stratified / semi-stratified (samplers.hpp:141-219), estimator split
@@ -643,7 +672,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       throw std::invalid_argument("sample_zeros_rejection: requested " + std::to_string(q) +
                                   " zeros but only " + u128_to_string(zeta128) + " exist");
     if (c->nranks > 1) throw std::invalid_argument("stratified sampling is single-rank in v1");
-    run_zero_sampler(c, q, sk->oversample, seed, iter, tag_z, host_check);
+    run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode);
     a.zero_list = c->zero_list.as<uint64_t>();
   }
   a.nseg = 0;
@@ -663,8 +692,8 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     }
   }
   res.n = p + q;
-  run_fused(c, a, record);
-  if (strat && q > 0 && host_check) {
+  run_fused(c, a, record, fold);
+  if (strat && q > 0 && zero_mode == ZERO_HOST_CHECK) {
     res.stats.tested = c->host_state.z_tested;
     res.stats.accepted = c->host_state.z_accepted;
     res.stats.rejected = c->host_state.z_rejected;
@@ -688,12 +717,14 @@ int64_t expected_samples(const gcpb_ctx* c, const gcpb_sampler* s) {
   (void)c;
 }
 
+// fold_reps > 0: the gradient is the sum of that many replicas (read and
+// re-zeroed by the kernel).  advance_rng: also step the device draw-stream base.
 template <typename T>
-void adam_launch(gcpb_ctx* c) {
+void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0) {
   const int grid = grid_for(c->nelem, 256, c->num_sms, 4);
-  adam_kernel<T><<<grid, 256, 0, c->stream>>>(c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(),
-                                               c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
-                                               static_cast<int>(c->r), c->dst());
+  adam_kernel<T><<<grid, 256, 0, c->stream>>>(
+      c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
+      static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride, advance_rng);
   CK(cudaGetLastError());
 }
 
@@ -729,6 +760,7 @@ void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
   const int64_t n = static_cast<int64_t>(keys.size());
   c->nnz = n;
   c->tensor_kind = 2;
+  c->tensor_version += 1;
   c->hash_ready = false;
   c->domain_flags = -1;
   c->dense.reset();
@@ -779,6 +811,168 @@ void given_launch(gcpb_ctx* c, int64_t n, const gcpb_loss* loss, bool y_given, b
   a.nseg = 1;
   a.seg[0] = make_seg(SEG_GIVEN, 0, 0, n, 0.0, 0, 0);
   run_fused(c, a, record);
+}
+
+// Uploads the Adam scalars (FitConfig fields + learning rate) through the
+// context's pinned block when they changed; no host synchronisation.
+void set_adam_params(gcpb_ctx* ctx, const gcpb_adam* adam) {
+  if (!adam) throw std::invalid_argument("adam: null");
+  DevState* st = ctx->dst();
+  DevState& h = ctx->host_state;
+  const int32_t has = adam->has_lower_bound ? 1 : 0;
+  const bool changed = !ctx->adam_params_valid || h.lr != adam->learning_rate ||
+                       h.beta1 != adam->beta1 || h.beta2 != adam->beta2 ||
+                       h.eps != adam->epsilon || h.lb != adam->lower_bound || h.has_lb != has;
+  if (!changed) return;
+  h.lr = adam->learning_rate;
+  h.beta1 = adam->beta1;
+  h.beta2 = adam->beta2;
+  h.eps = adam->epsilon;
+  h.lb = adam->lower_bound;
+  h.has_lb = has;
+  double* pin = ctx->pinned_params;
+  CK(cudaStreamSynchronize(ctx->stream));  // the pinned block may still be in flight
+  pin[0] = h.lr;
+  pin[1] = h.beta1;
+  pin[2] = h.beta2;
+  pin[3] = h.eps;
+  pin[4] = h.lb;
+  std::memcpy(&pin[5], &has, sizeof(has));
+  CK(cudaMemcpyAsync(&st->lr, pin, 5 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(&st->has_lb, &pin[5], sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->adam_params_valid = true;
+}
+
+void check_step_args(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss) {
+  validate_sampler(sampler);
+  validate_loss(loss);
+  if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+  if (sampler->strategy != GCPB_UNIFORM && ctx->tensor_kind != 2)
+    throw std::invalid_argument(sampler->strategy == GCPB_STRATIFIED
+                                    ? "stratified sampling requires a sparse tensor"
+                                    : "semi-stratified sampling requires a sparse tensor");
+  check_data_domain(ctx, loss->kind);
+}
+
+// One iteration: fused sample->MTTKRP, all-reduce when sharded, fused Adam
+// (which folds the replica reduction when not sharded).
+template <typename T>
+void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
+               uint64_t iter, const uint64_t* iter_base, int zero_mode) {
+  const bool multi = c->nranks > 1;
+  stoch_grad_impl<T>(c, sk, loss, seed, iter, true, false, zero_mode == ZERO_HOST_CHECK, false, -1,
+                     iter_base, /*fold=*/!multi, zero_mode);
+  int fold = 0;
+  if (multi) {
+    if (!c->comm) throw std::logic_error("sharded step without an NCCL communicator");
+    nck(ncclAllReduce(c->Gr.p, c->Gr.p, static_cast<size_t>(c->nelem),
+                      c->dtype == GCPB_F32 ? ncclFloat : ncclDouble, ncclSum, c->comm, c->stream),
+        "ncclAllReduce");
+  } else if (c->nrep > 1) {
+    fold = c->nrep;
+  }
+  adam_launch<T>(c, fold, iter_base ? 1 : 0);
+  c->grad_zero = true;
+}
+
+void set_rng_iter(gcpb_ctx* c, uint64_t iter0) {
+  CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(&c->pinned_params[8], &iter0, 8);
+  CK(cudaMemcpyAsync(&c->dst()->rng_iter, &c->pinned_params[8], 8, cudaMemcpyHostToDevice,
+                     c->stream));
+}
+
+std::string steps_key(const gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss,
+                      uint64_t seed, int64_t n) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf), "%d|%lld|%lld|%lld|%.17g|%d|%.17g|%llu|%lld|%lld|%d|%d|%d",
+                sk->strategy, static_cast<long long>(sk->num_samples),
+                static_cast<long long>(sk->nonzero_samples),
+                static_cast<long long>(sk->zero_samples), sk->oversample, loss->kind, loss->delta,
+                static_cast<unsigned long long>(seed), static_cast<long long>(n),
+                static_cast<long long>(c->tensor_version), c->rank, c->nranks,
+                c->hash_ready ? 1 : 0);
+  return buf;
+}
+
+template <typename T>
+void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
+                    uint64_t iter0, int64_t n, const gcpb_adam* adam) {
+  set_adam_params(c, adam);
+  ensure_grad_zero(c);
+  if (sk->strategy == GCPB_STRATIFIED) {
+    int64_t q = sk->zero_samples + (c->nnz == 0 ? sk->nonzero_samples : 0);
+    if (q > 0) {
+      const unsigned __int128 zeta = c->total128 - static_cast<unsigned __int128>(c->nnz);
+      if (zeta < static_cast<unsigned __int128>(q))
+        throw std::invalid_argument("sample_zeros_rejection: requested " + std::to_string(q) +
+                                    " zeros but only " + u128_to_string(zeta) + " exist");
+      prepare_zero_sampler(c, q, sk->oversample);
+    }
+  } else if (sk->strategy == GCPB_UNIFORM && c->tensor_kind == 2) {
+    ensure_hash(c);
+  }
+  set_rng_iter(c, iter0);
+  const std::string key = steps_key(c, sk, loss, seed, n);
+  if (!c->graph_exec || key != c->graph_key) {
+    if (c->graph_exec) {
+      cudaGraphExecDestroy(c->graph_exec);
+      c->graph_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int64_t k = 0; k < n; ++k)
+        step_impl<T>(c, sk, loss, seed, 0, &c->dst()->rng_iter, ZERO_CAPTURE);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &g));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    ck(e, "cudaGraphInstantiate");
+    c->graph_exec = ex;
+    c->graph_key = key;
+  }
+  CK(cudaGraphLaunch(c->graph_exec, c->stream));
+  c->grad_zero = true;
+}
+
+// Synchronise and surface deferred device-side failures (graph-mode
+// stratified shortfalls).
+void sync_and_check(gcpb_ctx* c) {
+  c->sync();
+  int32_t inc = 0;
+  CK(cudaMemcpyAsync(&inc, &c->dst()->z_incomplete, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (inc != 0) {
+    const int32_t zero = 0;
+    CK(cudaMemcpyAsync(&c->dst()->z_incomplete, &zero, 4, cudaMemcpyHostToDevice, c->stream));
+    c->sync();
+    throw std::runtime_error("stratified zero sampler: " + std::to_string(inc) +
+                             " graph-replayed iteration(s) found fewer than q zeros in the three "
+                             "device-planned batches; use gcpb_step for this problem");
+  }
+}
+
+double model_norm_host(const std::vector<std::vector<double>>& F, int64_t r) {
+  // KruskalModel::norm (kruskal.cpp:75-83): 1' (hadamard_k A_k' A_k) 1.
+  std::vector<double> gram(static_cast<size_t>(r * r), 1.0);
+  for (const auto& f : F) {
+    const int64_t n = static_cast<int64_t>(f.size()) / r;
+    for (int64_t a = 0; a < r; ++a)
+      for (int64_t b = 0; b < r; ++b) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) s += f[i * r + a] * f[i * r + b];
+        gram[a * r + b] *= s;
+      }
+  }
+  double ss = 0.0;
+  for (double v : gram) ss += v;
+  return std::sqrt(std::max(0.0, ss));
 }
 
 }  // namespace
@@ -867,7 +1061,7 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
     }
     cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);  // random gathers: 32-byte sectors
     c->dstate.alloc(sizeof(DevState));
-    CK(cudaMallocHost(reinterpret_cast<void**>(&c->pinned_params), 8 * sizeof(double)));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->pinned_params), 16 * sizeof(double)));
     std::memset(&c->host_state, 0, sizeof(DevState));
     c->host_state.lr = 1e-3;
     c->host_state.beta1 = 0.9;
@@ -937,6 +1131,7 @@ int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_so
       throw std::invalid_argument("value dtype must be F32 or F64");
     ctx->nnz = nnz;
     ctx->tensor_kind = 2;
+    ctx->tensor_version += 1;
     ctx->hash_ready = false;
     ctx->domain_flags = -1;
     ctx->dense.reset();
@@ -1058,6 +1253,7 @@ int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage) {
     ctx->sync();
     ctx->dense_storage = storage;
     ctx->tensor_kind = 1;
+    ctx->tensor_version += 1;
     ctx->nnz = 0;
     ctx->domain_flags = -1;
   });
@@ -1072,6 +1268,7 @@ int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage) {
     ctx->sync();
     ctx->dense_storage = storage;
     ctx->tensor_kind = 1;
+    ctx->tensor_version += 1;
     ctx->nnz = 0;
     ctx->domain_flags = -1;
   });
@@ -1114,6 +1311,7 @@ int gcpb_generate_dense_bernoulli(gcpb_ctx* ctx, int64_t true_rank, const double
     ctx->sync();
     ctx->dense_storage = storage;
     ctx->tensor_kind = 1;
+    ctx->tensor_version += 1;
     ctx->nnz = 0;
     ctx->domain_flags = -1;
   });
@@ -1351,33 +1549,7 @@ int gcpb_mttkrp_samples(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const doub
 // ---- optimizer -------------------------------------------------------------------------------
 int gcpb_adam_step(gcpb_ctx* ctx, const gcpb_adam* adam) {
   return guard(ctx, [&] {
-    if (!adam) throw std::invalid_argument("adam: null");
-    DevState* st = ctx->dst();
-    DevState& h = ctx->host_state;
-    const int32_t has = adam->has_lower_bound ? 1 : 0;
-    const bool changed = !ctx->adam_params_valid || h.lr != adam->learning_rate ||
-                         h.beta1 != adam->beta1 || h.beta2 != adam->beta2 ||
-                         h.eps != adam->epsilon || h.lb != adam->lower_bound || h.has_lb != has;
-    if (changed) {
-      // Staged through the context's pinned parameter block: no host sync.
-      h.lr = adam->learning_rate;
-      h.beta1 = adam->beta1;
-      h.beta2 = adam->beta2;
-      h.eps = adam->epsilon;
-      h.lb = adam->lower_bound;
-      h.has_lb = has;
-      double* pin = ctx->pinned_params;
-      pin[0] = h.lr;
-      pin[1] = h.beta1;
-      pin[2] = h.beta2;
-      pin[3] = h.eps;
-      pin[4] = h.lb;
-      std::memcpy(&pin[5], &has, sizeof(has));
-      CK(cudaMemcpyAsync(&st->lr, pin, 5 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-      CK(cudaMemcpyAsync(&st->has_lb, &pin[5], sizeof(int32_t), cudaMemcpyHostToDevice,
-                         ctx->stream));
-      ctx->adam_params_valid = true;
-    }
+    set_adam_params(ctx, adam);
     if (ctx->dtype == GCPB_F32)
       adam_launch<float>(ctx);
     else
@@ -1408,6 +1580,192 @@ int gcpb_set_iterations(gcpb_ctx* ctx, int64_t iterations) {
   return guard(ctx, [&] {
     CK(cudaMemcpyAsync(&ctx->dst()->t, &iterations, 8, cudaMemcpyHostToDevice, ctx->stream));
     ctx->sync();
+  });
+}
+
+int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss, uint64_t seed,
+              uint64_t iter, const gcpb_adam* adam) {
+  return guard(ctx, [&] {
+    check_step_args(ctx, sampler, loss);
+    set_adam_params(ctx, adam);
+    ensure_grad_zero(ctx);
+    if (ctx->dtype == GCPB_F32)
+      step_impl<float>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
+    else
+      step_impl<double>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
+  });
+}
+
+int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                   uint64_t seed, uint64_t iter0, int64_t n, const gcpb_adam* adam) {
+  return guard(ctx, [&] {
+    check_step_args(ctx, sampler, loss);
+    if (n < 0) throw std::invalid_argument("negative step count");
+    if (n == 0) return;
+    if (ctx->dtype == GCPB_F32)
+      run_steps_impl<float>(ctx, sampler, loss, seed, iter0, n, adam);
+    else
+      run_steps_impl<double>(ctx, sampler, loss, seed, iter0, n, adam);
+  });
+}
+
+int gcpb_synchronize(gcpb_ctx* ctx) {
+  return guard(ctx, [&] { sync_and_check(ctx); });
+}
+
+int gcpb_fit_gcp_adam(gcpb_ctx* ctx, const gcpb_loss* loss, const gcpb_fit_config* cfg,
+                      gcpb_trace_record* trace, int64_t trace_cap, int64_t* n_trace,
+                      double* final_estimate) {
+  return guard(ctx, [&] {
+    using clock = std::chrono::steady_clock;
+    const auto start = clock::now();
+    auto secs = [](clock::time_point a) {
+      return std::chrono::duration<double>(clock::now() - a).count();
+    };
+    if (!cfg) throw std::invalid_argument("fit: null config");
+    validate_loss(loss);
+    // FitConfig::validate (optimizer.cpp:31-45)
+    validate_sampler(&cfg->sampler);
+    if (!(cfg->learning_rate > 0.0)) throw std::invalid_argument("fit: learning rate must be > 0");
+    if (!(cfg->beta1 >= 0.0 && cfg->beta1 < 1.0) || !(cfg->beta2 >= 0.0 && cfg->beta2 < 1.0))
+      throw std::invalid_argument("fit: moment decays must satisfy 0 <= beta < 1");
+    if (!(cfg->epsilon > 0.0)) throw std::invalid_argument("fit: epsilon must be > 0");
+    if (cfg->epoch_iters < 1) throw std::invalid_argument("fit: iterations per epoch must be >= 1");
+    if (cfg->max_bad_epochs < 0) throw std::invalid_argument("fit: max bad epochs must be >= 0");
+    if (!(cfg->decay > 0.0 && cfg->decay < 1.0))
+      throw std::invalid_argument("fit: decay must be in (0, 1)");
+    if (cfg->estimator_samples < 0) throw std::invalid_argument("fit: estimator count must be >= 0");
+    if (cfg->max_epochs < 0) throw std::invalid_argument("fit: max epochs must be >= 0");
+    check_step_args(ctx, &cfg->sampler, loss);
+
+    // lower bound (optimizer.cpp:74)
+    gcpb_adam ad{cfg->learning_rate, cfg->beta1, cfg->beta2, cfg->epsilon, 0, 0.0};
+    if (cfg->lower_bound_mode == 1) {
+      ad.has_lower_bound = 1;
+      ad.lower_bound = cfg->lower_bound;
+    } else if (cfg->lower_bound_mode == 0) {
+      const int k = loss->kind;
+      if (k == GCPB_LOSS_POISSON || k == GCPB_LOSS_BERNOULLI_ODDS || k == GCPB_LOSS_GAMMA ||
+          k == GCPB_LOSS_BETA_HALF) {
+        ad.has_lower_bound = 1;
+        ad.lower_bound = 0.0;
+      }
+    }
+
+    // streams (optimizer.cpp:76-78)
+    const HostRngStream root(cfg->seed);
+    const uint64_t est_seed = root.split("estimator").key();
+    const uint64_t grad_seed = root.split("gradients").key();
+
+    // init (optimizer.cpp:80-82, kruskal.cpp:33-45,85-93)
+    if (!cfg->keep_factors) {
+      HostRngStream init = root.split("init");
+      std::vector<std::vector<double>> F(static_cast<size_t>(ctx->d));
+      for (int k = 0; k < ctx->d; ++k) {
+        F[k].resize(static_cast<size_t>(ctx->dims[k] * ctx->r));
+        for (auto& v : F[k]) v = init.next_double();
+      }
+      double data_norm = 0.0;  // TensorView::norm
+      if (gcpb_tensor_norm(ctx, &data_norm) != GCPB_OK) throw std::runtime_error(ctx->err);
+      if (data_norm > 0.0) {
+        const double current = model_norm_host(F, ctx->r);
+        if (current == 0.0) throw std::invalid_argument("kruskal model: cannot rescale a zero model");
+        const double ratio = std::pow(data_norm / current, 1.0 / ctx->d);
+        for (auto& f : F)
+          for (auto& v : f) v *= ratio;
+      }
+      std::vector<double> flat;
+      for (auto& f : F) flat.insert(flat.end(), f.begin(), f.end());
+      upload(ctx, ctx->A, -1, flat.data());
+    }
+
+    // estimator (optimizer.cpp:84-91)
+    const int est_kind = cfg->estimator_kind >= 0
+                             ? cfg->estimator_kind
+                             : (ctx->tensor_kind == 2 ? GCPB_EST_STRATIFIED : GCPB_EST_UNIFORM);
+    {
+      const int rc = gcpb_estimator_draw(ctx, est_kind, cfg->estimator_samples, 1.1, est_seed);
+      if (rc != GCPB_OK) throw std::runtime_error(ctx->err);
+    }
+    auto estimate = [&]() {
+      double f = 0.0;
+      const int rc = gcpb_estimate(ctx, loss, &f);
+      if (rc != GCPB_OK) throw std::runtime_error(ctx->err);
+      return f;
+    };
+
+    // AdamState::init (optimizer.cpp:93)
+    const size_t bytes = ctx->nelem * ctx->tsize;
+    CK(cudaMemsetAsync(ctx->B.p, 0, bytes, ctx->stream));
+    CK(cudaMemsetAsync(ctx->C.p, 0, bytes, ctx->stream));
+    {
+      const int64_t zero = 0;
+      CK(cudaMemcpyAsync(&ctx->dst()->t, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
+      ctx->sync();
+    }
+    double lr = cfg->learning_rate;
+    int64_t bad = 0;
+    double best = estimate();
+    if (!std::isfinite(best))
+      throw std::runtime_error("fit: initial loss estimate is not finite (" +
+                               std::to_string(best) + ")");
+    {
+      const int rc = gcpb_snapshot_save(ctx);
+      if (rc != GCPB_OK) throw std::runtime_error(ctx->err);
+    }
+    int64_t nt = 0;
+    auto record = [&](int64_t epoch, double f, double a, double sec, bool acc) {
+      if (nt < trace_cap && trace) trace[nt] = gcpb_trace_record{epoch, f, a, sec, acc ? 1 : 0};
+      ++nt;
+    };
+    record(0, best, lr, secs(start), true);
+    // Small stratified budgets step with the host-checked sampler (exact for
+    // any q); large ones replay a CUDA graph per epoch.
+    const bool graph_ok = !(cfg->sampler.strategy == GCPB_STRATIFIED &&
+                            cfg->sampler.zero_samples < 4096);
+    uint64_t it = 0;  // gradient stream position, never rewound (optimizer.cpp:78)
+    for (int64_t epoch = 1; epoch <= cfg->max_epochs; ++epoch) {
+      const auto e0 = clock::now();
+      const double alpha_used = lr;
+      ad.learning_rate = lr;
+      if (graph_ok) {
+        if (ctx->dtype == GCPB_F32)
+          run_steps_impl<float>(ctx, &cfg->sampler, loss, grad_seed, it, cfg->epoch_iters, &ad);
+        else
+          run_steps_impl<double>(ctx, &cfg->sampler, loss, grad_seed, it, cfg->epoch_iters, &ad);
+        sync_and_check(ctx);
+      } else {
+        set_adam_params(ctx, &ad);
+        ensure_grad_zero(ctx);
+        for (int64_t i = 0; i < cfg->epoch_iters; ++i) {
+          if (ctx->dtype == GCPB_F32)
+            step_impl<float>(ctx, &cfg->sampler, loss, grad_seed, it + i, nullptr, ZERO_HOST_CHECK);
+          else
+            step_impl<double>(ctx, &cfg->sampler, loss, grad_seed, it + i, nullptr, ZERO_HOST_CHECK);
+        }
+      }
+      it += static_cast<uint64_t>(cfg->epoch_iters);
+      const double fnew = estimate();
+      if (!std::isfinite(fnew))
+        throw std::runtime_error("fit: loss estimate became non-finite at epoch " +
+                                 std::to_string(epoch));
+      const double sec = secs(e0);
+      if (fnew <= best) {  // optimizer.cpp:128-135
+        best = fnew;
+        const int rc = gcpb_snapshot_save(ctx);
+        if (rc != GCPB_OK) throw std::runtime_error(ctx->err);
+        record(epoch, fnew, alpha_used, sec, true);
+      } else {  // optimizer.cpp:136-146
+        const int rc = gcpb_snapshot_restore(ctx);
+        if (rc != GCPB_OK) throw std::runtime_error(ctx->err);
+        lr *= cfg->decay;
+        ++bad;
+        record(epoch, fnew, alpha_used, sec, false);
+        if (bad > cfg->max_bad_epochs) break;
+      }
+    }
+    if (n_trace) *n_trace = nt;
+    if (final_estimate) *final_estimate = best;
   });
 }
 

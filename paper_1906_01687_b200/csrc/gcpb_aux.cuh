@@ -26,7 +26,8 @@ struct DevState {
   double z_total, z_zeta, z_rho;
   int64_t z_status_cap;
   int32_t z_overflow;
-  int32_t z_pad2;
+  int32_t z_incomplete;  // graph-mode steps whose zero sampler fell short
+  uint64_t rng_iter;     // draw-stream iteration base for graph-replayed steps
 };
 
 constexpr int kZcThreads = 256;
@@ -40,6 +41,7 @@ struct ZeroArgs {
   uint64_t stride[kMaxModes];
   uint64_t seed;
   uint64_t iter;
+  const uint64_t* iter_base;  // optional device-resident iteration base
   uint32_t tag;
   const uint64_t* hkeys;
   uint64_t hmask;
@@ -91,6 +93,11 @@ __global__ void zero_plan_kernel(DevState* st, int first) {
   st->z_nchunks = nchunks;
 }
 
+// Graph mode: counts steps whose device-planned batches did not yield q zeros.
+__global__ void zero_check_kernel(DevState* st) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && st->z_accepted < st->z_q) st->z_incomplete += 1;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -126,6 +133,7 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
   const uint32_t btag = st->z_batch_tag;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
+  const uint64_t iter = a.iter + (a.iter_base ? *a.iter_base : 0ull);
   for (;;) {
     if (threadIdx.x == 0) s_chunk = static_cast<long long>(atomicAdd(&st->z_ticket, 1ull));
     __syncthreads();
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       ++nvalid;
       uint64_t lin = 0;
       for (int g4 = 0; g4 * 4 < a.d; ++g4) {
-        const U4 b = philox_block(a.seed, a.tag, static_cast<uint32_t>(g4), 0u, a.iter,
+        const U4 b = philox_block(a.seed, a.tag, static_cast<uint32_t>(g4), 0u, iter,
                                   static_cast<uint64_t>(c));
         for (int sl = 0; sl < 4; ++sl) {
           const int k = g4 * 4 + sl;
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
           const uint64_t prod = static_cast<uint64_t>(word_of(b, sl)) * a.dims[k];
           uint32_t ik = (static_cast<uint32_t>(prod) >= a.thr[k])
                             ? static_cast<uint32_t>(prod >> 32)
-                            : bounded32_from(a.seed, a.tag, a.iter, static_cast<uint64_t>(c), k,
+                            : bounded32_from(a.seed, a.tag, iter, static_cast<uint64_t>(c), k,
                                              a.dims[k], a.thr[k], 1u);
           lin += static_cast<uint64_t>(ik) * a.stride[k];
         }
@@ -239,10 +247,15 @@ __global__ void hash_build_kernel(const uint64_t* __restrict__ keys, int64_t n,
 }
 
 // adam_step (optimizer.cpp:47-66) fused with zeroing the gradient; padding
-// columns (j >= r) are left untouched.  The last block advances t.
+// columns (j >= r) are left untouched.  With nrep > 0 the gradient is read
+// as the sum of the privatized replicas (folding grad_reduce_kernel into the
+// update) and the replicas are re-zeroed.  The last block advances t (and the
+// draw-stream base when advance_rng).
 template <typename T>
 __global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict__ B,
-                            T* __restrict__ C, int64_t n, int rp, int r, DevState* st) {
+                            T* __restrict__ C, int64_t n, int rp, int r, DevState* st,
+                            T* __restrict__ reps, int nrep, int64_t rep_stride,
+                            int advance_rng) {
   __shared__ double s_c1, s_c2;
   if (threadIdx.x == 0) {
     const double te = static_cast<double>(st->t + 1);
@@ -259,8 +272,18 @@ __global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict
   const T lb = static_cast<T>(st->lb);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const T g = Gr[i];
-    Gr[i] = static_cast<T>(0);
+    T g;
+    if (nrep > 0) {
+      g = static_cast<T>(0);
+      for (int q = 0; q < nrep; ++q) {
+        T* p = reps + q * rep_stride + i;
+        g += *p;
+        *p = static_cast<T>(0);
+      }
+    } else {
+      g = Gr[i];
+      Gr[i] = static_cast<T>(0);
+    }
     if (static_cast<int>(i % rp) >= r) continue;
     const T b = b1 * B[i] + ob1 * g;
     const T c = b2 * C[i] + ob2 * (g * g);
@@ -276,6 +299,7 @@ __global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict
     const unsigned prev = atomicAdd(&st->adam_done, 1u);
     if (prev == gridDim.x - 1) {
       st->t += 1;
+      if (advance_rng) st->rng_iter += 1;
       st->adam_done = 0;
     }
   }

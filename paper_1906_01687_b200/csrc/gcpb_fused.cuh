@@ -109,7 +109,7 @@ __device__ __forceinline__ SegRegs seg_of(const FusedArgs<T>& a, int64_t tile) {
 // Phase A: lane-per-sample draw of ordinal t of segment sg.
 template <typename T, int DM, bool EXACT>
 __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg, int64_t t,
-                                        uint32_t (&ik)[DM], Drawn<T>& s) {
+                                        uint64_t iter, uint32_t (&ik)[DM], Drawn<T>& s) {
   const int d = EXACT ? DM : a.d;
   s.valid = t < sg.t_end;
   s.x = static_cast<T>(0);
@@ -125,7 +125,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
     for (int g4 = 0; g4 < (DM + 3) / 4; ++g4) {
       if (EXACT || g4 * 4 < d) {
-        const U4 b = philox_block(a.seed, sg.tag, static_cast<uint32_t>(g4), 0u, a.iter, tt);
+        const U4 b = philox_block(a.seed, sg.tag, static_cast<uint32_t>(g4), 0u, iter, tt);
 #pragma unroll
         for (int sl = 0; sl < 4; ++sl) {
           const int k = g4 * 4 + sl;
@@ -133,7 +133,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
             const uint64_t prod = static_cast<uint64_t>(word_of(b, sl)) * a.dims[k];
             ik[k] = (static_cast<uint32_t>(prod) >= a.thr[k])
                         ? static_cast<uint32_t>(prod >> 32)
-                        : bounded32_from(a.seed, sg.tag, a.iter, tt, k, a.dims[k], a.thr[k], 1u);
+                        : bounded32_from(a.seed, sg.tag, iter, tt, k, a.dims[k], a.thr[k], 1u);
           }
         }
       }
@@ -170,14 +170,14 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
   } else if (kind == SEG_PICK) {
     uint64_t e;
     if (a.eta <= (1ull << 32)) {
-      const U4 b = philox_block(a.seed, sg.tag, 0u, 0u, a.iter, static_cast<uint64_t>(t));
+      const U4 b = philox_block(a.seed, sg.tag, 0u, 0u, iter, static_cast<uint64_t>(t));
       const uint64_t prod = static_cast<uint64_t>(b.x) * a.eta;
       e = (static_cast<uint32_t>(prod) >= a.thr_eta)
               ? (prod >> 32)
-              : bounded32_from(a.seed, sg.tag, a.iter, static_cast<uint64_t>(t), 0, a.eta,
+              : bounded32_from(a.seed, sg.tag, iter, static_cast<uint64_t>(t), 0, a.eta,
                                a.thr_eta, 1u);
     } else {
-      e = bounded64(a.seed, sg.tag, a.iter, static_cast<uint64_t>(t), 0, a.eta);
+      e = bounded64(a.seed, sg.tag, iter, static_cast<uint64_t>(t), 0, a.eta);
     }
     if (static_cast<int64_t>(e) < a.nz_begin || static_cast<int64_t>(e) >= a.nz_end) {
       s.valid = false;
@@ -360,12 +360,15 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   T* Gb = a.G + static_cast<int64_t>(blockIdx.x % a.nrep) * a.rep_stride;
+  // Iteration of the draw stream: kernel argument plus an optional
+  // device-resident base (graph-replayed steps advance it without relaunch).
+  const uint64_t iter = a.iter + (a.iter_base ? __ldg(a.iter_base) : 0ull);
   int64_t tile = warp0;
   if (tile >= total_tiles) return;
   uint32_t ik[DM];
   Drawn<T> s;
   SegRegs sg = seg_of<T>(a, tile);
-  phase_a<T, DM, EXACT>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, ik, s);
+  phase_a<T, DM, EXACT>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik, s);
   for (; tile < total_tiles; tile += nwarps) {
     const int64_t next = tile + nwarps;
     uint32_t ik2[DM];
@@ -373,7 +376,8 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
     SegRegs sg2 = sg;
     if (next < total_tiles) {  // prefetch: next tile's draws + tensor gathers in flight
       sg2 = seg_of<T>(a, next);
-      phase_a<T, DM, EXACT>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, ik2, s2);
+      phase_a<T, DM, EXACT>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, iter, ik2,
+                            s2);
     } else {
       s2.valid = false;
 #pragma unroll

@@ -59,6 +59,7 @@ struct FusedArgs {
   uint64_t stride[kMaxModes];
   uint64_t seed;
   uint64_t iter;
+  const uint64_t* iter_base;  // optional device-resident iteration base (graph replay)
   // tensor access
   int xkind;
   const void* dense;

@@ -424,6 +424,28 @@ class Engine:
                             0.0 if lower_bound is None else float(lower_bound))
         self._ck(lib.gcpb_adam_step(self._h, C.byref(a)))
 
+    @staticmethod
+    def _adam(learning_rate, beta1=0.9, beta2=0.999, epsilon=1e-8, lower_bound=None):
+        return _capi.gcpb_adam(learning_rate, beta1, beta2, epsilon,
+                               0 if lower_bound is None else 1,
+                               0.0 if lower_bound is None else float(lower_bound))
+
+    def step(self, sampler: SamplerKind, loss: LossFunction, seed: int, it: int,
+             learning_rate: float, beta1=0.9, beta2=0.999, epsilon=1e-8,
+             lower_bound: Optional[float] = None) -> None:
+        """One epoch-loop iteration (optimizer.cpp:116-119) on the device."""
+        sk, ls = sampler.c(), loss.c()
+        a = self._adam(learning_rate, beta1, beta2, epsilon, lower_bound)
+        self._ck(lib.gcpb_step(self._h, C.byref(sk), C.byref(ls), seed, it, C.byref(a)))
+
+    def run_steps(self, sampler: SamplerKind, loss: LossFunction, seed: int, it0: int, n: int,
+                  learning_rate: float, beta1=0.9, beta2=0.999, epsilon=1e-8,
+                  lower_bound: Optional[float] = None) -> None:
+        """n iterations it0..it0+n-1 replayed as one CUDA graph (asynchronous)."""
+        sk, ls = sampler.c(), loss.c()
+        a = self._adam(learning_rate, beta1, beta2, epsilon, lower_bound)
+        self._ck(lib.gcpb_run_steps(self._h, C.byref(sk), C.byref(ls), seed, it0, n, C.byref(a)))
+
     def adam_reset(self) -> None:
         self._ck(lib.gcpb_adam_reset(self._h))
 
@@ -464,8 +486,7 @@ class Engine:
 
     # ---- snapshots / multi-GPU -------------------------------------------------------
     def synchronize(self) -> None:
-        out = C.c_int64()
-        self._ck(lib.gcpb_get_iterations(self._h, C.byref(out)))  # syncs the stream
+        self._ck(lib.gcpb_synchronize(self._h))
 
     def snapshot_save(self) -> None:
         self._ck(lib.gcpb_snapshot_save(self._h))
