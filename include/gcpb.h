@@ -209,6 +209,12 @@ int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
  * next synchronising call. */
 int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter0, int64_t n, const gcpb_adam* adam);
+/* Per-launch timing of the fused sample->MTTKRP kernel: CUDA events recorded
+ * on the context's stream around each non-graph launch.  enable = 1 clears
+ * and starts recording, 0 stops.  gcpb_kernel_time synchronises and returns
+ * the summed event time and the number of timed launches. */
+int gcpb_kernel_timing(gcpb_ctx* ctx, int enable);
+int gcpb_kernel_time(gcpb_ctx* ctx, double* total_ms, int64_t* launches);
 /* Wait for queued device work and report deferred device-side failures. */
 int gcpb_synchronize(gcpb_ctx* ctx);
 

@@ -106,6 +106,8 @@ SIGNATURES = [
     ("gcpb_run_steps", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
                                  C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(gcpb_adam)]),
     ("gcpb_synchronize", C.c_int, [ctx_p]),
+    ("gcpb_kernel_timing", C.c_int, [ctx_p, C.c_int]),
+    ("gcpb_kernel_time", C.c_int, [ctx_p, f64p, i64p]),
     ("gcpb_fit_gcp_adam", C.c_int, [ctx_p, C.POINTER(gcpb_loss), C.POINTER(gcpb_fit_config),
                                     C.POINTER(gcpb_trace_record), C.c_int64, i64p, f64p]),
     ("gcpb_estimator_set", C.c_int, [ctx_p, C.c_int64, i64p, f64p, f64p]),

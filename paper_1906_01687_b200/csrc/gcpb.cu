@@ -198,6 +198,11 @@ struct gcpb_ctx {
   bool hash_ready = false;
   int domain_flags = -1;  // cached domain scan of the stored data
 
+  // fused-kernel event timing (gcpb_kernel_timing)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tevents;
+  size_t tevents_used = 0;
+
   // graph-replayed iterations (gcpb_run_steps)
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
@@ -220,6 +225,10 @@ struct gcpb_ctx {
   DBuf dims_dev;
 
   ~gcpb_ctx() {
+    for (auto& pr : tevents) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (pinned_params) {
       cudaStreamSynchronize(stream);
@@ -497,6 +506,22 @@ int replicas_for(const gcpb_ctx* c, int64_t n) {
 template <typename T>
 void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   const int64_t tiles = finish_segments(a);
+  cudaEvent_t ev1 = nullptr;
+  if (c->timing) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      if (c->tevents_used == c->tevents.size()) {
+        cudaEvent_t x, y;
+        CK(cudaEventCreate(&x));
+        CK(cudaEventCreate(&y));
+        c->tevents.emplace_back(x, y);
+      }
+      auto& pr = c->tevents[c->tevents_used++];
+      CK(cudaEventRecord(pr.first, c->stream));
+      ev1 = pr.second;
+    }
+  }
   if (a.scatter) {
     int64_t n = 0;
     for (int s = 0; s < a.nseg; ++s) n += std::max<int64_t>(0, a.seg[s].t_end - a.seg[s].t_begin);
@@ -505,6 +530,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     a.G = c->nrep > 1 ? c->Grep.as<T>() : c->Gr.as<T>();
   }
   CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms));
+  if (ev1) CK(cudaEventRecord(ev1, c->stream));
   if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
     grad_reduce_kernel<T><<<grid_for(c->nelem, 256, c->num_sms, 4), 256, 0, c->stream>>>(
         c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride);
@@ -1606,6 +1632,28 @@ int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
       run_steps_impl<float>(ctx, sampler, loss, seed, iter0, n, adam);
     else
       run_steps_impl<double>(ctx, sampler, loss, seed, iter0, n, adam);
+  });
+}
+
+int gcpb_kernel_timing(gcpb_ctx* ctx, int enable) {
+  return guard(ctx, [&] {
+    ctx->sync();
+    ctx->timing = enable != 0;
+    if (enable) ctx->tevents_used = 0;
+  });
+}
+
+int gcpb_kernel_time(gcpb_ctx* ctx, double* total_ms, int64_t* launches) {
+  return guard(ctx, [&] {
+    ctx->sync();
+    double tot = 0.0;
+    for (size_t i = 0; i < ctx->tevents_used; ++i) {
+      float ms = 0.0f;
+      CK(cudaEventElapsedTime(&ms, ctx->tevents[i].first, ctx->tevents[i].second));
+      tot += ms;
+    }
+    *total_ms = tot;
+    *launches = static_cast<int64_t>(ctx->tevents_used);
   });
 }
 

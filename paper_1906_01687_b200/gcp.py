@@ -485,6 +485,15 @@ class Engine:
         return out.value
 
     # ---- snapshots / multi-GPU -------------------------------------------------------
+    def kernel_timing(self, enable: bool) -> None:
+        self._ck(lib.gcpb_kernel_timing(self._h, 1 if enable else 0))
+
+    def kernel_time(self) -> tuple[float, int]:
+        """(summed ms, launches) of the fused kernel since kernel_timing(True)."""
+        t, n = C.c_double(), C.c_int64()
+        self._ck(lib.gcpb_kernel_time(self._h, C.byref(t), C.byref(n)))
+        return t.value, n.value
+
     def synchronize(self) -> None:
         self._ck(lib.gcpb_synchronize(self._h))
 

@@ -174,3 +174,96 @@ def sparse_values(w: Workload, n: int, seed: int) -> np.ndarray:
     v = rs.poisson(3.0, n)
     v[v == 0] = 1  # condition on >= 1: no explicit zeros (tensor.cpp:35)
     return np.log1p(v).astype(np.float32)
+
+
+def c5_device_data(w: Workload, seed: int = 1005, oversample: float = 1.36,
+                   bucket_limit: int = 1_500_000_000, device=None):
+    """C5 on the GPU (torch as ingest plumbing, off the hot path): per-mode
+    Zipf(1.05) indices by inverse CDF, u64 linear keys, the first `nnz`
+    distinct keys in generation order, returned sorted; values
+    log(1 + Poisson(3)) conditioned on Poisson >= 1 (no explicit zeros,
+    tensor.cpp:35).  Deduplication: candidate keys are split into key-range
+    buckets of < bucket_limit elements (torch sorts < 2^31 elements; buckets
+    never share a key), each bucket is stably sorted so the first element of a
+    run of equal keys is its first occurrence, and the exact count is reached
+    by bisection on the first-occurrence position."""
+    import torch
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    target = w.nnz
+    strides = [1]
+    for n in w.dims[:-1]:
+        strides.append(strides[-1] * n)
+    cdfs = []
+    for n in w.dims:
+        wt = 1.0 / torch.arange(1, n + 1, dtype=torch.float64, device=dev) ** 1.05
+        c = torch.cumsum(wt, 0)
+        cdfs.append(c / c[-1])
+    sign = torch.tensor(-(2 ** 63), dtype=torch.int64, device=dev)
+    gen = int(target * oversample)
+    while True:
+        keys = torch.zeros(gen, dtype=torch.int64, device=dev)
+        chunk = 1 << 27
+        for b in range(0, gen, chunk):
+            e = min(gen, b + chunk)
+            for k, n in enumerate(w.dims):
+                u = torch.rand(e - b, dtype=torch.float64, device=dev, generator=g)
+                ik = torch.searchsorted(cdfs[k], u, right=True).clamp_(max=n - 1)
+                keys[b:e] += ik * strides[k]  # wraps mod 2^64 (N > 2^63 for C5)
+                del u, ik
+        keys.bitwise_xor_(sign)  # u64 order as signed order
+        nb = -(-gen // bucket_limit)
+        if nb > 1:
+            probe = keys[torch.randint(0, gen, (1 << 20,), device=dev, generator=g)]
+            qs = torch.quantile(probe.to(torch.float64),
+                                torch.linspace(0, 1, nb + 1, dtype=torch.float64, device=dev)[1:-1])
+            pivots = [int(v) for v in qs.tolist()]
+        else:
+            pivots = []
+        bounds = [None] + pivots + [None]
+        uniqs, firsts = [], []
+        for bi in range(len(bounds) - 1):
+            m = torch.ones(gen, dtype=torch.bool, device=dev)
+            if bounds[bi] is not None:
+                m &= keys >= bounds[bi]
+            if bounds[bi + 1] is not None:
+                m &= keys < bounds[bi + 1]
+            pos = torch.nonzero(m).squeeze(1)
+            kb = keys[pos]
+            del m
+            sk, order = torch.sort(kb, stable=True)
+            del kb
+            pos = pos[order]
+            del order
+            st = torch.ones(sk.numel(), dtype=torch.bool, device=dev)
+            st[1:] = sk[1:] != sk[:-1]
+            uniqs.append(sk[st])
+            firsts.append(pos[st])
+            del sk, pos, st
+        del keys
+        uniq = torch.cat(uniqs)
+        first = torch.cat(firsts)
+        del uniqs, firsts
+        if uniq.numel() >= target:
+            break
+        del uniq, first
+        gen = int(gen * 1.3)
+    lo, hi = 0, gen  # smallest T with count(first < T) == target
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if int((first < mid).sum()) >= target:
+            hi = mid
+        else:
+            lo = mid + 1
+    sel = uniq[first < lo]
+    del uniq, first
+    assert sel.numel() == target
+    sel.bitwise_xor_(sign)  # back to the u64 bit pattern (still ascending as u64)
+    lam = torch.full((target,), 3.0, dtype=torch.float32, device=dev)
+    v = torch.poisson(lam, generator=g)
+    del lam
+    v.clamp_(min=1.0)
+    vals = torch.log1p(v)
+    del v
+    return sel, vals
