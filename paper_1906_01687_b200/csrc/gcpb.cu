@@ -474,6 +474,14 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     }
   }
   a.scatter = 1;
+  // Factor + gradient tables beyond ~half of L2: prefetch rows a tile ahead.
+  // Measured on C5: the L2 prefetch of the next tile's rows costs more issue
+  // slots than it hides latency, so it is opt-in (GCPB_PREFETCH=1).
+  a.prefetch = 0;
+  if (const char* ev = getenv("GCPB_PREFETCH")) a.prefetch = atoi(ev);
+  // Factor tables beyond ~half of L2 gather from HBM: use the staged kernel.
+  a.stage = (c->nelem * static_cast<int64_t>(c->tsize) > (int64_t{64} << 20)) ? 1 : 0;
+  if (const char* ev = getenv("GCPB_STAGE")) a.stage = atoi(ev);
   return a;
 }
 
@@ -747,7 +755,7 @@ int64_t expected_samples(const gcpb_ctx* c, const gcpb_sampler* s) {
 // re-zeroed by the kernel).  advance_rng: also step the device draw-stream base.
 template <typename T>
 void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0) {
-  const int grid = grid_for(c->nelem, 256, c->num_sms, 4);
+  const int grid = grid_for(c->nelem / c->vw, 256, c->num_sms, 8);
   adam_kernel<T><<<grid, 256, 0, c->stream>>>(
       c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
       static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride, advance_rng);

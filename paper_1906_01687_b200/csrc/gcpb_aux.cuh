@@ -249,13 +249,62 @@ __global__ void hash_build_kernel(const uint64_t* __restrict__ keys, int64_t n,
 // adam_step (optimizer.cpp:47-66) fused with zeroing the gradient; padding
 // columns (j >= r) are left untouched.  With nrep > 0 the gradient is read
 // as the sum of the privatized replicas (folding grad_reduce_kernel into the
-// update) and the replicas are re-zeroed.  The last block advances t (and the
-// draw-stream base when advance_rng).
+// update) and the replicas are re-zeroed.  Vectorised: each thread owns one
+// 16-byte chunk per array per iteration (rows are padded to 32 bytes, so a
+// chunk never straddles rows), two chunks in flight.  The last block advances
+// t (and the draw-stream base when advance_rng).
 template <typename T>
-__global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict__ B,
-                            T* __restrict__ C, int64_t n, int rp, int r, DevState* st,
-                            T* __restrict__ reps, int nrep, int64_t rep_stride,
-                            int advance_rng) {
+__device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr,
+                                           T* __restrict__ B, T* __restrict__ C, int64_t i0,
+                                           int col0, int r, T* __restrict__ reps, int nrep,
+                                           int64_t rep_stride, T c1, T c2, T lr, T b1, T b2,
+                                           T ob1, T ob2, T eps, bool has_lb, T lb) {
+  constexpr int VW = Vec<T>::W;
+  Vec<T> a, g, b, c;
+  load_chunk(A + i0, a);
+  load_chunk(B + i0, b);
+  load_chunk(C + i0, c);
+  if (nrep > 0) {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) g.v[e] = static_cast<T>(0);
+    for (int q = 0; q < nrep; ++q) {
+      T* p = reps + q * rep_stride + i0;
+      Vec<T> x;
+      load_chunk(p, x);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) g.v[e] += x.v[e];
+      store_chunk(p, Vec<T>{});
+    }
+  } else {
+    load_chunk(Gr + i0, g);
+    store_chunk(Gr + i0, Vec<T>{});
+  }
+  Vec<T> ao = a, bo = b, co = c;  // padding columns keep their (zero) values
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    if (col0 + e < r) {
+      const T gv = g.v[e];
+      const T bv = b1 * b.v[e] + ob1 * gv;
+      const T cv = b2 * c.v[e] + ob2 * (gv * gv);
+      bo.v[e] = bv;
+      co.v[e] = cv;
+      T av = a.v[e] - lr * (bv / c1) / sqrt((cv / c2) + eps);
+      if (has_lb) av = av > lb ? av : lb;
+      ao.v[e] = av;
+    }
+  }
+  store_chunk(A + i0, ao);
+  store_chunk(B + i0, bo);
+  store_chunk(C + i0, co);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restrict__ Gr,
+                                                   T* __restrict__ B, T* __restrict__ C,
+                                                   int64_t n, int rp, int r, DevState* st,
+                                                   T* __restrict__ reps, int nrep,
+                                                   int64_t rep_stride, int advance_rng) {
+  constexpr int VW = Vec<T>::W;
   __shared__ double s_c1, s_c2;
   if (threadIdx.x == 0) {
     const double te = static_cast<double>(st->t + 1);
@@ -270,28 +319,55 @@ __global__ void adam_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict
   const T eps = static_cast<T>(st->eps);
   const bool has_lb = st->has_lb != 0;
   const T lb = static_cast<T>(st->lb);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    T g;
-    if (nrep > 0) {
-      g = static_cast<T>(0);
-      for (int q = 0; q < nrep; ++q) {
-        T* p = reps + q * rep_stride + i;
-        g += *p;
-        *p = static_cast<T>(0);
+  const uint32_t nchunk = static_cast<uint32_t>(n / VW);  // n < 2^31, multiple of VW
+  const uint32_t stride = gridDim.x * blockDim.x;
+  if (nrep > 0) {  // small problems: replicas folded, simple loop
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nchunk; q += stride)
+      adam_chunk<T>(A, Gr, B, C, static_cast<int64_t>(q) * VW,
+                    static_cast<int>((q * VW) % static_cast<uint32_t>(rp)), r, reps, nrep,
+                    rep_stride, c1, c2, lr, b1, b2, ob1, ob2, eps, has_lb, lb);
+  } else {
+    // Streaming path: U chunks per thread with all 4U loads issued before any
+    // use, so enough bytes are in flight to cover HBM latency.
+    constexpr int U = 4;
+    for (uint32_t q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < nchunk; q0 += U * stride) {
+      Vec<T> a[U], g[U], b[U], c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t q = q0 + u * stride;
+        q = q < nchunk ? q : nchunk - 1;
+        const int64_t i0 = static_cast<int64_t>(q) * VW;
+        load_chunk(A + i0, a[u]);
+        load_chunk(Gr + i0, g[u]);
+        load_chunk(B + i0, b[u]);
+        load_chunk(C + i0, c[u]);
       }
-    } else {
-      g = Gr[i];
-      Gr[i] = static_cast<T>(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = q0 + u * stride;
+        if (q >= nchunk) break;
+        const int64_t i0 = static_cast<int64_t>(q) * VW;
+        const int col0 = static_cast<int>((q * VW) % static_cast<uint32_t>(rp));
+        Vec<T> ao = a[u], bo = b[u], co = c[u];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          if (col0 + e < r) {
+            const T gv = g[u].v[e];
+            const T bv = b1 * b[u].v[e] + ob1 * gv;
+            const T cv = b2 * c[u].v[e] + ob2 * (gv * gv);
+            bo.v[e] = bv;
+            co.v[e] = cv;
+            T av = a[u].v[e] - lr * (bv / c1) / sqrt((cv / c2) + eps);
+            if (has_lb) av = av > lb ? av : lb;
+            ao.v[e] = av;
+          }
+        }
+        store_chunk(Gr + i0, Vec<T>{});
+        store_chunk(A + i0, ao);
+        store_chunk(B + i0, bo);
+        store_chunk(C + i0, co);
+      }
     }
-    if (static_cast<int>(i % rp) >= r) continue;
-    const T b = b1 * B[i] + ob1 * g;
-    const T c = b2 * C[i] + ob2 * (g * g);
-    B[i] = b;
-    C[i] = c;
-    T a = A[i] - lr * (b / c1) / sqrt((c / c2) + eps);
-    if (has_lb) a = a > lb ? a : lb;
-    A[i] = a;
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -219,6 +219,21 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
       s.flag = a.g_flag ? a.g_flag[t] : 0;
     }
   }
+  // Factor tables larger than L2 (C5: 531 MB): pull this sample's rows (and
+  // its gradient rows, so the reductions hit L2) in while the previous tile
+  // computes.  Rows are 32-byte aligned; one line prefetch per 128 bytes.
+  if (a.prefetch && s.valid) {
+#pragma unroll
+    for (int k = 0; k < DM; ++k) {
+      if (EXACT || k < d) {
+        const int64_t ro = a.off[k] + static_cast<int64_t>(ik[k]) * a.rp;
+        for (int b = 0; b < a.rp * static_cast<int>(sizeof(T)); b += 128) {
+          prefetch_l2(reinterpret_cast<const char*>(a.A + ro) + b);
+          prefetch_l2(reinterpret_cast<const char*>(a.G + ro) + b);
+        }
+      }
+    }
+  }
 }
 
 template <typename T, int DM, bool EXACT, int G, int VPL, bool REC>
@@ -435,6 +450,195 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
   return go(fused_grad_kernel<T, DM, EXACT, 32, 8, REC, 1>);
 }
 
+
+// ---------------------------------------------------------------------------
+// Staged variant for factor tables that exceed L2 (C5: 531 MB).  Phase A of
+// tile i+1 also issues cp.async copies of each sample's d factor rows into a
+// per-warp double buffer in shared memory (lane = sample, 16-byte copies, no
+// registers held), so the HBM gather latency of the next tile overlaps the
+// current tile's Phase B, which reads its rows from shared memory.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename T, int DM>
+__device__ __forceinline__ void stage_rows(const FusedArgs<T>& a, T* slot,
+                                           const uint32_t (&ik)[DM], bool valid) {
+  constexpr int VW = Vec<T>::W;
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < DM; ++k) {
+      const T* src = a.A + a.off[k] + static_cast<int64_t>(ik[k]) * a.rp;
+      for (int c = 0; c < a.nchunks; ++c) cp_async16(slot + k * a.rp + c * VW, src + c * VW);
+    }
+  }
+  cp_async_commit();
+}
+
+template <typename T, int DM, int G>
+__device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegRegs& sg,
+                                               const T* wbuf, const Drawn<T>& s,
+                                               const uint32_t (&ik)[DM], T* __restrict__ Gb) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int NGRP = 32 / G;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const bool given = sg.kind == SEG_GIVEN;
+  const T wseg = static_cast<T>(sg.weight);
+  const int cidx = gl < a.nchunks ? gl : a.nchunks - 1;
+  const T cmask = gl < a.nchunks ? static_cast<T>(1) : static_cast<T>(0);
+  const bool owns = gl < a.nchunks;
+#pragma unroll 1
+  for (int pass = 0; pass < G; ++pass) {
+    const int src = pass * NGRP + grp;
+    const bool v = __shfl_sync(FULL, s.valid, src);
+    uint32_t ii[DM];
+#pragma unroll
+    for (int k = 0; k < DM; ++k) ii[k] = __shfl_sync(FULL, ik[k], src);
+    const T xv = __shfl_sync(FULL, s.x, src);
+    T wv = wseg;
+    int fv = sg.flag;
+    if (given) {
+      wv = static_cast<T>(__shfl_sync(FULL, s.w, src));
+      fv = __shfl_sync(FULL, s.flag, src);
+    }
+    const T* rows = wbuf + src * DM * a.rp;
+    T row[DM][VW], pre[DM][VW];
+#pragma unroll
+    for (int k = 0; k < DM; ++k) {
+      Vec<T> q;
+      if constexpr (sizeof(T) == 4) {
+        const float4 f = *reinterpret_cast<const float4*>(rows + k * a.rp + cidx * VW);
+        q.v[0] = f.x, q.v[1] = f.y, q.v[2] = f.z, q.v[3] = f.w;
+      } else {
+        const double2 f = *reinterpret_cast<const double2*>(rows + k * a.rp + cidx * VW);
+        q.v[0] = f.x, q.v[1] = f.y;
+      }
+#pragma unroll
+      for (int e = 0; e < VW; ++e) row[k][e] = q.v[e];
+    }
+    T mp = static_cast<T>(0);
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      T p = row[0][e];
+      pre[0][e] = static_cast<T>(1);
+#pragma unroll
+      for (int k = 1; k < DM; ++k) {
+        pre[k][e] = p;
+        p = p * row[k][e];
+      }
+      mp += p;
+    }
+    mp *= cmask;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
+    T g = loss_deriv_fast(a.loss, a.delta, xv, mp);
+    if (fv) g = g - loss_deriv_fast(a.loss, a.delta, static_cast<T>(0), mp);
+    const T y = wv * g;
+    if (a.scatter && v && owns) {
+      T suf[VW];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) suf[e] = static_cast<T>(1);
+#pragma unroll
+      for (int k = DM - 1; k >= 0; --k) {
+        T out[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          out[e] = y * (pre[k][e] * suf[e]);
+          suf[e] = suf[e] * row[k][e];
+        }
+        red_chunk(Gb + static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.rp) +
+                      cidx * VW,
+                  out);
+      }
+    }
+  }
+}
+
+template <typename T, int DM, int G>
+__global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T> a,
+                                                              int64_t total_tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  T* Gb = a.G + static_cast<int64_t>(blockIdx.x % a.nrep) * a.rep_stride;
+  const int slot_elems = DM * a.rp;              // one sample's rows
+  T* wbuf = reinterpret_cast<T*>(smem_raw) + static_cast<int64_t>(wib) * 2 * 32 * slot_elems;
+  const uint64_t iter = a.iter + (a.iter_base ? __ldg(a.iter_base) : 0ull);
+  int64_t tile = warp0;
+  if (tile >= total_tiles) return;
+  uint32_t ik[DM];
+  Drawn<T> s;
+  SegRegs sg = seg_of<T>(a, tile);
+  phase_a<T, DM, true>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik, s);
+  int buf = 0;
+  stage_rows<T, DM>(a, wbuf + (buf * 32 + lane) * slot_elems, ik, s.valid);
+  for (; tile < total_tiles; tile += nwarps) {
+    const int64_t next = tile + nwarps;
+    uint32_t ik2[DM];
+    Drawn<T> s2;
+    SegRegs sg2 = sg;
+    if (next < total_tiles) {
+      sg2 = seg_of<T>(a, next);
+      phase_a<T, DM, true>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, iter, ik2,
+                           s2);
+    } else {
+      s2.valid = false;
+#pragma unroll
+      for (int k = 0; k < DM; ++k) ik2[k] = 0;
+    }
+    stage_rows<T, DM>(a, wbuf + ((buf ^ 1) * 32 + lane) * slot_elems, ik2, s2.valid);
+    cp_async_wait<1>();  // this tile's rows have landed; the next tile's stay in flight
+    __syncwarp();
+    phase_b_staged<T, DM, G>(a, sg, wbuf + buf * 32 * slot_elems, s, ik, Gb);
+    __syncwarp();        // the buffer is restaged two tiles later
+#pragma unroll
+    for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
+    s = s2;
+    sg = sg2;
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+template <typename T, int DM>
+bool launch_staged(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream, int num_sms,
+                   cudaError_t* err) {
+  const int G = pow2ceil(a.nchunks);
+  const size_t smem = static_cast<size_t>(8) * 2 * 32 * DM * a.rp * sizeof(T);
+  if (G > 8 || smem > 110 * 1024) return false;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (total_tiles + 7) / 8;
+    const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(a, total_tiles);
+    *err = cudaGetLastError();
+  };
+  switch (G) {
+    case 1: go(fused_staged_kernel<T, DM, 1>); break;
+    case 2: go(fused_staged_kernel<T, DM, 2>); break;
+    case 4: go(fused_staged_kernel<T, DM, 4>); break;
+    default: go(fused_staged_kernel<T, DM, 8>); break;
+  }
+  return true;
+}
+
 template <typename T, bool REC>
 cudaError_t launch_fused_rec(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
                              int num_sms) {
@@ -453,6 +657,12 @@ template <typename T>
 cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
                          cudaStream_t stream, int num_sms) {
   if (total_tiles <= 0) return cudaSuccess;
+  if (!record && a.stage && a.g_y == nullptr && (a.d == 3 || a.d == 4)) {
+    cudaError_t err = cudaSuccess;
+    const bool done = a.d == 3 ? launch_staged<T, 3>(a, total_tiles, stream, num_sms, &err)
+                               : launch_staged<T, 4>(a, total_tiles, stream, num_sms, &err);
+    if (done) return err;
+  }
   if (record) return launch_fused_rec<T, true>(a, total_tiles, stream, num_sms);
   return launch_fused_rec<T, false>(a, total_tiles, stream, num_sms);
 }

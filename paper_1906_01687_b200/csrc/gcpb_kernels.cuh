@@ -90,6 +90,8 @@ struct FusedArgs {
   double* r_m;
   double* r_y;
   int scatter;
+  int prefetch;  // 1: prefetch the next tile's rows into L2 (opt-in)
+  int stage;     // 1: factor tables exceed L2 -> cp.async-staged kernel variant
 };
 
 // ---------------------------------------------------------------------------
@@ -173,6 +175,13 @@ __device__ __forceinline__ void load_chunk(const double* p, Vec<double>& out) {
   out.v[1] = q.y;
 }
 
+__device__ __forceinline__ void store_chunk(float* p, const Vec<float>& v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
+}
+__device__ __forceinline__ void store_chunk(double* p, const Vec<double>& v) {
+  *reinterpret_cast<double2*>(p) = make_double2(v.v[0], v.v[1]);
+}
+
 // Scatter-add of one chunk: red.global.add.v4.f32 (one 16-byte vector
 // reduction in L2) for fp32, two red.global.add.f64 for fp64.
 __device__ __forceinline__ void red_chunk(float* p, const float (&v)[4]) {
@@ -212,6 +221,10 @@ __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const uint64_t* p) {
                : "=l"(v.x), "=l"(v.y)
                : "l"(p));
   return v;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
 // Open-addressing membership test: 2^b buckets of four u64 keys (one 32-byte
