@@ -38,6 +38,10 @@
 #ifndef GCPB_MINB
 #define GCPB_MINB 3
 #endif
+// Same for the slim hot-path kernels (no host-given samples, no recording).
+#ifndef GCPB_MINB_SLIM
+#define GCPB_MINB_SLIM 4
+#endif
 
 namespace gcpb {
 
@@ -107,15 +111,17 @@ __device__ __forceinline__ SegRegs seg_of(const FusedArgs<T>& a, int64_t tile) {
 }
 
 // Phase A: lane-per-sample draw of ordinal t of segment sg.
-template <typename T, int DM, bool EXACT>
+template <typename T, int DM, bool EXACT, bool GV = true>
 __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg, int64_t t,
                                         uint64_t iter, uint32_t (&ik)[DM], Drawn<T>& s) {
   const int d = EXACT ? DM : a.d;
   s.valid = t < sg.t_end;
   s.x = static_cast<T>(0);
-  s.w = sg.weight;
-  s.flag = sg.flag;
-  s.yg = 0.0;
+  if (GV) {
+    s.w = sg.weight;
+    s.flag = sg.flag;
+    s.yg = 0.0;
+  }
 #pragma unroll
   for (int k = 0; k < DM; ++k) ik[k] = 0;
   if (!s.valid) return;
@@ -207,7 +213,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
         s.x = static_cast<T>(__hiloint2double(static_cast<int>(wds[1]), static_cast<int>(wds[0])));
       }
     }
-  } else {  // SEG_GIVEN
+  } else if (GV) {  // SEG_GIVEN
 #pragma unroll
     for (int k = 0; k < DM; ++k)
       if (EXACT || k < d) ik[k] = static_cast<uint32_t>(a.g_idx[t * d + k]);
@@ -236,7 +242,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
-template <typename T, int DM, bool EXACT, int G, int VPL, bool REC>
+template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, bool GV>
 __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg, int64_t tile,
                                         const uint32_t (&ik)[DM], const Drawn<T>& s,
                                         T* __restrict__ Gb) {
@@ -248,7 +254,7 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   const int grp = lane / G;
   const int gl = lane % G;
   const int d = EXACT ? DM : a.d;
-  const bool given = sg.kind == SEG_GIVEN;
+  const bool given = GV && sg.kind == SEG_GIVEN;
   const bool ygiven = given && a.g_y != nullptr;
   const T wseg = static_cast<T>(sg.weight);
   // Chunk ownership, clamped so every load stays inside its row; masks zero
@@ -274,11 +280,13 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
     double wd = sg.weight;
     int fv = sg.flag;
     double yg = 0.0;
-    if (given) {  // warp-uniform
-      wd = __shfl_sync(FULL, s.w, src);
-      wv = static_cast<T>(wd);
-      fv = __shfl_sync(FULL, s.flag, src);
-      yg = __shfl_sync(FULL, s.yg, src);
+    if constexpr (GV) {
+      if (given) {  // warp-uniform
+        wd = __shfl_sync(FULL, s.w, src);
+        wv = static_cast<T>(wd);
+        fv = __shfl_sync(FULL, s.flag, src);
+        yg = __shfl_sync(FULL, s.yg, src);
+      }
     }
     // Row offsets (32-bit element offsets; factor buffers < 2^32 elements).
     uint32_t roff[DM];
@@ -368,7 +376,7 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
-template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB>
+template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
                                                                int64_t total_tiles) {
   const int lane = threadIdx.x & 31;
@@ -383,7 +391,8 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
   uint32_t ik[DM];
   Drawn<T> s;
   SegRegs sg = seg_of<T>(a, tile);
-  phase_a<T, DM, EXACT>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik, s);
+  phase_a<T, DM, EXACT, GV>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik,
+                            s);
   for (; tile < total_tiles; tile += nwarps) {
     const int64_t next = tile + nwarps;
     uint32_t ik2[DM];
@@ -391,14 +400,14 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
     SegRegs sg2 = sg;
     if (next < total_tiles) {  // prefetch: next tile's draws + tensor gathers in flight
       sg2 = seg_of<T>(a, next);
-      phase_a<T, DM, EXACT>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, iter, ik2,
-                            s2);
+      phase_a<T, DM, EXACT, GV>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, iter,
+                                ik2, s2);
     } else {
       s2.valid = false;
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
-    phase_b<T, DM, EXACT, G, VPL, REC>(a, sg, tile, ik, s, Gb);
+    phase_b<T, DM, EXACT, G, VPL, REC, GV>(a, sg, tile, ik, s, Gb);
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
     s = s2;
@@ -424,6 +433,8 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
     G = 32;
     vpl = pow2ceil((nchunks + 31) / 32);
   }
+  bool given = false;
+  for (int s = 0; s < a.nseg; ++s) given = given || a.seg[s].kind == SEG_GIVEN;
   auto go = [&](auto kern) -> cudaError_t {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
@@ -436,6 +447,18 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
     return cudaGetLastError();
   };
   if (vpl == 1) {
+    if constexpr (!REC && EXACT) {
+      if (!given) {  // hot path: no host-given samples -> slim live state
+        switch (G) {
+          case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, GCPB_MINB_SLIM, false>);
+          case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, GCPB_MINB_SLIM, false>);
+          case 4: return go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, GCPB_MINB_SLIM, false>);
+          case 8: return go(fused_grad_kernel<T, DM, EXACT, 8, 1, REC, GCPB_MINB_SLIM, false>);
+          case 16: return go(fused_grad_kernel<T, DM, EXACT, 16, 1, REC, GCPB_MINB_SLIM, false>);
+          default: return go(fused_grad_kernel<T, DM, EXACT, 32, 1, REC, GCPB_MINB_SLIM, false>);
+        }
+      }
+    }
     switch (G) {
       case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, GCPB_MINB>);
       case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, GCPB_MINB>);
@@ -449,7 +472,6 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
   if (vpl <= 4) return go(fused_grad_kernel<T, DM, EXACT, 32, 4, REC, 1>);
   return go(fused_grad_kernel<T, DM, EXACT, 32, 8, REC, 1>);
 }
-
 
 // ---------------------------------------------------------------------------
 // Staged variant for factor tables that exceed L2 (C5: 531 MB).  Phase A of
