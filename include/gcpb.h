@@ -278,6 +278,15 @@ int gcpb_nccl_unique_id(char out[128]);
 int gcpb_comm_init(gcpb_ctx* ctx, const char unique_id[128], int rank, int nranks);
 int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks);
 int gcpb_allreduce_grad(gcpb_ctx* ctx);
+/* Host-callback communicator, an alternative to NCCL for process groups the
+ * caller already has (gloo, MPI) and for in-process multi-context tests:
+ * allgather: recv[i] = the value rank i sent (nranks entries);
+ * allreduce: in-place element-wise sum of n doubles across ranks.
+ * Callbacks return 0 on success.  Graph-replayed steps need NCCL. */
+typedef int (*gcpb_allgather_i64_fn)(void* user, int64_t send, int64_t* recv);
+typedef int (*gcpb_allreduce_f64_fn)(void* user, double* buf, int64_t n);
+int gcpb_comm_init_host(gcpb_ctx* ctx, int rank, int nranks, gcpb_allgather_i64_fn allgather,
+                        gcpb_allreduce_f64_fn allreduce, void* user);
 
 /* ---- host-only helpers (no device needed) ----------------------------------------- */
 /* Product Philox stream: bounded draw in [0, n). */

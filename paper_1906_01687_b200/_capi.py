@@ -60,6 +60,9 @@ class gcpb_trace_record(C.Structure):
                 ("learning_rate", C.c_double), ("seconds", C.c_double), ("accepted", C.c_int32)]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64))
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+
 ctx_p = C.c_void_p
 i64p = C.POINTER(C.c_int64)
 f64p = C.POINTER(C.c_double)
@@ -121,6 +124,8 @@ SIGNATURES = [
     ("gcpb_comm_init", C.c_int, [ctx_p, C.c_char_p, C.c_int, C.c_int]),
     ("gcpb_set_shard", C.c_int, [ctx_p, C.c_int, C.c_int]),
     ("gcpb_allreduce_grad", C.c_int, [ctx_p]),
+    ("gcpb_comm_init_host", C.c_int, [ctx_p, C.c_int, C.c_int, ALLGATHER_FN, ALLREDUCE_FN,
+                                      C.c_void_p]),
     ("gcpb_philox_bounded", C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                          C.c_uint64]),
     ("gcpb_zero_batch_size", C.c_int64, [C.c_double, C.c_double, C.c_double, C.c_int64]),

@@ -208,9 +208,15 @@ struct gcpb_ctx {
   std::string graph_key;
   int64_t tensor_version = 0;
 
-  // sharding
+  // sharding and communicator (NCCL or host callbacks)
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  gcpb_allgather_i64_fn host_allgather = nullptr;
+  gcpb_allreduce_f64_fn host_allreduce = nullptr;
+  void* host_user = nullptr;
+  DBuf comm_buf;
+  DBuf zscratch;  // multi-rank stratified: this rank's accepts of one batch
+  int64_t zscratch_cap = 0;
 
   // stratified zero sampler
   DBuf zero_list, zstatus;
@@ -645,6 +651,131 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   }
 }
 
+// ---- communicator helpers -----------------------------------------------------
+bool has_comm(const gcpb_ctx* c) { return c->comm != nullptr || c->host_allgather != nullptr; }
+
+std::vector<int64_t> comm_allgather_i64(gcpb_ctx* c, int64_t v) {
+  std::vector<int64_t> out(static_cast<size_t>(c->nranks), 0);
+  if (c->nranks == 1) {
+    out[0] = v;
+    return out;
+  }
+  if (c->host_allgather) {
+    c->sync();
+    if (c->host_allgather(c->host_user, v, out.data()) != 0)
+      throw std::runtime_error("host allgather callback failed");
+    return out;
+  }
+  if (!c->comm) throw std::logic_error("multi-rank call without a communicator");
+  c->comm_buf.alloc(static_cast<size_t>(c->nranks + 1) * sizeof(int64_t));
+  int64_t* d = c->comm_buf.as<int64_t>();
+  CK(cudaMemcpyAsync(d + c->nranks, &v, 8, cudaMemcpyHostToDevice, c->stream));
+  nck(ncclAllGather(d + c->nranks, d, 1, ncclInt64, c->comm, c->stream), "ncclAllGather");
+  CK(cudaMemcpyAsync(out.data(), d, c->nranks * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  return out;
+}
+
+template <typename T>
+void comm_allreduce_grad(gcpb_ctx* c) {
+  if (c->nranks == 1) return;
+  if (c->comm) {
+    nck(ncclAllReduce(c->Gr.p, c->Gr.p, static_cast<size_t>(c->nelem),
+                      sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclSum, c->comm, c->stream),
+        "ncclAllReduce");
+    return;
+  }
+  if (!c->host_allreduce) throw std::logic_error("multi-rank call without a communicator");
+  std::vector<T> h(static_cast<size_t>(c->nelem));
+  CK(cudaMemcpyAsync(h.data(), c->Gr.p, c->nelem * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  std::vector<double> hd(h.begin(), h.end());
+  if (c->host_allreduce(c->host_user, hd.data(), c->nelem) != 0)
+    throw std::runtime_error("host allreduce callback failed");
+  for (size_t i = 0; i < h.size(); ++i) h[i] = static_cast<T>(hd[i]);
+  CK(cudaMemcpyAsync(c->Gr.p, h.data(), c->nelem * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  c->sync();
+}
+
+// Multi-rank stratified zero sampler: every rank runs the
+// reference's batch formula on the global shortfall, tests its contiguous
+// slice of the batch's candidate ordinals, all-gathers its accept count, and
+// keeps the accepts whose global rank (candidate order = rank order) is below
+// the remaining need — exactly the first q non-hits of the single-rank run.
+// Returns this rank's kept count (its zero_list prefix).
+int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t seed,
+                                   uint64_t iter, uint32_t tag, gcpb_stats* stats) {
+  ensure_hash(c);
+  const double zeta = static_cast<double>(c->total128 - static_cast<unsigned __int128>(c->nnz));
+  if (c->zero_cap < q) {
+    c->zero_list.alloc(static_cast<size_t>(q) * sizeof(uint64_t));
+    c->zero_cap = q;
+  }
+  DevState* st = c->dst();
+  ZeroArgs za;
+  std::memset(&za, 0, sizeof(za));
+  za.d = c->d;
+  uint64_t stride = 1;
+  for (int k = 0; k < c->d; ++k) {
+    za.dims[k] = static_cast<uint32_t>(c->dims[k]);
+    za.thr[k] = lemire_threshold32(static_cast<uint64_t>(c->dims[k]));
+    za.stride[k] = stride;
+    stride *= static_cast<uint64_t>(c->dims[k]);
+  }
+  za.seed = seed;
+  za.iter = iter;
+  za.tag = tag;
+  za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
+  za.hmask = c->hmask;
+  za.st = st;
+  int64_t tested = 0, accepted = 0, kept_local = 0;
+  while (std::min(accepted, q) < q) {
+    const int64_t batch = zero_batch_size_dev(c->total_d, zeta, rho, q - accepted);
+    int64_t lo = 0, hi = 0;
+    gcpb_shard_range(batch, c->rank, c->nranks, &lo, &hi);
+    const int64_t size = hi - lo;
+    int64_t mine = 0;
+    if (size > 0) {
+      const int64_t nchunks = (size + kZcChunk - 1) / kZcChunk;
+      if (c->zstatus_cap < nchunks) {
+        c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
+        c->zstatus_cap = nchunks;
+      }
+      if (c->zscratch_cap < size) {
+        c->zscratch.alloc(static_cast<size_t>(size) * sizeof(uint64_t));
+        c->zscratch_cap = size;
+      }
+      CK(cudaMemsetAsync(c->zstatus.p, 0, static_cast<size_t>(nchunks) * 8, c->stream));
+      CK(cudaMemcpyAsync(&st->z_status_cap, &c->zstatus_cap, 8, cudaMemcpyHostToDevice,
+                         c->stream));
+      zero_plan_slice_kernel<<<1, 1, 0, c->stream>>>(st, tested + lo, size, nchunks);
+      za.status = c->zstatus.as<unsigned long long>();
+      za.zero_list = c->zscratch.as<uint64_t>();
+      const int grid =
+          static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
+      zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(&mine, &st->z_accepted, 8, cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+    }
+    const std::vector<int64_t> counts = comm_allgather_i64(c, mine);
+    int64_t offset = 0, keep = 0;
+    gcpb_stratified_keep(counts.data(), c->nranks, c->rank, q - accepted, &offset, &keep);
+    if (keep > 0)
+      CK(cudaMemcpyAsync(c->zero_list.as<uint64_t>() + kept_local, c->zscratch.p,
+                         static_cast<size_t>(keep) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    kept_local += keep;
+    for (int64_t v : counts) accepted += v;
+    tested += batch;
+  }
+  if (stats) {
+    stats->tested = tested;
+    stats->accepted = accepted;
+    stats->rejected = tested - accepted;
+  }
+  return kept_local;
+}
+
 struct SampleResult {
   int64_t n = 0;
   gcpb_stats stats{0, 0, 0};
@@ -701,12 +832,20 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   }
   const double eta_over_p = p > 0 ? static_cast<double>(eta) / static_cast<double>(p) : 0.0;
   const bool strat = sk->strategy == GCPB_STRATIFIED;
+  int64_t zero_kept_local = q;
   if (strat && q > 0) {
     if (zeta128 < static_cast<unsigned __int128>(q))
       throw std::invalid_argument("sample_zeros_rejection: requested " + std::to_string(q) +
                                   " zeros but only " + u128_to_string(zeta128) + " exist");
-    if (c->nranks > 1) throw std::invalid_argument("stratified sampling is single-rank in v1");
-    run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode);
+    if (c->nranks > 1) {
+      if (zero_mode != ZERO_HOST_CHECK || record)
+        throw std::invalid_argument(
+            "multi-rank stratified sampling runs host-checked (gcpb_stoch_grad / gcpb_step)");
+      zero_kept_local = run_zero_sampler_multirank(c, q, sk->oversample, seed, iter, tag_z,
+                                                   &res.stats);
+    } else {
+      run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode);
+    }
     a.zero_list = c->zero_list.as<uint64_t>();
   }
   a.nseg = 0;
@@ -718,7 +857,8 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   if (q > 0) {
     const double zeta_d = static_cast<double>(zeta128);
     if (strat) {
-      a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, tag_z, 0, q, zeta_d / static_cast<double>(q), 0, p);
+      a.seg[a.nseg++] =
+          make_seg(SEG_ZERO_LIST, tag_z, 0, zero_kept_local, zeta_d / static_cast<double>(q), 0, p);
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1,
@@ -727,7 +867,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   }
   res.n = p + q;
   run_fused(c, a, record, fold);
-  if (strat && q > 0 && zero_mode == ZERO_HOST_CHECK) {
+  if (strat && q > 0 && zero_mode == ZERO_HOST_CHECK && c->nranks == 1) {
     res.stats.tested = c->host_state.z_tested;
     res.stats.accepted = c->host_state.z_accepted;
     res.stats.rejected = c->host_state.z_rejected;
@@ -898,10 +1038,10 @@ void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint6
                      iter_base, /*fold=*/!multi, zero_mode);
   int fold = 0;
   if (multi) {
-    if (!c->comm) throw std::logic_error("sharded step without an NCCL communicator");
-    nck(ncclAllReduce(c->Gr.p, c->Gr.p, static_cast<size_t>(c->nelem),
-                      c->dtype == GCPB_F32 ? ncclFloat : ncclDouble, ncclSum, c->comm, c->stream),
-        "ncclAllReduce");
+    if (!has_comm(c)) throw std::logic_error("sharded step without a communicator");
+    if (!c->comm && zero_mode == ZERO_CAPTURE)
+      throw std::invalid_argument("graph-replayed multi-rank steps need an NCCL communicator");
+    comm_allreduce_grad<T>(c);
   } else if (c->nrep > 1) {
     fold = c->nrep;
   }
@@ -1987,11 +2127,24 @@ int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks) {
 int gcpb_allreduce_grad(gcpb_ctx* ctx) {
   return guard(ctx, [&] {
     if (ctx->nranks == 1) return;
-    if (!ctx->comm) throw std::logic_error("allreduce without an NCCL communicator");
-    nck(ncclAllReduce(ctx->Gr.p, ctx->Gr.p, static_cast<size_t>(ctx->nelem),
-                      ctx->dtype == GCPB_F32 ? ncclFloat : ncclDouble, ncclSum, ctx->comm,
-                      ctx->stream),
-        "ncclAllReduce");
+    if (!has_comm(ctx)) throw std::logic_error("allreduce without a communicator");
+    if (ctx->dtype == GCPB_F32)
+      comm_allreduce_grad<float>(ctx);
+    else
+      comm_allreduce_grad<double>(ctx);
+  });
+}
+
+int gcpb_comm_init_host(gcpb_ctx* ctx, int rank, int nranks, gcpb_allgather_i64_fn allgather,
+                        gcpb_allreduce_f64_fn allreduce, void* user) {
+  return guard(ctx, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank/nranks");
+    if (!allgather || !allreduce) throw std::invalid_argument("host communicator needs callbacks");
+    ctx->host_allgather = allgather;
+    ctx->host_allreduce = allreduce;
+    ctx->host_user = user;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
   });
 }
 

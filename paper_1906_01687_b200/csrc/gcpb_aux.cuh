@@ -93,6 +93,23 @@ __global__ void zero_plan_kernel(DevState* st, int first) {
   st->z_nchunks = nchunks;
 }
 
+// Multi-rank stratified: the host plans the batch; this rank tests the slice
+// [begin, begin + size) and collects its accepts (local ranks) from 0.
+__global__ void zero_plan_slice_kernel(DevState* st, int64_t begin, int64_t size,
+                                       int64_t nchunks) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  st->z_tested = 0;
+  st->z_accepted = 0;
+  st->z_rejected = 0;
+  st->z_acc_before = 0;
+  st->z_q = size;
+  st->z_ticket = 0;
+  st->z_batch_tag += 1;
+  st->z_batch_begin = begin;
+  st->z_batch_size = size;
+  st->z_nchunks = nchunks;
+}
+
 // Graph mode: counts steps whose device-planned batches did not yield q zeros.
 __global__ void zero_check_kernel(DevState* st) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && st->z_accepted < st->z_q) st->z_incomplete += 1;

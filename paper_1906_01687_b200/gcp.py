@@ -515,6 +515,32 @@ class Engine:
     def allreduce_grad(self) -> None:
         self._ck(lib.gcpb_allreduce_grad(self._h))
 
+    def comm_init_host(self, rank: int, nranks: int,
+                       allgather: Callable[[int], Sequence[int]],
+                       allreduce: Callable[[np.ndarray], None]) -> None:
+        """Host-callback communicator: allgather(value) -> list of nranks ints;
+        allreduce(array) sums the float64 array across ranks in place."""
+        def _ag(user, send, recv):
+            try:
+                vals = allgather(int(send))
+                for i, v in enumerate(vals):
+                    recv[i] = int(v)
+                return 0
+            except Exception:  # surfaced as GCPB_ERR_RUNTIME
+                return 1
+
+        def _ar(user, buf, n):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(n,))
+                allreduce(arr)
+                return 0
+            except Exception:
+                return 1
+
+        self._comm_cbs = (_capi.ALLGATHER_FN(_ag), _capi.ALLREDUCE_FN(_ar))
+        self._ck(lib.gcpb_comm_init_host(self._h, rank, nranks, self._comm_cbs[0],
+                                         self._comm_cbs[1], None))
+
 
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)

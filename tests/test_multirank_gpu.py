@@ -1,0 +1,131 @@
+"""Multi-rank decomposition on one GPU, through the engine's host-callback
+communicator (NCCL refuses two ranks on one device).  R contexts, one per
+"rank", run in R host threads; the callbacks exchange accept counts and
+gradients through a barrier-synchronised hub.  No kernel ever waits on
+another rank's kernel — every exchange is a host-level synchronisation.
+
+Checks, for every sampler: the multi-rank gradient (sharded samples + summed
+gradient) equals the single-rank gradient, and for the stratified sampler the
+global RejectionStats and the kept zero set equal the single-rank run's
+(first q non-hits in candidate order).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+class Hub:
+    def __init__(self, n):
+        self.n = n
+        self.barrier = threading.Barrier(n)
+        self.slots = [None] * n
+
+    def allgather(self, rank, v):
+        self.slots[rank] = v
+        self.barrier.wait()
+        out = list(self.slots)
+        self.barrier.wait()
+        return out
+
+    def allreduce(self, rank, arr):
+        self.slots[rank] = arr.copy()
+        self.barrier.wait()
+        total = np.sum(self.slots, axis=0)
+        self.barrier.wait()
+        arr[:] = total
+
+
+def _problem(seed):
+    rs = np.random.default_rng(seed)
+    dims, r = (40, 30, 20, 10), 6
+    lin = np.nonzero(rs.random(int(np.prod(dims))) < 0.03)[0]
+    coords = np.stack(np.unravel_index(lin, dims, order="F"), 1)
+    vals = np.ones(len(lin))
+    F = [rs.uniform(0.1, 1.0, (n, r)) for n in dims]
+    return dims, r, coords, vals, F
+
+
+def _run_ranks(nranks, fn):
+    out = [None] * nranks
+    err = []
+
+    def worker(rank):
+        try:
+            out[rank] = fn(rank)
+        except Exception as ex:  # pragma: no cover - surfaced below
+            err.append(ex)
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+def test_multirank_gradient_equals_single_rank(nranks, strategy):
+    import paper_1906_01687_b200.gcp as G
+    dims, r, coords, vals, F = _problem(11 + strategy)
+    sk = {0: G.SamplerKind.uniform(5000), 1: G.SamplerKind.stratified(1500, 2500, 1.05),
+          2: G.SamplerKind.semi_stratified(1500, 2500)}[strategy]
+    lf = G.LossFunction.bernoulli_odds()
+    single = G.Engine(dims, r, "f64")
+    single.set_sparse(coords, vals)
+    single.set_factors(F)
+    st1 = single.stoch_grad(sk, lf, 5, 2)
+    want = single.grad_flat()
+    hub = Hub(nranks)
+
+    def rank_fn(rank):
+        e = G.Engine(dims, r, "f64")
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.comm_init_host(rank, nranks, lambda v: hub.allgather(rank, v),
+                         lambda a: hub.allreduce(rank, a))
+        st = e.stoch_grad(sk, lf, 5, 2)
+        e.allreduce_grad()
+        return st, e.grad_flat()
+
+    res = _run_ranks(nranks, rank_fn)
+    for st, g in res:
+        assert O.rel_error(g, want) <= 1e-12
+        if strategy == 1:
+            assert (st.tested, st.accepted, st.rejected) == (st1.tested, st1.accepted, st1.rejected)
+
+
+def test_multirank_steps_match_single_rank():
+    """gcpb_step with the host communicator: sharded samples, summed gradient,
+    replicated Adam keep the factor replicas identical to a single-rank run."""
+    import paper_1906_01687_b200.gcp as G
+    dims, r, coords, vals, F = _problem(29)
+    sk, lf = G.SamplerKind.stratified(800, 1200, 1.1), G.LossFunction.bernoulli_odds()
+    single = G.Engine(dims, r, "f64")
+    single.set_sparse(coords, vals)
+    single.set_factors(F)
+    for it in range(4):
+        single.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+    want = single.factors()
+    hub = Hub(2)
+
+    def rank_fn(rank):
+        e = G.Engine(dims, r, "f64")
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.comm_init_host(rank, 2, lambda v: hub.allgather(rank, v),
+                         lambda a: hub.allreduce(rank, a))
+        for it in range(4):
+            e.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+        return e.factors()
+
+    for got in _run_ranks(2, rank_fn):
+        for x, y in zip(got, want):
+            assert O.rel_error(x, y) <= 1e-12
