@@ -215,6 +215,17 @@ int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
  * the summed event time and the number of timed launches. */
 int gcpb_kernel_timing(gcpb_ctx* ctx, int enable);
 int gcpb_kernel_time(gcpb_ctx* ctx, double* total_ms, int64_t* launches);
+/* Draw stream of the samplers.  kind 0 (default): the Philox stream, `seed`
+ * is its key and `iter` the iteration.  kind 1 (RefStream, parity mode): the
+ * reference's RngStream sequence (src/rng.cpp:43-61) — `seed` is the stream
+ * key (e.g. RngStream(s).split("gradients")), `iter` is ignored, and the
+ * draw counter lives on the device, starts at `counter` and advances by the
+ * draws each call consumes, in the reference's consumption order, so
+ * successive calls continue one stream exactly like draw_gradient_samples
+ * does.  A draw in next_below's rejection region (probability <= n/2^64) is
+ * reported by the next synchronising call. */
+int gcpb_set_draw_stream(gcpb_ctx* ctx, int kind, uint64_t counter);
+int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter);
 /* Wait for queued device work and report deferred device-side failures. */
 int gcpb_synchronize(gcpb_ctx* ctx);
 
@@ -240,6 +251,8 @@ typedef struct {
   int64_t max_epochs;
   uint64_t seed;
   int32_t keep_factors; /* 1: start from the factors already set */
+  int32_t draw_stream;  /* 0: Philox streams keyed by the split keys; 1: RefStream — the
+                           reference's own estimator and gradient draws */
 } gcpb_fit_config;
 
 /* FitTraceRecord (include/gcp/optimizer.hpp:30-36). */

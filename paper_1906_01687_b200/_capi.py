@@ -52,7 +52,8 @@ class gcpb_fit_config(C.Structure):
                 ("max_bad_epochs", C.c_int64), ("decay", C.c_double),
                 ("lower_bound_mode", C.c_int32), ("lower_bound", C.c_double),
                 ("estimator_samples", C.c_int64), ("estimator_kind", C.c_int32),
-                ("max_epochs", C.c_int64), ("seed", C.c_uint64), ("keep_factors", C.c_int32)]
+                ("max_epochs", C.c_int64), ("seed", C.c_uint64), ("keep_factors", C.c_int32),
+                ("draw_stream", C.c_int32)]
 
 
 class gcpb_trace_record(C.Structure):
@@ -109,6 +110,8 @@ SIGNATURES = [
     ("gcpb_run_steps", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
                                  C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(gcpb_adam)]),
     ("gcpb_synchronize", C.c_int, [ctx_p]),
+    ("gcpb_set_draw_stream", C.c_int, [ctx_p, C.c_int, C.c_uint64]),
+    ("gcpb_get_draw_counter", C.c_int, [ctx_p, u64p]),
     ("gcpb_kernel_timing", C.c_int, [ctx_p, C.c_int]),
     ("gcpb_kernel_time", C.c_int, [ctx_p, f64p, i64p]),
     ("gcpb_fit_gcp_adam", C.c_int, [ctx_p, C.POINTER(gcpb_loss), C.POINTER(gcpb_fit_config),

@@ -203,6 +203,9 @@ struct gcpb_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tevents;
   size_t tevents_used = 0;
 
+  // draw stream: 0 = Philox (default), 1 = RefStream (reference RngStream)
+  int draw_stream = 0;
+
   // graph-replayed iterations (gcpb_run_steps)
   cudaGraphExec_t graph_exec = nullptr;
   std::string graph_key;
@@ -455,6 +458,18 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   }
   a.seed = seed;
   a.iter = iter;
+  if (c->draw_stream == 1) {
+    a.refstream = 1;
+    a.ref_key = seed;
+    a.ref_ctr = &c->dst()->ref_ctr;
+    a.ref_flag = &c->dst()->ref_flag;
+    for (int k = 0; k < c->d; ++k) {
+      const uint64_t n = static_cast<uint64_t>(c->dims[k]);
+      a.thr64[k] = (0 - n) % n;
+    }
+    const uint64_t eta = static_cast<uint64_t>(c->nnz > 0 ? c->nnz : 1);
+    a.thr64_eta = (0 - eta) % eta;
+  }
   if (c->tensor_kind == 1) {
     a.xkind = c->dense_storage == GCPB_STORE_BIT
                   ? X_DENSE_BIT
@@ -552,9 +567,11 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   }
 }
 
-Seg make_seg(int kind, uint32_t tag, int64_t tb, int64_t te, double w, int flag, int64_t out) {
+Seg make_seg(int kind, uint32_t tag, int64_t tb, int64_t te, double w, int flag, int64_t out,
+             int64_t ref_off = 0) {
   Seg s;
   std::memset(&s, 0, sizeof(s));
+  s.ref_off = ref_off;
   s.kind = kind;
   s.tag = tag;
   s.t_begin = tb;
@@ -602,8 +619,19 @@ enum ZeroMode { ZERO_HOST_CHECK = 0, ZERO_DEVICE_ONLY = 1, ZERO_CAPTURE = 2 };
 // round trip; ZERO_HOST_CHECK then synchronises and continues host-side until
 // exactly q accepts exist (reference semantics for any q); ZERO_CAPTURE (graph
 // mode, prepared beforehand) only counts shortfalls on the device.
+void fill_refstream(const gcpb_ctx* c, ZeroArgs& za, uint64_t key, int64_t p_ref) {
+  if (c->draw_stream != 1) return;
+  za.refstream = 1;
+  za.ref_key = key;
+  za.ref_off = p_ref;
+  for (int k = 0; k < c->d; ++k) {
+    const uint64_t n = static_cast<uint64_t>(c->dims[k]);
+    za.thr64[k] = (0 - n) % n;
+  }
+}
+
 void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
-                      const uint64_t* iter_base, uint32_t tag, int mode) {
+                      const uint64_t* iter_base, uint32_t tag, int mode, int64_t p_ref = 0) {
   if (mode != ZERO_CAPTURE) prepare_zero_sampler(c, q, rho);
   const int64_t nchunks = c->z_nchunks_first;
   // Look-back words from earlier calls must not alias this call's batch tags.
@@ -629,6 +657,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   za.st = st;
   za.status = c->zstatus.as<unsigned long long>();
   za.zero_list = c->zero_list.as<uint64_t>();
+  fill_refstream(c, za, seed, p_ref);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
   for (int b = 0; b < 3; ++b) {
     zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, b == 0 ? 1 : 0);
@@ -704,7 +733,8 @@ void comm_allreduce_grad(gcpb_ctx* c) {
 // the remaining need — exactly the first q non-hits of the single-rank run.
 // Returns this rank's kept count (its zero_list prefix).
 int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t seed,
-                                   uint64_t iter, uint32_t tag, gcpb_stats* stats) {
+                                   uint64_t iter, uint32_t tag, gcpb_stats* stats,
+                                   int64_t p_ref = 0) {
   ensure_hash(c);
   const double zeta = static_cast<double>(c->total128 - static_cast<unsigned __int128>(c->nnz));
   if (c->zero_cap < q) {
@@ -728,6 +758,7 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
   za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
   za.hmask = c->hmask;
   za.st = st;
+  fill_refstream(c, za, seed, p_ref);
   int64_t tested = 0, accepted = 0, kept_local = 0;
   while (std::min(accepted, q) < q) {
     const int64_t batch = zero_batch_size_dev(c->total_d, zeta, rho, q - accepted);
@@ -811,10 +842,18 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     const double w = c->total_d / static_cast<double>(s);  // samplers.hpp:83
     a.nseg = 1;
     a.seg[0] = make_seg(SEG_UNIFORM, tag_u, b0, b1, w, 0, 0);
-    if (c->tensor_kind == 2) ensure_hash(c), a.hkeys = c->hkeys.as<uint64_t>(),
-                             a.hvals = c->hvals.as<uint32_t>(), a.hmask = c->hmask;
+    if (c->tensor_kind == 2) {
+      ensure_hash(c);
+      a.hkeys = c->hkeys.as<uint64_t>();
+      a.hvals = c->hvals.as<uint32_t>();
+      a.hmask = c->hmask;
+    }
     res.n = s;
     run_fused(c, a, record, fold);
+    if (c->draw_stream == 1) {  // sample_uniform consumed s * d draws
+      ref_advance_kernel<<<1, 1, 0, c->stream>>>(c->dst(), static_cast<uint64_t>(s) * c->d, 0, c->d);
+      CK(cudaGetLastError());
+    }
     return res;
   }
   // stratified / semi-stratified (samplers.hpp:141-219), estimator split
@@ -842,9 +881,9 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
         throw std::invalid_argument(
             "multi-rank stratified sampling runs host-checked (gcpb_stoch_grad / gcpb_step)");
       zero_kept_local = run_zero_sampler_multirank(c, q, sk->oversample, seed, iter, tag_z,
-                                                   &res.stats);
+                                                   &res.stats, p);
     } else {
-      run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode);
+      run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p);
     }
     a.zero_list = c->zero_list.as<uint64_t>();
   }
@@ -857,16 +896,27 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   if (q > 0) {
     const double zeta_d = static_cast<double>(zeta128);
     if (strat) {
-      a.seg[a.nseg++] =
-          make_seg(SEG_ZERO_LIST, tag_z, 0, zero_kept_local, zeta_d / static_cast<double>(q), 0, p);
+      a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, tag_z, 0, zero_kept_local,
+                                 zeta_d / static_cast<double>(q), 0, p, p);
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1,
-                                 c->total_d / static_cast<double>(q), 0, p);
+                                 c->total_d / static_cast<double>(q), 0, p, p);
     }
   }
   res.n = p + q;
   run_fused(c, a, record, fold);
+  if (c->draw_stream == 1) {  // p picks, then d draws per tested candidate / q draw
+    if (strat && q > 0 && c->nranks > 1)
+      ref_advance_kernel<<<1, 1, 0, c->stream>>>(
+          c->dst(), static_cast<uint64_t>(p + res.stats.tested * c->d), 0, c->d);
+    else if (strat && q > 0)
+      ref_advance_kernel<<<1, 1, 0, c->stream>>>(c->dst(), static_cast<uint64_t>(p), 1, c->d);
+    else
+      ref_advance_kernel<<<1, 1, 0, c->stream>>>(c->dst(), static_cast<uint64_t>(p + q * c->d), 0,
+                                                 c->d);
+    CK(cudaGetLastError());
+  }
   if (strat && q > 0 && zero_mode == ZERO_HOST_CHECK && c->nranks == 1) {
     res.stats.tested = c->host_state.z_tested;
     res.stats.accepted = c->host_state.z_accepted;
@@ -1066,7 +1116,7 @@ std::string steps_key(const gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss
                 static_cast<unsigned long long>(seed), static_cast<long long>(n),
                 static_cast<long long>(c->tensor_version), c->rank, c->nranks,
                 c->hash_ready ? 1 : 0);
-  return buf;
+  return std::string(buf) + (c->draw_stream ? "|ref" : "|philox");
 }
 
 template <typename T>
@@ -1119,6 +1169,14 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
 // stratified shortfalls).
 void sync_and_check(gcpb_ctx* c) {
   c->sync();
+  if (c->draw_stream == 1) {
+    uint32_t rf = 0;
+    CK(cudaMemcpyAsync(&rf, &c->dst()->ref_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (rf)
+      throw std::runtime_error("RefStream: a draw fell in RngStream::next_below's rejection "
+                               "region (p <= n/2^64); the reference would have redrawn");
+  }
   int32_t inc = 0;
   CK(cudaMemcpyAsync(&inc, &c->dst()->z_incomplete, 4, cudaMemcpyDeviceToHost, c->stream));
   c->sync();
@@ -1805,6 +1863,25 @@ int gcpb_kernel_time(gcpb_ctx* ctx, double* total_ms, int64_t* launches) {
   });
 }
 
+int gcpb_set_draw_stream(gcpb_ctx* ctx, int kind, uint64_t counter) {
+  return guard(ctx, [&] {
+    if (kind != 0 && kind != 1) throw std::invalid_argument("draw stream must be 0 or 1");
+    ctx->sync();
+    ctx->draw_stream = kind;
+    const uint32_t zero = 0;
+    CK(cudaMemcpyAsync(&ctx->dst()->ref_ctr, &counter, 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(&ctx->dst()->ref_flag, &zero, 4, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+  });
+}
+
+int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
+  return guard(ctx, [&] {
+    CK(cudaMemcpyAsync(counter, &ctx->dst()->ref_ctr, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
 int gcpb_synchronize(gcpb_ctx* ctx) {
   return guard(ctx, [&] { sync_and_check(ctx); });
 }
@@ -1852,6 +1929,10 @@ int gcpb_fit_gcp_adam(gcpb_ctx* ctx, const gcpb_loss* loss, const gcpb_fit_confi
     const HostRngStream root(cfg->seed);
     const uint64_t est_seed = root.split("estimator").key();
     const uint64_t grad_seed = root.split("gradients").key();
+    {
+      const int rc = gcpb_set_draw_stream(ctx, cfg->draw_stream == 1 ? 1 : 0, 0);
+      if (rc != GCPB_OK) throw std::runtime_error(ctx->err);
+    }
 
     // init (optimizer.cpp:80-82, kruskal.cpp:33-45,85-93)
     if (!cfg->keep_factors) {
@@ -2007,6 +2088,15 @@ int gcpb_estimator_draw(gcpb_ctx* ctx, int kind, int64_t count, double rho, uint
     const int64_t n = count;
     alloc_record(ctx, n);
     gcpb_loss l{GCPB_LOSS_GAUSSIAN, 0.0};
+    // RefStream: the estimator has its own stream (split "estimator"), drawn
+    // from counter 0; the gradient stream's counter is preserved.
+    uint64_t saved_ctr = 0;
+    if (ctx->draw_stream == 1) {
+      CK(cudaMemcpyAsync(&saved_ctr, &ctx->dst()->ref_ctr, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      const uint64_t zero = 0;
+      CK(cudaMemcpyAsync(&ctx->dst()->ref_ctr, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
     if (n > 0) {
       if (kind == GCPB_EST_UNIFORM) {
         if (ctx->dtype == GCPB_F32)
@@ -2030,6 +2120,9 @@ int gcpb_estimator_draw(gcpb_ctx* ctx, int kind, int64_t count, double rho, uint
       CK(cudaMemcpyAsync(ctx->est_w.p, ctx->s_w.p, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     ctx->est_n = n;
+    if (ctx->draw_stream == 1) {
+      CK(cudaMemcpyAsync(&ctx->dst()->ref_ctr, &saved_ctr, 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
     ctx->sync();
   });
 }

@@ -28,6 +28,9 @@ struct DevState {
   int32_t z_overflow;
   int32_t z_incomplete;  // graph-mode steps whose zero sampler fell short
   uint64_t rng_iter;     // draw-stream iteration base for graph-replayed steps
+  uint64_t ref_ctr;      // RefStream counter (draws consumed so far)
+  uint32_t ref_flag;     // RefStream: a draw hit the rejection region
+  uint32_t ref_pad;
 };
 
 constexpr int kZcThreads = 256;
@@ -48,6 +51,10 @@ struct ZeroArgs {
   DevState* st;
   unsigned long long* status;
   uint64_t* zero_list;
+  int refstream;
+  uint64_t ref_key;
+  int64_t ref_off;  // draw index of candidate 0's first slot (= picks drawn before)
+  uint64_t thr64[kMaxModes];
 };
 
 // Batch size of one rejection round, samplers.hpp:118-122, evaluated with
@@ -110,6 +117,13 @@ __global__ void zero_plan_slice_kernel(DevState* st, int64_t begin, int64_t size
   st->z_nchunks = nchunks;
 }
 
+// RefStream: advance the counter by the draws one sampler call consumed:
+// fixed + (per_tested ? tested * d : 0)  (stratified: p + tested * d).
+__global__ void ref_advance_kernel(DevState* st, uint64_t fixed, int per_tested, int d) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  st->ref_ctr += fixed + (per_tested ? static_cast<uint64_t>(st->z_tested) * d : 0ull);
+}
+
 // Graph mode: counts steps whose device-planned batches did not yield q zeros.
 __global__ void zero_check_kernel(DevState* st) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && st->z_accepted < st->z_q) st->z_incomplete += 1;
@@ -151,6 +165,7 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const uint64_t iter = a.iter + (a.iter_base ? *a.iter_base : 0ull);
+  const uint64_t rbase = a.refstream ? st->ref_ctr : 0ull;
   for (;;) {
     if (threadIdx.x == 0) s_chunk = static_cast<long long>(atomicAdd(&st->z_ticket, 1ull));
     __syncthreads();
@@ -165,7 +180,14 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       if (c >= bend) break;
       ++nvalid;
       uint64_t lin = 0;
-      for (int g4 = 0; g4 * 4 < a.d; ++g4) {
+      if (a.refstream) {
+        for (int k = 0; k < a.d; ++k) {
+          const uint64_t j = static_cast<uint64_t>(a.ref_off + c * a.d + k);
+          lin += refstream_below(a.ref_key, rbase + j + 1, a.dims[k], a.thr64[k], &st->ref_flag) *
+                 a.stride[k];
+        }
+      }
+      for (int g4 = 0; !a.refstream && g4 * 4 < a.d; ++g4) {
         const U4 b = philox_block(a.seed, a.tag, static_cast<uint32_t>(g4), 0u, iter,
                                   static_cast<uint64_t>(c));
         for (int sl = 0; sl < 4; ++sl) {

@@ -90,6 +90,7 @@ struct SegRegs {
   uint32_t tag;
   double weight;
   int64_t t_begin, t_end, tiles_begin, out_offset;
+  int64_t ref_off;
 };
 
 template <typename T>
@@ -107,6 +108,7 @@ __device__ __forceinline__ SegRegs seg_of(const FusedArgs<T>& a, int64_t tile) {
   r.t_end = g.t_end;
   r.tiles_begin = g.tiles_begin;
   r.out_offset = g.out_offset;
+  r.ref_off = g.ref_off;
   return r;
 }
 
@@ -128,9 +130,18 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
   const int kind = sg.kind;
   if (kind == SEG_UNIFORM || kind == SEG_DRAW_ZERO || kind == SEG_ZERO_LIST) {
     const uint64_t tt = (kind == SEG_ZERO_LIST) ? a.zero_list[t] : static_cast<uint64_t>(t);
+    if (a.refstream) {  // parity mode: the reference's RngStream sequence
+      const uint64_t rbase = *a.ref_ctr;
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (EXACT || k < d)
+          ik[k] = static_cast<uint32_t>(refstream_below(
+              a.ref_key, rbase + static_cast<uint64_t>(sg.ref_off) + tt * d + k + 1, a.dims[k],
+              a.thr64[k], a.ref_flag));
+    }
 #pragma unroll
     for (int g4 = 0; g4 < (DM + 3) / 4; ++g4) {
-      if (EXACT || g4 * 4 < d) {
+      if (!a.refstream && (EXACT || g4 * 4 < d)) {
         const U4 b = philox_block(a.seed, sg.tag, static_cast<uint32_t>(g4), 0u, iter, tt);
 #pragma unroll
         for (int sl = 0; sl < 4; ++sl) {
@@ -175,7 +186,10 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
     }
   } else if (kind == SEG_PICK) {
     uint64_t e;
-    if (a.eta <= (1ull << 32)) {
+    if (a.refstream) {
+      e = refstream_below(a.ref_key, *a.ref_ctr + static_cast<uint64_t>(sg.ref_off + t) + 1, a.eta,
+                          a.thr64_eta, a.ref_flag);
+    } else if (a.eta <= (1ull << 32)) {
       const U4 b = philox_block(a.seed, sg.tag, 0u, 0u, iter, static_cast<uint64_t>(t));
       const uint64_t prod = static_cast<uint64_t>(b.x) * a.eta;
       e = (static_cast<uint32_t>(prod) >= a.thr_eta)

@@ -40,6 +40,7 @@ struct Seg {
   int64_t tiles_begin;  // first global tile of this segment
   int64_t out_offset;   // record position of ordinal t_begin
   double weight;
+  int64_t ref_off;      // RefStream: draw index of this segment's first draw
 };
 
 template <typename T>
@@ -90,6 +91,15 @@ struct FusedArgs {
   double* r_m;
   double* r_y;
   int scatter;
+  // RefStream mode: draws reproduce the reference's RngStream
+  // (rng.cpp:43-61): u = mix64(key + phi * (counter + j + 1)), value u % n,
+  // with j the draw's position in the reference's consumption order.
+  int refstream;
+  uint64_t ref_key;
+  const uint64_t* ref_ctr;    // device counter base of this call
+  uint64_t thr64[kMaxModes];  // (2^64 - n_k) mod n_k
+  uint64_t thr64_eta;
+  unsigned* ref_flag;         // set when a draw would have been rejected
   int prefetch;  // 1: prefetch the next tile's rows into L2 (opt-in)
   int stage;     // 1: factor tables exceed L2 -> cp.async-staged kernel variant
 };
@@ -221,6 +231,16 @@ __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const uint64_t* p) {
                : "=l"(v.x), "=l"(v.y)
                : "l"(p));
   return v;
+}
+
+// One RngStream draw (rng.cpp:43-61) at counter ctr, bounded by n.  The
+// reference retries on u < thr (probability thr/2^64 <= n/2^64); this path
+// reports it instead, since a retry would shift every later draw.
+__device__ __forceinline__ uint64_t refstream_below(uint64_t key, uint64_t ctr, uint64_t n,
+                                                   uint64_t thr, unsigned* flag) {
+  const uint64_t u = mix64(key + 0x9e3779b97f4a7c15ull * ctr);
+  if (u < thr) atomicOr(flag, 1u);
+  return u % n;
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {

@@ -35,6 +35,7 @@ class FitConfig:
     max_epochs: int = 100
     seed: int = 0
     keep_factors: bool = False            # start from the engine's current factors
+    draw_stream: str = "philox"           # "reference": RefStream, the reference's own draws
 
 
 @dataclass
@@ -74,6 +75,7 @@ def fit_gcp_adam(engine: Engine, loss: LossFunction, cfg: FitConfig) -> FitResul
     c.max_epochs = cfg.max_epochs
     c.seed = cfg.seed
     c.keep_factors = 1 if cfg.keep_factors else 0
+    c.draw_stream = 1 if cfg.draw_stream == "reference" else 0
     cap = cfg.max_epochs + 1
     trace = (_capi.gcpb_trace_record * cap)()
     n = C.c_int64()

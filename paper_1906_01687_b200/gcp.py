@@ -485,6 +485,18 @@ class Engine:
         return out.value
 
     # ---- snapshots / multi-GPU -------------------------------------------------------
+    def set_draw_stream(self, kind: str = "philox", counter: int = 0) -> None:
+        """'philox' (default) or 'reference' (RefStream: the reference's
+        RngStream sequence; stoch_grad's seed is then the stream key)."""
+        k = {"philox": 0, "reference": 1}[kind]
+        self._ck(lib.gcpb_set_draw_stream(self._h, k, counter))
+
+    @property
+    def draw_counter(self) -> int:
+        v = C.c_uint64()
+        self._ck(lib.gcpb_get_draw_counter(self._h, C.byref(v)))
+        return v.value
+
     def kernel_timing(self, enable: bool) -> None:
         self._ck(lib.gcpb_kernel_timing(self._h, 1 if enable else 0))
 
