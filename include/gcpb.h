@@ -229,6 +229,23 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter);
 /* Wait for queued device work and report deferred device-side failures. */
 int gcpb_synchronize(gcpb_ctx* ctx);
 
+/* ---- exact gradients and sampler diagnostics (oracle-scale, on the device) -------
+ * gradient_full (src/kernels.cpp:170-198): loss derivative at every entry
+ * (N <= 1e8, the reference's cap) -> the context's gradient. */
+int gcpb_gradient_full(gcpb_ctx* ctx, const gcpb_loss* loss);
+/* gradient_poisson_implicit (src/kernels.cpp:200-235): exact Poisson gradient
+ * from factor column sums plus a pass over the stored nonzeros only. */
+int gcpb_gradient_poisson_implicit(gcpb_ctx* ctx, const gcpb_loss* loss);
+/* empirical_bias_variance (src/samplers.cpp:134-168): `trials` stochastic
+ * gradients (trial t = iteration t of the Philox stream keyed by seed; in
+ * RefStream mode the stream RngStream-split(t) of the key `seed`, like the
+ * reference's rng.split(t)); bias = ||mean - exact||_2, variance = mean
+ * squared distance to the mean.  exact: flattened gradient (GradientSet
+ * order) or NULL to use gcpb_gradient_full. */
+int gcpb_bias_variance(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                       int64_t trials, uint64_t seed, const double* exact, double* bias,
+                       double* variance);
+
 /* ---- fit driver -------------------------------------------------------------------
  * fit_gcp_adam (src/optimizer.cpp:68-158) with the epoch loop on the device:
  * factors start as the reference's init (RngStream(seed).split("init") uniform

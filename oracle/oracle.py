@@ -328,6 +328,11 @@ class Reference:
                                              f64p, C.c_int, f64p]
         L.ref_gradient_full.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, C.c_int, C.c_double,
                                         f64p]
+        L.ref_gradient_poisson_implicit.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, f64p]
+        L.ref_empirical_bias_variance.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, C.c_int,
+                                                  C.c_double, C.c_int, C.c_int64, C.c_int64,
+                                                  C.c_int64, C.c_double, C.c_int64, C.c_uint64,
+                                                  f64p, f64p]
         L.ref_adam_step.argtypes = [C.c_int, i64p, C.c_int64, f64p, f64p, f64p, i64p, C.c_double,
                                     f64p, C.c_double, C.c_double, C.c_double, C.c_int, C.c_double]
         L.ref_estimator_scripted.argtypes = [vp, C.c_int, C.c_int64, C.c_double, u64p, C.c_int64,
@@ -536,6 +541,19 @@ class RefTensor:
             C.byref(n), C.byref(est)))
         k = n.value
         return idx[:k], x[:k], w[:k], est.value
+
+    def gradient_poisson_implicit(self, r, factors):
+        out = np.zeros(int(np.sum(self.dims)) * r)
+        self.ref._ck(self.ref.lib.ref_gradient_poisson_implicit(
+            self.h, len(self.dims), _i64(self.dims), r, _f64(Oracle.flat(factors)), _f64(out)))
+        return out
+
+    def bias_variance(self, r, factors, loss_kind, delta, strategy, s, p, q, rho, trials, seed):
+        b, v = C.c_double(), C.c_double()
+        self.ref._ck(self.ref.lib.ref_empirical_bias_variance(
+            self.h, len(self.dims), _i64(self.dims), r, _f64(Oracle.flat(factors)), loss_kind,
+            delta, strategy, s, p, q, rho, trials, seed, C.byref(b), C.byref(v)))
+        return b.value, v.value
 
     def gradient_full(self, r, factors, loss_kind, delta):
         out = np.zeros(int(np.sum(self.dims)) * r)

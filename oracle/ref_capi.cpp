@@ -332,6 +332,36 @@ int ref_gradient_full(void* tensor, int d, const std::int64_t* dims, std::int64_
   });
 }
 
+int ref_gradient_poisson_implicit(void* tensor, int d, const std::int64_t* dims, std::int64_t r,
+                                  const double* factors, double* grad_out) {
+  return guard([&] {
+    const TensorH* t = static_cast<TensorH*>(tensor);
+    const gcp::KruskalModel model = make_model(d, dims, r, factors);
+    const gcp::GradientSet g =
+        gcp::gradient_poisson_implicit(*t->sparse, model, gcp::LossFunction::poisson());
+    flatten_mats(g.modes, grad_out);
+  });
+}
+
+// empirical_bias_variance(kind, x, model, loss, trials, RngStream(seed))
+// (samplers.cpp:157-168).
+int ref_empirical_bias_variance(void* tensor, int d, const std::int64_t* dims, std::int64_t r,
+                                const double* factors, int loss_kind, double delta, int strategy,
+                                std::int64_t s, std::int64_t p, std::int64_t q, double rho,
+                                std::int64_t trials, std::uint64_t seed, double* bias,
+                                double* variance) {
+  return guard([&] {
+    const TensorH* t = static_cast<TensorH*>(tensor);
+    const gcp::KruskalModel model = make_model(d, dims, r, factors);
+    gcp::RngStream rng(seed);
+    const gcp::BiasVariance bv = gcp::empirical_bias_variance(
+        make_kind(strategy, s, p, q, rho), t->view(), model, make_loss(loss_kind, delta), trials,
+        rng);
+    *bias = bv.bias;
+    *variance = bv.variance;
+  });
+}
+
 // ---- adam_step (optimizer.cpp:47-66) -----------------------------------------------
 int ref_adam_step(int d, const std::int64_t* dims, std::int64_t r, double* factors, double* first,
                   double* second, std::int64_t* iterations, double learning_rate,

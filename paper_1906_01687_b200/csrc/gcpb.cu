@@ -1207,6 +1207,132 @@ double model_norm_host(const std::vector<std::vector<double>>& F, int64_t r) {
   return std::sqrt(std::max(0.0, ss));
 }
 
+// ---- exact gradients and bias/variance ------------------------------------------
+template <typename T>
+void gradient_full_impl(gcpb_ctx* c, const gcpb_loss* loss) {
+  if (c->tensor_kind == 0) throw std::invalid_argument("no tensor set");
+  if (!c->total_fits || c->total > 100000000ull)  // kernels.cpp:176-179
+    throw std::invalid_argument("gradient: tensor too large for the full-entry walk: " +
+                                u128_to_string(c->total128) + " entries");
+  check_data_domain(c, loss->kind);
+  if (c->tensor_kind == 2) ensure_hash(c);
+  FusedArgs<T> a = base_args<T>(c, loss, 0, 0);
+  a.refstream = 0;
+  if (c->tensor_kind == 2) {
+    a.hkeys = c->hkeys.as<uint64_t>();
+    a.hvals = c->hvals.as<uint32_t>();
+    a.hmask = c->hmask;
+  }
+  a.nseg = 1;
+  a.seg[0] = make_seg(SEG_FULL, 0, 0, static_cast<int64_t>(c->total), 1.0, 0, 0);
+  CK(cudaMemsetAsync(c->Gr.p, 0, c->nelem * c->tsize, c->stream));
+  run_fused(c, a, false);
+  c->grad_zero = false;
+}
+
+template <typename T>
+void poisson_implicit_impl(gcpb_ctx* c, const gcpb_loss* loss) {
+  if (loss->kind != GCPB_LOSS_POISSON)
+    throw std::invalid_argument(std::string("implicit gradient requires the poisson loss, got ") +
+                                loss_name(loss->kind));  // kernels.cpp:202-205
+  if (c->tensor_kind != 2) throw std::invalid_argument("implicit gradient requires a sparse tensor");
+  check_data_domain(c, loss->kind);
+  const int d = c->d, r = static_cast<int>(c->r);
+  // sparse part first (it overwrites G when gradient replicas are in use)
+  FusedArgs<T> a = base_args<T>(c, loss, 0, 0);
+  a.refstream = 0;
+  a.nseg = 1;
+  a.seg[0] = make_seg(SEG_NZ_ALL, 0, 0, c->nnz, 1.0, 2, 0);
+  CK(cudaMemsetAsync(c->Gr.p, 0, c->nelem * c->tsize, c->stream));
+  if (c->nnz > 0) run_fused(c, a, false);
+  // all-ones part: rows += prod of the other factors' column sums (LeaveOneOut order)
+  DBuf cs, offd, rowc;
+  cs.alloc(static_cast<size_t>(d) * r * sizeof(double));
+  offd.alloc(kMaxModes * sizeof(int64_t));
+  CK(cudaMemcpyAsync(offd.p, c->off, kMaxModes * sizeof(int64_t), cudaMemcpyHostToDevice,
+                     c->stream));
+  colsum_kernel<T><<<d * r, 256, 0, c->stream>>>(c->A.as<T>(), offd.as<int64_t>(),
+                                                 c->dims_dev.as<int64_t>(),
+                                                 static_cast<int>(c->rp), r, cs.as<double>());
+  std::vector<double> h(static_cast<size_t>(d) * r);
+  CK(cudaMemcpyAsync(h.data(), cs.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  std::vector<double> pre(static_cast<size_t>(d) * r), suf(static_cast<size_t>(d) * r),
+      out(static_cast<size_t>(d) * r);
+  for (int j = 0; j < r; ++j) pre[j] = 1.0;
+  for (int k = 1; k < d; ++k)
+    for (int j = 0; j < r; ++j) pre[k * r + j] = pre[(k - 1) * r + j] * h[(k - 1) * r + j];
+  for (int j = 0; j < r; ++j) suf[(d - 1) * r + j] = 1.0;
+  for (int k = d - 2; k >= 0; --k)
+    for (int j = 0; j < r; ++j) suf[k * r + j] = suf[(k + 1) * r + j] * h[(k + 1) * r + j];
+  for (size_t i = 0; i < out.size(); ++i) out[i] = pre[i] * suf[i];
+  rowc.alloc(out.size() * 8);
+  CK(cudaMemcpyAsync(rowc.p, out.data(), out.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  add_rowconst_kernel<T><<<grid_for(c->nelem, 256, c->num_sms), 256, 0, c->stream>>>(
+      c->Gr.as<T>(), rowc.as<double>(), c->nelem, static_cast<int>(c->rp), r, offd.as<int64_t>(),
+      d);
+  CK(cudaGetLastError());
+  c->sync();
+  c->grad_zero = false;
+}
+
+template <typename T>
+void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss,
+                        int64_t trials, uint64_t seed, const double* exact, double* bias,
+                        double* variance) {
+  if (trials < 2) throw std::invalid_argument("empirical_bias_variance: need >= 2 trials");
+  const int64_t n = c->nelem;
+  DBuf E, mean, m2, parts;
+  E.alloc(n * 8);
+  mean.alloc(n * 8);
+  m2.alloc(n * 8);
+  if (exact) {  // unpadded GradientSet order -> padded layout
+    std::vector<double> h(static_cast<size_t>(n), 0.0);
+    const double* src = exact;
+    for (int k = 0; k < c->d; ++k)
+      for (int64_t i = 0; i < c->dims[k]; ++i)
+        for (int64_t j = 0; j < c->r; ++j) h[c->off[k] + i * c->rp + j] = *src++;
+    CK(cudaMemcpyAsync(E.p, h.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    c->sync();
+  } else {
+    gradient_full_impl<T>(c, loss);
+    to_double_kernel<T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(c->Gr.as<T>(),
+                                                                              E.as<double>(), n);
+  }
+  CK(cudaMemsetAsync(mean.p, 0, n * 8, c->stream));
+  CK(cudaMemsetAsync(m2.p, 0, n * 8, c->stream));
+  const HostRngStream parent = HostRngStream::from_key(seed);
+  for (int64_t t = 0; t < trials; ++t) {
+    uint64_t key = seed, it = static_cast<uint64_t>(t);
+    if (c->draw_stream == 1) {  // samplers.cpp:140-141: trial stream = rng.split(t), from counter 0
+      key = parent.split(static_cast<uint64_t>(t)).key();
+      const uint64_t zero = 0;
+      CK(cudaMemcpyAsync(&c->dst()->ref_ctr, &zero, 8, cudaMemcpyHostToDevice, c->stream));
+      it = 0;
+    }
+    ensure_grad_zero(c);
+    stoch_grad_impl<T>(c, sk, loss, key, it, true, false, true, false, -1);
+    c->grad_zero = false;
+    welford_kernel<T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
+        c->Gr.as<T>(), mean.as<double>(), m2.as<double>(), n, static_cast<double>(t + 1));
+    CK(cudaGetLastError());
+  }
+  constexpr int kGrid = 296;
+  parts.alloc(2 * kGrid * 8);
+  sqdiff_sum_kernel<<<kGrid, 256, 0, c->stream>>>(mean.as<double>(), E.as<double>(),
+                                                  m2.as<double>(), n, parts.as<double>());
+  std::vector<double> hp(2 * kGrid);
+  CK(cudaMemcpyAsync(hp.data(), parts.p, hp.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  double sb = 0.0, sv = 0.0;
+  for (int b = 0; b < kGrid; ++b) {
+    sb += hp[2 * b];
+    sv += hp[2 * b + 1];
+  }
+  *bias = std::sqrt(sb);
+  *variance = sv / static_cast<double>(trials);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1884,6 +2010,39 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
 
 int gcpb_synchronize(gcpb_ctx* ctx) {
   return guard(ctx, [&] { sync_and_check(ctx); });
+}
+
+int gcpb_gradient_full(gcpb_ctx* ctx, const gcpb_loss* loss) {
+  return guard(ctx, [&] {
+    validate_loss(loss);
+    if (ctx->dtype == GCPB_F32)
+      gradient_full_impl<float>(ctx, loss);
+    else
+      gradient_full_impl<double>(ctx, loss);
+    ctx->sync();
+  });
+}
+
+int gcpb_gradient_poisson_implicit(gcpb_ctx* ctx, const gcpb_loss* loss) {
+  return guard(ctx, [&] {
+    validate_loss(loss);
+    if (ctx->dtype == GCPB_F32)
+      poisson_implicit_impl<float>(ctx, loss);
+    else
+      poisson_implicit_impl<double>(ctx, loss);
+  });
+}
+
+int gcpb_bias_variance(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                       int64_t trials, uint64_t seed, const double* exact, double* bias,
+                       double* variance) {
+  return guard(ctx, [&] {
+    check_step_args(ctx, sampler, loss);
+    if (ctx->dtype == GCPB_F32)
+      bias_variance_impl<float>(ctx, sampler, loss, trials, seed, exact, bias, variance);
+    else
+      bias_variance_impl<double>(ctx, sampler, loss, trials, seed, exact, bias, variance);
+  });
 }
 
 int gcpb_fit_gcp_adam(gcpb_ctx* ctx, const gcpb_loss* loss, const gcpb_fit_config* cfg,

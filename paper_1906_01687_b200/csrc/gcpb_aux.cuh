@@ -117,6 +117,86 @@ __global__ void zero_plan_slice_kernel(DevState* st, int64_t begin, int64_t size
   st->z_nchunks = nchunks;
 }
 
+// Column sums of every factor in fp64 (gradient_poisson_implicit's all-ones
+// part, kernels.cpp:213-216): one block per (mode, column).
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ A, const int64_t* off, const int64_t* dims,
+                              int rp, int r, double* out) {
+  const int k = blockIdx.x / r, j = blockIdx.x % r;
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < dims[k]; i += blockDim.x) acc += A[off[k] + i * rp + j];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[k * r + j] = s[0];
+}
+
+// G_k(i, :) += c_k(:) for every row i of every mode (rowwise() +=).
+template <typename T>
+__global__ void add_rowconst_kernel(T* __restrict__ G, const double* __restrict__ c,
+                                    int64_t n, int rp, int r, const int64_t* off, int d) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int col = static_cast<int>(e % rp);
+    if (col >= r) continue;
+    int k = 0;
+    while (k + 1 < d && e >= off[k + 1]) ++k;
+    G[e] += static_cast<T>(c[k * r + col]);
+  }
+}
+
+// Element-wise Welford over trials: mean, M2 (fp64), trial count n (1-based).
+template <typename T>
+__global__ void welford_kernel(const T* __restrict__ g, double* mean, double* m2, int64_t n_elem,
+                               double n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n_elem;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = static_cast<double>(g[e]);
+    const double d1 = x - mean[e];
+    const double mu = mean[e] + d1 / n;
+    m2[e] += d1 * (x - mu);
+    mean[e] = mu;
+  }
+}
+
+// Per-block partial sums of (a - b)^2 and of v (fixed grid).
+__global__ void sqdiff_sum_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                  const double* __restrict__ v, int64_t n, double* partials) {
+  __shared__ double s1[256], s2[256];
+  double x1 = 0.0, x2 = 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double dd = a[e] - b[e];
+    x1 += dd * dd;
+    x2 += v[e];
+  }
+  s1[threadIdx.x] = x1;
+  s2[threadIdx.x] = x2;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = s1[0];
+    partials[2 * blockIdx.x + 1] = s2[0];
+  }
+}
+
+template <typename T>
+__global__ void to_double_kernel(const T* __restrict__ in, double* out, int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[e] = static_cast<double>(in[e]);
+}
+
 // RefStream: advance the counter by the draws one sampler call consumed:
 // fixed + (per_tested ? tested * d : 0)  (stratified: p + tested * d).
 __global__ void ref_advance_kernel(DevState* st, uint64_t fixed, int per_tested, int d) {

@@ -227,6 +227,47 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
         s.x = static_cast<T>(__hiloint2double(static_cast<int>(wds[1]), static_cast<int>(wds[0])));
       }
     }
+  } else if (GV && (kind == SEG_FULL || kind == SEG_NZ_ALL)) {
+    // Exact-gradient walks: every entry (t = first-mode-fastest linear index)
+    // or every stored nonzero (t = ordinal); weight 1.
+    if (kind == SEG_FULL) {
+      uint64_t rem = static_cast<uint64_t>(t);
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (EXACT || k < d) {
+          ik[k] = static_cast<uint32_t>(rem % a.dims[k]);
+          rem /= a.dims[k];
+        }
+      const uint64_t lin = static_cast<uint64_t>(t);
+      switch (a.xkind) {
+        case X_DENSE_BIT:
+          s.x = static_cast<T>((static_cast<const uint32_t*>(a.dense)[lin >> 5] >> (lin & 31u)) & 1u);
+          break;
+        case X_DENSE_U8:
+          s.x = static_cast<T>(static_cast<const uint8_t*>(a.dense)[lin]);
+          break;
+        case X_DENSE_F32:
+          s.x = static_cast<T>(static_cast<const float*>(a.dense)[lin]);
+          break;
+        case X_DENSE_F64:
+          s.x = static_cast<T>(static_cast<const double*>(a.dense)[lin]);
+          break;
+        case X_SPARSE: {
+          const int64_t slot = hash_find(a.hkeys, a.hmask, lin);
+          s.x = slot < 0 ? static_cast<T>(0) : a.vals[a.hvals[slot]];
+          break;
+        }
+        default:
+          break;
+      }
+    } else {
+      constexpr int VWD = sizeof(T) / 4;
+      const uint32_t* rp = a.nzrec + t * a.rec_words;
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (EXACT || k < d) ik[k] = rp[VWD + k];
+      s.x = a.vals[t];
+    }
   } else if (GV) {  // SEG_GIVEN
 #pragma unroll
     for (int k = 0; k < DM; ++k)
@@ -347,6 +388,8 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
     T y;
     if (ygiven) {
       y = static_cast<T>(yg);
+    } else if (GV && fv == 2) {  // poisson implicit sparse part: -x / (m + eps) (kernels.cpp:226)
+      y = -wv * (xv / (m + static_cast<T>(1e-10)));
     } else {
       T g = loss_deriv_fast(a.loss, a.delta, xv, m);
       if (fv) g = g - loss_deriv_fast(a.loss, a.delta, static_cast<T>(0), m);
@@ -447,8 +490,8 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
     G = 32;
     vpl = pow2ceil((nchunks + 31) / 32);
   }
-  bool given = false;
-  for (int s = 0; s < a.nseg; ++s) given = given || a.seg[s].kind == SEG_GIVEN;
+  bool given = false;  // any segment beyond the samplers needs the general kernel
+  for (int s = 0; s < a.nseg; ++s) given = given || a.seg[s].kind >= SEG_GIVEN;
   auto go = [&](auto kern) -> cudaError_t {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
@@ -693,7 +736,9 @@ template <typename T>
 cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
                          cudaStream_t stream, int num_sms) {
   if (total_tiles <= 0) return cudaSuccess;
-  if (!record && a.stage && a.g_y == nullptr && (a.d == 3 || a.d == 4)) {
+  bool special = false;
+  for (int s = 0; s < a.nseg; ++s) special = special || a.seg[s].kind >= SEG_GIVEN;
+  if (!record && a.stage && !special && (a.d == 3 || a.d == 4)) {
     cudaError_t err = cudaSuccess;
     const bool done = a.d == 3 ? launch_staged<T, 3>(a, total_tiles, stream, num_sms, &err)
                                : launch_staged<T, 4>(a, total_tiles, stream, num_sms, &err);

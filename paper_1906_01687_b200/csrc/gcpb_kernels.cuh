@@ -28,6 +28,8 @@ enum SegKind : int {
   SEG_DRAW_ZERO = 2,  // semi-stratified unrestricted draws, x = 0 (samplers.hpp:211-216)
   SEG_ZERO_LIST = 3,  // stratified accepted zero candidates (samplers.hpp:169-172)
   SEG_GIVEN = 4,      // host-given samples (parity entry points)
+  SEG_FULL = 5,       // every entry, t = linear index (gradient_full, kernels.cpp:170-198)
+  SEG_NZ_ALL = 6,     // every stored nonzero, t = ordinal (gradient_poisson_implicit)
 };
 
 struct Seg {

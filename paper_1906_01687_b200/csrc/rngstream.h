@@ -21,6 +21,10 @@ class HostRngStream {
     }
     return HostRngStream(mix(key_ ^ mix(h + kGolden)), 0);
   }
+  HostRngStream split(uint64_t label) const {  // rng.cpp:35-37
+    return HostRngStream(mix(key_ ^ mix(label + kGolden)), 0);
+  }
+  static HostRngStream from_key(uint64_t key) { return HostRngStream(key, 0); }
   uint64_t next_u64() { return mix(key_ + kGolden * ++counter_); }
   double next_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
   uint64_t key() const { return key_; }

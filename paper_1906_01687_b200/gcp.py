@@ -485,6 +485,27 @@ class Engine:
         return out.value
 
     # ---- snapshots / multi-GPU -------------------------------------------------------
+    def gradient_full(self, loss: LossFunction) -> None:
+        """Exact gradient over every entry (kernels.cpp:170-198) -> grad()."""
+        ls = loss.c()
+        self._ck(lib.gcpb_gradient_full(self._h, C.byref(ls)))
+
+    def gradient_poisson_implicit(self, loss: LossFunction) -> None:
+        """Exact Poisson gradient touching only nonzeros (kernels.cpp:200-235)."""
+        ls = loss.c()
+        self._ck(lib.gcpb_gradient_poisson_implicit(self._h, C.byref(ls)))
+
+    def bias_variance(self, sampler: SamplerKind, loss: LossFunction, trials: int, seed: int,
+                      exact: Optional[np.ndarray] = None) -> tuple[float, float]:
+        """empirical_bias_variance (samplers.cpp:134-168) on the device."""
+        sk, ls = sampler.c(), loss.c()
+        b, v = C.c_double(), C.c_double()
+        ex = None if exact is None else np.ascontiguousarray(exact, dtype=np.float64)
+        self._ck(lib.gcpb_bias_variance(self._h, C.byref(sk), C.byref(ls), trials, seed,
+                                        _f64(ex) if ex is not None else None, C.byref(b),
+                                        C.byref(v)))
+        return b.value, v.value
+
     def set_draw_stream(self, kind: str = "philox", counter: int = 0) -> None:
         """'philox' (default) or 'reference' (RefStream: the reference's
         RngStream sequence; stoch_grad's seed is then the stream key)."""
