@@ -318,6 +318,39 @@ typedef int (*gcpb_allreduce_f64_fn)(void* user, double* buf, int64_t n);
 int gcpb_comm_init_host(gcpb_ctx* ctx, int rank, int nranks, gcpb_allgather_i64_fn allgather,
                         gcpb_allreduce_f64_fn allreduce, void* user);
 
+/* ---- tensor files (host; src/io.cpp) ------------------------------------------------
+ * A coordinate list as read from / written to disk: d modes, dims[d], nnz
+ * entries, coords nnz x d row-major 0-based, values[nnz].  Buffers filled by a
+ * reader are owned by the struct: release with gcpb_coo_free.  Errors are
+ * runtime errors "path[:line]: message" (status 1), like the reference's. */
+typedef struct gcpb_coo {
+  int d;
+  int64_t dims[16];
+  int64_t nnz;
+  int64_t* coords;
+  double* values;
+} gcpb_coo;
+/* read_tns (src/io.cpp:75-139): '#shape: n1 .. nd' header (optional; else
+ * dims = per-mode index maxima), '#' comment lines, one entry per line as d
+ * 1-based indices and a value.  Entries are returned in file order (not
+ * normalised: gcpb_set_sparse sums duplicates and drops zeros, as the
+ * reference's SparseTensor constructor does).  threads <= 0: all cores. */
+int gcpb_tns_read(const char* path, int threads, gcpb_coo* out);
+/* write_tns (src/io.cpp:141-151): header + 1-based entries, values %.17g. */
+int gcpb_tns_write(const char* path, const gcpb_coo* coo);
+/* Binary coordinate format "GCPBCOO1" (own): 40-byte header {magic[8],
+ * u32 version=1, u32 d, i64 nnz, u32 index_bytes (4|8), u32 flags, u64 0},
+ * i64 dims[d], coords nnz x d (index_bytes each, little-endian), f64 values. */
+int gcpb_coo_write(const char* path, const gcpb_coo* coo);
+int gcpb_coo_read(const char* path, int threads, gcpb_coo* out);
+void gcpb_coo_free(gcpb_coo* coo);
+/* read_dense / write_dense (src/io.cpp:195-250): raw little-endian f64 in
+ * first-mode-fastest order, shape in the text sidecar path + ".shape".
+ * gcpb_dense_shape fills d/dims; gcpb_dense_read fills values[prod(dims)]. */
+int gcpb_dense_shape(const char* path, int* d, int64_t* dims);
+int gcpb_dense_read(const char* path, int64_t n, double* values);
+int gcpb_dense_write(const char* path, int d, const int64_t* dims, const double* values);
+
 /* ---- host-only helpers (no device needed) ----------------------------------------- */
 /* Product Philox stream: bounded draw in [0, n). */
 uint64_t gcpb_philox_bounded(uint64_t seed, uint32_t tag, uint64_t iter, uint64_t t, int slot,

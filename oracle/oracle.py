@@ -328,6 +328,11 @@ class Reference:
                                              f64p, C.c_int, f64p]
         L.ref_gradient_full.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, C.c_int, C.c_double,
                                         f64p]
+        L.ref_read_tns.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
+        L.ref_write_tns.argtypes = [vp, C.c_char_p]
+        L.ref_read_dense.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
+        L.ref_write_dense.argtypes = [vp, C.c_char_p]
+        L.ref_dense_export.argtypes = [vp, f64p]
         L.ref_gradient_poisson_implicit.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, f64p]
         L.ref_empirical_bias_variance.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, C.c_int,
                                                   C.c_double, C.c_int, C.c_int64, C.c_int64,
@@ -375,6 +380,16 @@ class Reference:
         h = C.c_void_p()
         self._ck(self.lib.ref_dense_new(len(dims), _i64(dims), _f64(values), C.byref(h)))
         return RefTensor(self, h, dims)
+
+    def read_tns(self, path):
+        h, d, dims = C.c_void_p(), C.c_int(), np.zeros(16, dtype=np.int64)
+        self._ck(self.lib.ref_read_tns(str(path).encode(), C.byref(h), C.byref(d), _i64(dims)))
+        return RefTensor(self, h, dims[:d.value].copy())
+
+    def read_dense(self, path):
+        h, d, dims = C.c_void_p(), C.c_int(), np.zeros(16, dtype=np.int64)
+        self._ck(self.lib.ref_read_dense(str(path).encode(), C.byref(h), C.byref(d), _i64(dims)))
+        return RefTensor(self, h, dims[:d.value].copy())
 
     # -- rng
     def rng(self, seed):
@@ -496,6 +511,17 @@ class RefTensor:
 
     def norm(self):
         return float(self.ref.lib.ref_tensor_norm(self.h))
+
+    def write_tns(self, path):
+        self.ref._ck(self.ref.lib.ref_write_tns(self.h, str(path).encode()))
+
+    def write_dense(self, path):
+        self.ref._ck(self.ref.lib.ref_write_dense(self.h, str(path).encode()))
+
+    def dense_values(self):
+        out = np.zeros(int(np.prod(self.dims)))
+        self.ref._ck(self.ref.lib.ref_dense_export(self.h, _f64(out)))
+        return out
 
     def draw_scripted(self, r, factors, loss_kind, delta, strategy, s, p, q, rho, script,
                       cap=None):

@@ -13,11 +13,13 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <iostream>  // static libstdc++ in the .so: pull in the stream/locale init
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "gcp/io.hpp"
 #include "gcp/kernels.hpp"
 #include "gcp/kruskal.hpp"
 #include "gcp/loss.hpp"
@@ -235,6 +237,42 @@ int ref_tensor_value_at(void* h, const std::int64_t* idx, double* out) {
   });
 }
 double ref_tensor_norm(void* h) { return static_cast<TensorH*>(h)->view().norm(); }
+
+// ---- tensor files (io.cpp) ------------------------------------------------------------
+namespace {
+void shape_out(const gcp::Shape& s, int* d, std::int64_t* dims) {
+  *d = s.ndims();
+  for (int k = 0; k < s.ndims(); ++k) dims[k] = s.dim(k);
+}
+}  // namespace
+int ref_read_tns(const char* path, void** out, int* d, std::int64_t* dims) {
+  return guard([&] {
+    auto h = std::make_unique<TensorH>();
+    h->sparse = std::make_unique<gcp::SparseTensor>(gcp::read_tns(path));
+    shape_out(h->sparse->shape(), d, dims);
+    *out = h.release();
+  });
+}
+int ref_write_tns(void* h, const char* path) {
+  return guard([&] { gcp::write_tns(*static_cast<TensorH*>(h)->sparse, path); });
+}
+int ref_read_dense(const char* path, void** out, int* d, std::int64_t* dims) {
+  return guard([&] {
+    auto h = std::make_unique<TensorH>();
+    h->dense = std::make_unique<gcp::DenseTensor>(gcp::read_dense(path));
+    shape_out(h->dense->shape(), d, dims);
+    *out = h.release();
+  });
+}
+int ref_write_dense(void* h, const char* path) {
+  return guard([&] { gcp::write_dense(*static_cast<TensorH*>(h)->dense, path); });
+}
+int ref_dense_export(void* h, double* out) {
+  return guard([&] {
+    const auto v = static_cast<TensorH*>(h)->dense->values();
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+  });
+}
 
 // ---- model evaluation -------------------------------------------------------------
 int ref_model_entry(int d, const std::int64_t* dims, std::int64_t r, const double* factors,

@@ -61,6 +61,11 @@ class gcpb_trace_record(C.Structure):
                 ("learning_rate", C.c_double), ("seconds", C.c_double), ("accepted", C.c_int32)]
 
 
+class gcpb_coo(C.Structure):
+    _fields_ = [("d", C.c_int32), ("dims", C.c_int64 * 16), ("nnz", C.c_int64),
+                ("coords", C.POINTER(C.c_int64)), ("values", C.POINTER(C.c_double))]
+
+
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64))
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
 
@@ -133,6 +138,14 @@ SIGNATURES = [
     ("gcpb_allreduce_grad", C.c_int, [ctx_p]),
     ("gcpb_comm_init_host", C.c_int, [ctx_p, C.c_int, C.c_int, ALLGATHER_FN, ALLREDUCE_FN,
                                       C.c_void_p]),
+    ("gcpb_tns_read", C.c_int, [C.c_char_p, C.c_int, C.POINTER(gcpb_coo)]),
+    ("gcpb_tns_write", C.c_int, [C.c_char_p, C.POINTER(gcpb_coo)]),
+    ("gcpb_coo_write", C.c_int, [C.c_char_p, C.POINTER(gcpb_coo)]),
+    ("gcpb_coo_read", C.c_int, [C.c_char_p, C.c_int, C.POINTER(gcpb_coo)]),
+    ("gcpb_coo_free", None, [C.POINTER(gcpb_coo)]),
+    ("gcpb_dense_shape", C.c_int, [C.c_char_p, i32p, i64p]),
+    ("gcpb_dense_read", C.c_int, [C.c_char_p, C.c_int64, f64p]),
+    ("gcpb_dense_write", C.c_int, [C.c_char_p, C.c_int, i64p, f64p]),
     ("gcpb_philox_bounded", C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                          C.c_uint64]),
     ("gcpb_zero_batch_size", C.c_int64, [C.c_double, C.c_double, C.c_double, C.c_int64]),

@@ -32,12 +32,13 @@ NVFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
     "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
 ]
-SOURCES = ["gcpb.cu", "gcpb_fused_f32.cu", "gcpb_fused_f64.cu"]
+SOURCES = ["gcpb.cu", "gcpb_fused_f32.cu", "gcpb_fused_f64.cu", "gcpb_io.cpp"]
 _FUSED_DEPS = ["philox.cuh", "gcpb_kernels.cuh", "gcpb_fused.cuh"]
 DEPS = {
     "gcpb.cu": ["philox.cuh", "gcpb_kernels.cuh", "gcpb_aux.cuh"],
     "gcpb_fused_f32.cu": _FUSED_DEPS,
     "gcpb_fused_f64.cu": _FUSED_DEPS,
+    "gcpb_io.cpp": [],
 }
 
 
@@ -52,7 +53,7 @@ def _compile(src: str, force: bool) -> tuple[str, bool]:
     s = CSRC / src
     o = OBJ / (Path(src).stem + ".o")
     deps = [s] + [CSRC / h for h in DEPS.get(src, [])]
-    if src == "gcpb.cu":
+    if src in ("gcpb.cu", "gcpb_io.cpp"):
         deps.append(ROOT / "include" / "gcpb.h")
     if not force and not _stale(o, deps):
         return src, False

@@ -1335,6 +1335,11 @@ void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* lo
 
 }  // namespace
 
+namespace gcpb {
+// Shared with gcpb_io.cpp: context-free calls report through gcpb_last_error(NULL).
+void set_global_error(const std::string& msg) { g_global_err = msg; }
+}  // namespace gcpb
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
