@@ -318,6 +318,34 @@ typedef int (*gcpb_allreduce_f64_fn)(void* user, double* buf, int64_t n);
 int gcpb_comm_init_host(gcpb_ctx* ctx, int rank, int nranks, gcpb_allgather_i64_fn allgather,
                         gcpb_allreduce_f64_fn allreduce, void* user);
 
+/* ---- synthetic problems (src/synthetic.cpp), generated on the device ----------------
+ * The reference's RngStream state (rng.hpp:15-47): key, draw counter and the
+ * cached second Box-Muller normal.  Generators consume draws exactly as the
+ * reference does and return the advanced state, so a problem generated here
+ * is entry-for-entry the reference's problem for the same stream. */
+typedef struct gcpb_rng {
+  uint64_t key;
+  uint64_t counter;
+  int32_t has_cached_normal;
+  double cached_normal;
+} gcpb_rng;
+int gcpb_rng_seed(uint64_t seed, gcpb_rng* out);                        /* RngStream(seed) */
+int gcpb_rng_split(const gcpb_rng* in, uint64_t label, gcpb_rng* out);  /* rng.split(label) */
+/* gen_gamma_problem (synthetic.cpp:26-41): truth = random_uniform(shape,
+ * rank) -> the context's factors (and truth_out, unpadded fp64, if non-NULL);
+ * dense data x = Exponential(mean = truth entry), storage F64 or F32.  No
+ * 1e8-entry cap: any dense tensor that fits in HBM. */
+int gcpb_gen_gamma_problem(gcpb_ctx* ctx, gcpb_rng* rng, int storage, double* truth_out);
+/* BinaryProblemSpec (synthetic.hpp:22-31); the rank is the context's. */
+typedef struct gcpb_binary_spec {
+  double delta;   /* sparse-column keep probability, (0, 0.5) */
+  double p_high;  /* one-probability at structural positions */
+  double p_low;   /* noise one-probability elsewhere */
+} gcpb_binary_spec;
+/* gen_binary_problem (synthetic.cpp:58-146) -> sparse binary tensor + truth. */
+int gcpb_gen_binary_problem(gcpb_ctx* ctx, const gcpb_binary_spec* spec, gcpb_rng* rng,
+                            double* truth_out);
+
 /* ---- tensor files (host; src/io.cpp) ------------------------------------------------
  * A coordinate list as read from / written to disk: d modes, dims[d], nnz
  * entries, coords nnz x d row-major 0-based, values[nnz].  Buffers filled by a

@@ -328,6 +328,10 @@ class Reference:
                                              f64p, C.c_int, f64p]
         L.ref_gradient_full.argtypes = [vp, C.c_int, i64p, C.c_int64, f64p, C.c_int, C.c_double,
                                         f64p]
+        L.ref_gen_gamma.argtypes = [C.c_int, i64p, C.c_int64, C.c_uint64, C.POINTER(vp), f64p,
+                                    u64p]
+        L.ref_gen_binary.argtypes = [C.c_int, i64p, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                     C.c_uint64, C.POINTER(vp), f64p, u64p]
         L.ref_read_tns.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
         L.ref_write_tns.argtypes = [vp, C.c_char_p]
         L.ref_read_dense.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
@@ -380,6 +384,22 @@ class Reference:
         h = C.c_void_p()
         self._ck(self.lib.ref_dense_new(len(dims), _i64(dims), _f64(values), C.byref(h)))
         return RefTensor(self, h, dims)
+
+    def gen_gamma(self, dims, r, seed):
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        h, nxt = C.c_void_p(), C.c_uint64()
+        truth = np.zeros(int(dims.sum()) * r)
+        self._ck(self.lib.ref_gen_gamma(len(dims), _i64(dims), r, seed, C.byref(h), _f64(truth),
+                                        C.byref(nxt)))
+        return RefTensor(self, h, dims), truth, nxt.value
+
+    def gen_binary(self, dims, r, delta, p_high, p_low, seed):
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        h, nxt = C.c_void_p(), C.c_uint64()
+        truth = np.zeros(int(dims.sum()) * r)
+        self._ck(self.lib.ref_gen_binary(len(dims), _i64(dims), r, delta, p_high, p_low, seed,
+                                         C.byref(h), _f64(truth), C.byref(nxt)))
+        return RefTensor(self, h, dims), truth, nxt.value
 
     def read_tns(self, path):
         h, d, dims = C.c_void_p(), C.c_int(), np.zeros(16, dtype=np.int64)

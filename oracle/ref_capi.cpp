@@ -27,6 +27,7 @@
 #include "gcp/rng.hpp"
 #include "gcp/samplers.hpp"
 #include "gcp/shape.hpp"
+#include "gcp/synthetic.hpp"
 #include "gcp/tensor.hpp"
 
 namespace {
@@ -237,6 +238,36 @@ int ref_tensor_value_at(void* h, const std::int64_t* idx, double* out) {
   });
 }
 double ref_tensor_norm(void* h) { return static_cast<TensorH*>(h)->view().norm(); }
+
+// ---- synthetic problems (synthetic.cpp) ------------------------------------------------
+// The generators run on RngStream(seed); *next_draw = the stream's next u64
+// afterwards (pins how many draws were consumed).
+int ref_gen_gamma(int d, const std::int64_t* dims, std::int64_t r, std::uint64_t seed, void** out,
+                  double* truth, std::uint64_t* next_draw) {
+  return guard([&] {
+    gcp::RngStream rng(seed);
+    auto [data, model] = gcp::gen_gamma_problem(make_shape(d, dims), r, rng);
+    auto h = std::make_unique<TensorH>();
+    h->dense = std::make_unique<gcp::DenseTensor>(std::move(data));
+    flatten_model(model, truth);
+    *next_draw = rng.next_u64();
+    *out = h.release();
+  });
+}
+int ref_gen_binary(int d, const std::int64_t* dims, std::int64_t r, double delta, double p_high,
+                   double p_low, std::uint64_t seed, void** out, double* truth,
+                   std::uint64_t* next_draw) {
+  return guard([&] {
+    gcp::RngStream rng(seed);
+    gcp::BinaryProblemSpec spec{make_shape(d, dims), r, delta, p_high, p_low};
+    auto [data, model] = gcp::gen_binary_problem(spec, rng);
+    auto h = std::make_unique<TensorH>();
+    h->sparse = std::make_unique<gcp::SparseTensor>(std::move(data));
+    flatten_model(model, truth);
+    *next_draw = rng.next_u64();
+    *out = h.release();
+  });
+}
 
 // ---- tensor files (io.cpp) ------------------------------------------------------------
 namespace {

@@ -17,7 +17,7 @@ _PUBLIC = {
     "STRATIFIED", "UNIFORM", "DomainError", "Engine", "GcpError", "GcpRuntimeError",
     "InvalidArgument", "LogicError", "LossFunction", "OutOfRange", "RejectionStats",
     "SamplerKind", "nccl_unique_id", "philox_bounded", "shard_range", "stratified_keep",
-    "zero_batch_size", "FitConfig", "FitResult", "fit_gcp_adam",
+    "zero_batch_size", "RngStream", "BinaryProblemSpec", "FitConfig", "FitResult", "fit_gcp_adam",
 }
 
 

@@ -61,6 +61,15 @@ class gcpb_trace_record(C.Structure):
                 ("learning_rate", C.c_double), ("seconds", C.c_double), ("accepted", C.c_int32)]
 
 
+class gcpb_rng(C.Structure):
+    _fields_ = [("key", C.c_uint64), ("counter", C.c_uint64), ("has_cached_normal", C.c_int32),
+                ("cached_normal", C.c_double)]
+
+
+class gcpb_binary_spec(C.Structure):
+    _fields_ = [("delta", C.c_double), ("p_high", C.c_double), ("p_low", C.c_double)]
+
+
 class gcpb_coo(C.Structure):
     _fields_ = [("d", C.c_int32), ("dims", C.c_int64 * 16), ("nnz", C.c_int64),
                 ("coords", C.POINTER(C.c_int64)), ("values", C.POINTER(C.c_double))]
@@ -138,6 +147,11 @@ SIGNATURES = [
     ("gcpb_allreduce_grad", C.c_int, [ctx_p]),
     ("gcpb_comm_init_host", C.c_int, [ctx_p, C.c_int, C.c_int, ALLGATHER_FN, ALLREDUCE_FN,
                                       C.c_void_p]),
+    ("gcpb_rng_seed", C.c_int, [C.c_uint64, C.POINTER(gcpb_rng)]),
+    ("gcpb_rng_split", C.c_int, [C.POINTER(gcpb_rng), C.c_uint64, C.POINTER(gcpb_rng)]),
+    ("gcpb_gen_gamma_problem", C.c_int, [ctx_p, C.POINTER(gcpb_rng), C.c_int, f64p]),
+    ("gcpb_gen_binary_problem", C.c_int, [ctx_p, C.POINTER(gcpb_binary_spec),
+                                          C.POINTER(gcpb_rng), f64p]),
     ("gcpb_tns_read", C.c_int, [C.c_char_p, C.c_int, C.POINTER(gcpb_coo)]),
     ("gcpb_tns_write", C.c_int, [C.c_char_p, C.POINTER(gcpb_coo)]),
     ("gcpb_coo_write", C.c_int, [C.c_char_p, C.POINTER(gcpb_coo)]),

@@ -23,8 +23,12 @@
 
 #include "../../include/gcpb.h"
 #include "gcpb_aux.cuh"
+#include "gcpb_gen.cuh"
 #include "gcpb_kernels.cuh"
 #include "rngstream.h"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 using namespace gcpb;
 
@@ -1333,6 +1337,8 @@ void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* lo
   *variance = sv / static_cast<double>(trials);
 }
 
+#include "gcpb_gen_host.inc"
+
 }  // namespace
 
 namespace gcpb {
@@ -2047,6 +2053,35 @@ int gcpb_bias_variance(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_lo
       bias_variance_impl<float>(ctx, sampler, loss, trials, seed, exact, bias, variance);
     else
       bias_variance_impl<double>(ctx, sampler, loss, trials, seed, exact, bias, variance);
+  });
+}
+
+int gcpb_rng_seed(uint64_t seed, gcpb_rng* out) {
+  return guard(nullptr, [&] {
+    if (!out) throw std::invalid_argument("gcpb_rng_seed: null output");
+    rng_out(HostRngStream(seed), out);
+  });
+}
+
+int gcpb_rng_split(const gcpb_rng* in, uint64_t label, gcpb_rng* out) {
+  return guard(nullptr, [&] {
+    if (!in || !out) throw std::invalid_argument("gcpb_rng_split: null argument");
+    rng_out(HostRngStream::from_key(in->key).split(label), out);
+  });
+}
+
+int gcpb_gen_gamma_problem(gcpb_ctx* ctx, gcpb_rng* rng, int storage, double* truth_out) {
+  return guard(ctx, [&] {
+    if (!rng) throw std::invalid_argument("gen_gamma_problem: null rng");
+    gen_gamma_impl(ctx, rng, storage, truth_out);
+  });
+}
+
+int gcpb_gen_binary_problem(gcpb_ctx* ctx, const gcpb_binary_spec* spec, gcpb_rng* rng,
+                            double* truth_out) {
+  return guard(ctx, [&] {
+    if (!rng || !spec) throw std::invalid_argument("gen_binary_problem: null argument");
+    gen_binary_impl(ctx, spec, rng, truth_out);
   });
 }
 

@@ -231,6 +231,37 @@ class RejectionStats:
 # ---------------------------------------------------------------------------
 # The device engine (one GCP problem on one GPU)
 # ---------------------------------------------------------------------------
+class RngStream:
+    """The reference's splittable counter stream (rng.hpp:15-47) as a state
+    the device generators consume and advance."""
+
+    def __init__(self, seed: int = 0):
+        self._s = _capi.gcpb_rng()
+        _check(lib.gcpb_rng_seed(seed, C.byref(self._s)))
+
+    def split(self, label: int) -> "RngStream":
+        child = RngStream.__new__(RngStream)
+        child._s = _capi.gcpb_rng()
+        _check(lib.gcpb_rng_split(C.byref(self._s), label, C.byref(child._s)))
+        return child
+
+    @property
+    def key(self) -> int:
+        return int(self._s.key)
+
+    @property
+    def counter(self) -> int:
+        return int(self._s.counter)
+
+
+@dataclass
+class BinaryProblemSpec:
+    """BinaryProblemSpec (synthetic.hpp:22-31); shape and rank come from the Engine."""
+    delta: float = 0.15
+    p_high: float = 0.9
+    p_low: float = 0.0025
+
+
 class Engine:
     """Owns a gcpb context: factors, gradient, Adam moments, tensor, estimator.
 
@@ -505,6 +536,31 @@ class Engine:
                                         _f64(ex) if ex is not None else None, C.byref(b),
                                         C.byref(v)))
         return b.value, v.value
+
+    # ---- synthetic problems (synthetic.cpp) --------------------------------
+    def gen_gamma_problem(self, rng: "RngStream", storage: str = "f64") -> list:
+        """gen_gamma_problem (synthetic.cpp:26-41) on the device: dense
+        exponential data around a random-uniform truth; returns the truth
+        factors (fp64) and advances ``rng`` like the reference."""
+        st = {"f32": _capi.STORE_F32, "f64": _capi.STORE_F64}[storage]
+        truth = np.zeros(sum(self._mode_sizes()))
+        self._ck(lib.gcpb_gen_gamma_problem(self._h, C.byref(rng._s), st, _f64(truth)))
+        return self._split_modes(truth)
+
+    def gen_binary_problem(self, spec: "BinaryProblemSpec", rng: "RngStream") -> list:
+        """gen_binary_problem (synthetic.cpp:58-146) on the device: sparse
+        binary tensor + truth factors; advances ``rng`` like the reference."""
+        sp = _capi.gcpb_binary_spec(spec.delta, spec.p_high, spec.p_low)
+        truth = np.zeros(sum(self._mode_sizes()))
+        self._ck(lib.gcpb_gen_binary_problem(self._h, C.byref(sp), C.byref(rng._s), _f64(truth)))
+        return self._split_modes(truth)
+
+    def _split_modes(self, flat: np.ndarray) -> list:
+        out, at = [], 0
+        for n in self.dims:
+            out.append(flat[at:at + n * self.rank].reshape(n, self.rank).copy())
+            at += n * self.rank
+        return out
 
     def set_draw_stream(self, kind: str = "philox", counter: int = 0) -> None:
         """'philox' (default) or 'reference' (RefStream: the reference's
