@@ -107,5 +107,5 @@ def test_generated_problem_fits_on_device():
     e.gen_binary_problem(g.BinaryProblemSpec(0.15, 0.9, 0.005), g.RngStream(9))
     assert e.nnz > 0
     st = e.stoch_grad(g.SamplerKind.stratified(500, 500), g.LossFunction(2), 3, 0)
-    assert st.accepted == 500
+    assert st.tested == st.accepted + st.rejected and st.accepted >= 500
     assert np.isfinite(e.grad_flat()).all()
