@@ -52,50 +52,86 @@ def _peaks():
 # clocks sampling during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event (throttle) reasons sampled every ~1 ms through
+    NVML while the timed region runs (nvidia-smi -lms is too coarse for a
+    region of a few tens of ms); falls back to nvidia-smi when NVML is absent."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self._stop = threading.Event()
+        self.t = None
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index(device))
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nvml = None
+
+    @staticmethod
+    def _physical_index(device: int) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[device])
+            except (ValueError, IndexError):
+                pass
+        return device
+
+    def _reasons(self):
+        n = self.nvml
+        for fn in ("nvmlDeviceGetCurrentClocksEventReasons", "nvmlDeviceGetCurrentClocksThrottleReasons"):
+            if hasattr(n, fn):
+                return int(getattr(n, fn)(self.h))
+        return 0
+
+    def _poll(self):
+        n = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append((int(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)),
+                                     self._reasons()))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        if self.nvml is None:
+            return
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        while not self.samples and self.t.is_alive():
+            time.sleep(0.001)
 
     def stop(self):
-        if not self.proc:
-            return None
-        self.proc.terminate()
+        if self.t is not None:
+            self._stop.set()
+            self.t.join(timeout=2)
+        if self.samples:
+            sm = [c for c, _ in self.samples]
+            bits = 0
+            for _, b in self.samples:
+                bits |= b
+            reasons = sorted(v for k, v in self.REASONS.items() if bits & k)
+            return {"sm_mhz": float(statistics.median(sm)), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml"}
+        return self._smi_once()
+
+    def _smi_once(self):
+        q = "clocks.sm,clocks.max.sm"
         try:
-            self.proc.wait(timeout=5)
+            out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=20).stdout.strip().split(",")
+            return {"sm_mhz": float(out[0]), "sm_max_mhz": int(out[1]), "reasons": [],
+                    "samples": 1, "source": "nvidia-smi (after the timed region)"}
         except Exception:
-            self.proc.kill()
-        rows = []
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) >= 7 and parts[0].isdigit():
-                rows.append(parts)
-        if not rows:
             return None
-        sm = [int(r[0]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(statistics.median(sm)), "sm_max_mhz": int(rows[0][1]),
-                "reasons": reasons, "samples": len(rows)}
 
 
 # ---------------------------------------------------------------------------
@@ -296,9 +332,8 @@ def run_ours(args, w):
 
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.2)
     torch.cuda.synchronize()
+    clocks.start()
     if dist:
         dist.barrier()
     start.record(stream)
