@@ -5,7 +5,7 @@ with the config's shape, size, value distribution and loss.  Seeds: data
 1000 + c, init 2000 + c, Philox key = 3000 + c.
 
 C1 dense 100^3 fp64, gaussian, r=5, uniform s=300
-C2 dense 200^4 binary (u8), bernoulli-odds, r=16, uniform s in {1e5,1e6,1.6e7}
+C2 dense 200^4 binary (bit-packed; u8 via GCPB_C2_STORAGE=u8), bernoulli-odds, r=16, uniform s in {1e5,1e6,1.6e7}
 C3 sparse 1000^4, 1e7 nnz Zipf(1.1), bernoulli-odds, r=32, stratified p=q=1e6
 C4 sparse 183x24x1140x1717, 3.3e6 nnz, poisson, r=20, semi-stratified p=q=1e5
 C5 sparse 4.8e6x1.7e6x1.8e6, 1.7e9 nnz Zipf(1.05), gaussian, r=16, semi p=q=1.6e7
@@ -59,7 +59,7 @@ def get(name: str, s: Optional[int] = None) -> Workload:
     if name == "c2":
         return Workload("c2", (200, 200, 200, 200), 16, "f32", "bernoulli-odds", "uniform",
                         s=s or 16_000_000, lower_bound=0.0,
-                        description="dense 200^4 binary (u8 in HBM) from a rank-8 nonnegative "
+                        description="dense 200^4 binary (bit-packed in HBM, 200 MB) from a rank-8 nonnegative "
                                     "odds model (mean p~0.1), bernoulli-odds, r=16, uniform")
     if name == "c3":
         return Workload("c3", (1000, 1000, 1000, 1000), 32, "f32", "bernoulli-odds", "stratified",
