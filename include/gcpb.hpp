@@ -144,6 +144,83 @@ struct FitTraceRecord {
   bool accepted;
 };
 
+// RngStream (include/gcp/rng.hpp:15-47) as the state the device generators
+// consume and advance.
+class RngStream {
+ public:
+  explicit RngStream(uint64_t seed) { check(gcpb_rng_seed(seed, &s_)); }
+  RngStream split(uint64_t label) const {
+    RngStream c(0);
+    check(gcpb_rng_split(&s_, label, &c.s_));
+    return c;
+  }
+  gcpb_rng* c() { return &s_; }
+  uint64_t key() const { return s_.key; }
+  uint64_t counter() const { return s_.counter; }
+
+ private:
+  gcpb_rng s_{};
+};
+
+// BinaryProblemSpec (include/gcp/synthetic.hpp:22-31); shape and rank are the engine's.
+struct BinaryProblemSpec {
+  double delta = 0.15;
+  double p_high = 0.9;
+  double p_low = 0.0025;
+};
+
+struct BiasVariance {  // samplers.hpp BiasVariance
+  double bias = 0.0;
+  double variance = 0.0;
+};
+
+// A coordinate list read from / written to a file (io.hpp).
+struct CooTensor {
+  std::vector<int64_t> dims;
+  std::vector<int64_t> coords;  // nnz x d, 0-based
+  std::vector<double> values;
+};
+
+inline CooTensor take_coo(gcpb_coo& c) {
+  CooTensor t;
+  t.dims.assign(c.dims, c.dims + c.d);
+  t.coords.assign(c.coords, c.coords + c.nnz * c.d);
+  t.values.assign(c.values, c.values + c.nnz);
+  gcpb_coo_free(&c);
+  return t;
+}
+
+inline gcpb_coo view_coo(const CooTensor& t) {
+  gcpb_coo c{};
+  c.d = static_cast<int>(t.dims.size());
+  for (int k = 0; k < c.d && k < 16; ++k) c.dims[k] = t.dims[k];
+  c.nnz = static_cast<int64_t>(t.values.size());
+  c.coords = const_cast<int64_t*>(t.coords.data());
+  c.values = const_cast<double*>(t.values.data());
+  return c;
+}
+
+// read_tns / write_tns (io.cpp:75-151): entries in file order; Engine::set_sparse
+// normalises them like the SparseTensor constructor.
+inline CooTensor read_tns(const std::string& path, int threads = 0) {
+  gcpb_coo c{};
+  check(gcpb_tns_read(path.c_str(), threads, &c));
+  return take_coo(c);
+}
+inline void write_tns(const CooTensor& t, const std::string& path) {
+  const gcpb_coo c = view_coo(t);
+  check(gcpb_tns_write(path.c_str(), &c));
+}
+inline CooTensor read_coo(const std::string& path, int threads = 0) {
+  gcpb_coo c{};
+  check(gcpb_coo_read(path.c_str(), threads, &c));
+  return take_coo(c);
+}
+inline void write_coo(const CooTensor& t, const std::string& path) {
+  const gcpb_coo c = view_coo(t);
+  check(gcpb_coo_write(path.c_str(), &c));
+}
+
 // One stochastic-GCP problem on one GPU.
 class Engine {
  public:
@@ -201,6 +278,35 @@ class Engine {
     check(gcpb_step(ctx_, &s.c, loss.c(), seed, iter, &a), ctx_);
   }
 
+  // Exact gradients (kernels.cpp:170-235) -> gradient().
+  void gradient_full(const LossFunction& loss) { check(gcpb_gradient_full(ctx_, loss.c()), ctx_); }
+  void gradient_poisson_implicit(const LossFunction& loss) {
+    check(gcpb_gradient_poisson_implicit(ctx_, loss.c()), ctx_);
+  }
+  // empirical_bias_variance (samplers.cpp:134-168); exact empty -> gradient_full.
+  BiasVariance bias_variance(const SamplerKind& s, const LossFunction& loss, int64_t trials,
+                             uint64_t seed, const std::vector<double>& exact = {}) {
+    BiasVariance bv;
+    check(gcpb_bias_variance(ctx_, &s.c, loss.c(), trials, seed,
+                             exact.empty() ? nullptr : exact.data(), &bv.bias, &bv.variance),
+          ctx_);
+    return bv;
+  }
+  // Synthetic problems (synthetic.cpp), generated in HBM; returns the truth.
+  std::vector<double> gen_gamma_problem(RngStream& rng, int storage = GCPB_STORE_F64) {
+    std::vector<double> truth(truth_size());
+    check(gcpb_gen_gamma_problem(ctx_, rng.c(), storage, truth.data()), ctx_);
+    return truth;
+  }
+  std::vector<double> gen_binary_problem(const BinaryProblemSpec& spec, RngStream& rng) {
+    std::vector<double> truth(truth_size());
+    const gcpb_binary_spec cs{spec.delta, spec.p_high, spec.p_low};
+    check(gcpb_gen_binary_problem(ctx_, &cs, rng.c(), truth.data()), ctx_);
+    return truth;
+  }
+  void set_sparse(const CooTensor& t) { set_sparse(t.coords, t.values); }
+  int64_t nnz() const { return gcpb_nnz(ctx_); }
+
  private:
   template <typename F>
   std::vector<std::vector<double>> get(F fn) const {
@@ -210,6 +316,11 @@ class Engine {
       check(fn(ctx_, k, out[k].data()), ctx_);
     }
     return out;
+  }
+  size_t truth_size() const {
+    size_t n = 0;
+    for (int64_t d : dims_) n += static_cast<size_t>(d * rank_);
+    return n;
   }
   gcpb_ctx* ctx_ = nullptr;
   std::vector<int64_t> dims_;

@@ -75,6 +75,40 @@ int main() {
   const auto res = gcpb::fit_gcp_adam(e, gcpb::LossFunction::bernoulli_odds(), cfg);
   EXPECT(!res.trace.empty() && res.trace.front().epoch == 0);
   EXPECT(res.final_loss_estimate <= res.trace.front().loss_estimate);
+  // .tns round trip through the native reader/writer
+  gcpb::CooTensor t{dims, coords, vals};
+  gcpb::write_tns(t, "/tmp/gcpb_demo.tns");
+  const gcpb::CooTensor back = gcpb::read_tns("/tmp/gcpb_demo.tns");
+  EXPECT(back.dims == dims && back.coords == coords && back.values == vals);
+  bool io_err = false;
+  try {
+    gcpb::read_tns("/tmp/gcpb_demo_missing.tns");
+  } catch (const std::runtime_error&) {
+    io_err = true;
+  }
+  EXPECT(io_err);
+  // exact gradients: the implicit Poisson form equals the full walk
+  e.set_sparse(back);
+  e.set_factors(F);
+  e.gradient_full(gcpb::LossFunction::poisson());
+  const auto gf = e.gradient();
+  e.gradient_poisson_implicit(gcpb::LossFunction::poisson());
+  const auto gi = e.gradient();
+  double num = 0.0, den = 0.0;
+  for (int k = 0; k < 3; ++k)
+    for (size_t i = 0; i < gf[k].size(); ++i) {
+      num += (gf[k][i] - gi[k][i]) * (gf[k][i] - gi[k][i]);
+      den += gf[k][i] * gf[k][i];
+    }
+  EXPECT(std::sqrt(num / den) < 1e-12);
+  const auto bv = e.bias_variance(gcpb::SamplerKind::stratified(200, 200),
+                                  gcpb::LossFunction::bernoulli_odds(), 64, 5);
+  EXPECT(bv.variance > 0.0 && bv.bias * bv.bias < 4.0 * bv.variance / 64);
+  // device generators
+  gcpb::RngStream rng(3);
+  gcpb::Engine b({30, 20, 10}, 3, GCPB_F32);
+  const auto truth = b.gen_binary_problem(gcpb::BinaryProblemSpec{}, rng);
+  EXPECT(truth.size() == 60 * 3 && b.nnz() > 0 && rng.counter() > 0);
   std::printf("ok\n");
   return 0;
 }
