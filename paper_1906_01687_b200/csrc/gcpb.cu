@@ -29,6 +29,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 using namespace gcpb;
 
@@ -983,6 +984,37 @@ int record_words(int d, size_t tsize) {
   return w;
 }
 
+// Sorted unique keys + f64 values already on the device -> records.
+void set_sparse_normalized_device(gcpb_ctx* c, const uint64_t* d_keys, const double* d_vals,
+                                  int64_t n) {
+  c->nnz = n;
+  c->tensor_kind = 2;
+  c->tensor_version += 1;
+  c->hash_ready = false;
+  c->domain_flags = -1;
+  c->dense.reset();
+  c->rec_words = record_words(c->d, c->tsize);
+  const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+  c->keys.alloc(nn * sizeof(uint64_t));
+  c->nzrec.alloc(nn * c->rec_words * sizeof(uint32_t));
+  c->vals.alloc(nn * c->tsize);
+  if (n > 0) {
+    CK(cudaMemcpyAsync(c->keys.p, d_keys, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                       c->stream));
+    const int g = grid_for(n, 256, c->num_sms);
+    if (c->dtype == GCPB_F32)
+      keys_to_records_kernel<double, float><<<g, 256, 0, c->stream>>>(
+          c->keys.as<uint64_t>(), d_vals, n, c->d, c->dims_dev.as<int64_t>(),
+          c->nzrec.as<uint32_t>(), c->rec_words, c->vals.as<float>());
+    else
+      keys_to_records_kernel<double, double><<<g, 256, 0, c->stream>>>(
+          c->keys.as<uint64_t>(), d_vals, n, c->d, c->dims_dev.as<int64_t>(),
+          c->nzrec.as<uint32_t>(), c->rec_words, c->vals.as<double>());
+    CK(cudaGetLastError());
+  }
+  c->sync();
+}
+
 void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
                            const std::vector<double>& values) {
   const int64_t n = static_cast<int64_t>(keys.size());
@@ -1339,6 +1371,73 @@ void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* lo
 
 #include "gcpb_gen_host.inc"
 
+// SparseTensor(shape, indices, values) on the device (tensor.cpp:10-41): keys
+// + index check, stable radix sort of (key, value), left-to-right run sums,
+// zero sums dropped, then the usual records.  Same result as a host stable
+// sort; the reference's std::sort can order duplicates differently, which
+// only matters in the last bit of sums of three or more duplicates.
+void normalize_on_device(gcpb_ctx* c, int64_t nnz, const int64_t* coords, const double* values) {
+  const int d = c->d;
+  if (nnz == 0) {
+    std::vector<uint64_t> k;
+    std::vector<double> v;
+    set_sparse_normalized(c, k, v);
+    return;
+  }
+  DBuf keys_in, keys_out, vals_in, vals_out, sums, keep, stage, bad, tmp, nsel;
+  keys_in.alloc(nnz * 8);
+  keys_out.alloc(nnz * 8);
+  vals_in.alloc(nnz * 8);
+  vals_out.alloc(nnz * 8);
+  bad.alloc(8);
+  CK(cudaMemsetAsync(bad.p, 0xff, 8, c->stream));
+  CK(cudaMemcpyAsync(vals_in.p, values, nnz * 8, cudaMemcpyHostToDevice, c->stream));
+  const int64_t chunk = std::min<int64_t>(nnz, std::max<int64_t>(1, (int64_t{256} << 20) / (8 * d)));
+  stage.alloc(chunk * d * 8);
+  for (int64_t b = 0; b < nnz; b += chunk) {
+    const int64_t m = std::min(chunk, nnz - b);
+    CK(cudaMemcpyAsync(stage.p, coords + b * d, m * d * 8, cudaMemcpyHostToDevice, c->stream));
+    coords_to_keys_kernel<<<grid_for(m, 256, c->num_sms, 16), 256, 0, c->stream>>>(
+        stage.as<int64_t>(), m, d, c->dims_dev.as<int64_t>(), b, keys_in.as<uint64_t>() + b,
+        bad.as<unsigned long long>());
+    CK(cudaGetLastError());
+    c->sync();  // the staging buffer is reused
+  }
+  unsigned long long first_bad = 0;
+  CK(cudaMemcpyAsync(&first_bad, bad.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (first_bad != ~0ull) {
+    check_index_host(c, coords + static_cast<int64_t>(first_bad) * d);  // throws (tensor.cpp:21)
+    throw std::out_of_range("sparse tensor: index out of range");
+  }
+  int end_bit = 1;
+  while (end_bit < 64 && (c->total - 1) >> end_bit) ++end_bit;
+  cub_call(tmp, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
+                                           vals_in.as<double>(), vals_out.as<double>(), nnz, 0,
+                                           end_bit, c->stream);
+  });
+  sums.alloc(nnz * 8);
+  keep.alloc(nnz);
+  run_sum_kernel<<<grid_for(nnz, 256, c->num_sms, 16), 256, 0, c->stream>>>(
+      keys_out.as<uint64_t>(), vals_out.as<double>(), nnz, sums.as<double>(), keep.as<uint8_t>());
+  CK(cudaGetLastError());
+  nsel.alloc(8);
+  int64_t n_unique = 0;
+  cub_call(tmp, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, keys_out.as<uint64_t>(), keep.as<uint8_t>(),
+                                      keys_in.as<uint64_t>(), nsel.as<int64_t>(), nnz, c->stream);
+  });
+  cub_call(tmp, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, sums.as<double>(), keep.as<uint8_t>(),
+                                      vals_in.as<double>(), nsel.as<int64_t>(), nnz, c->stream);
+  });
+  CK(cudaMemcpyAsync(&n_unique, nsel.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  set_sparse_normalized_device(c, keys_in.as<uint64_t>(), vals_in.as<double>(), n_unique);
+}
+
+
 }  // namespace
 
 namespace gcpb {
@@ -1460,34 +1559,9 @@ void* gcpb_get_stream(gcpb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stre
 int gcpb_set_sparse(gcpb_ctx* ctx, int64_t nnz, const int64_t* coords, const double* values) {
   return guard(ctx, [&] {
     if (nnz < 0) throw std::invalid_argument("sparse tensor: negative nnz");
+    if (nnz > 0 && (!coords || !values)) throw std::invalid_argument("sparse tensor: null buffers");
     if (!ctx->total_fits) throw std::invalid_argument("sparse tensor: N >= 2^64 unsupported (u64 keys)");
-    const int d = ctx->d;
-    std::vector<std::pair<uint64_t, double>> entries(static_cast<size_t>(nnz));
-    for (int64_t e = 0; e < nnz; ++e) {
-      check_index_host(ctx, coords + e * d);  // tensor.cpp:21
-      uint64_t lin = 0, stride = 1;
-      for (int k = 0; k < d; ++k) {
-        lin += static_cast<uint64_t>(coords[e * d + k]) * stride;
-        stride *= static_cast<uint64_t>(ctx->dims[k]);
-      }
-      entries[e] = {lin, values[e]};
-    }
-    std::stable_sort(entries.begin(), entries.end(),
-                     [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<uint64_t> keys;
-    std::vector<double> vals;
-    keys.reserve(entries.size());
-    vals.reserve(entries.size());
-    size_t e = 0;
-    while (e < entries.size()) {  // tensor.cpp:30-40: sum duplicates, drop zeros
-      const uint64_t key = entries[e].first;
-      double sum = 0.0;
-      while (e < entries.size() && entries[e].first == key) sum += entries[e++].second;
-      if (sum == 0.0) continue;
-      keys.push_back(key);
-      vals.push_back(sum);
-    }
-    set_sparse_normalized(ctx, keys, vals);
+    normalize_on_device(ctx, nnz, coords, values);
   });
 }
 

@@ -224,3 +224,51 @@ __global__ void fill_f64_kernel(double* __restrict__ out, double v, int64_t n) {
 }
 
 }  // namespace gcpb
+
+namespace gcpb {
+
+// ---- SparseTensor normalisation on the device (tensor.cpp:10-41) ----------
+// Linear key of each entry (first-mode-fastest); the first out-of-range
+// entry in input order is reported through atomicMin so the host can raise
+// the reference's check_index message for exactly that entry.
+__global__ void coords_to_keys_kernel(const int64_t* __restrict__ coords, int64_t n, int d,
+                                      const int64_t* __restrict__ dims, int64_t base,
+                                      uint64_t* __restrict__ keys,
+                                      unsigned long long* __restrict__ first_bad) {
+  int64_t dm[kMaxModes];
+  for (int k = 0; k < d; ++k) dm[k] = dims[k];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t lin = 0, stride = 1;
+    bool bad = false;
+    for (int k = 0; k < d; ++k) {
+      const int64_t v = coords[i * d + k];
+      bad |= v < 0 || v >= dm[k];
+      lin += static_cast<uint64_t>(v) * stride;
+      stride *= static_cast<uint64_t>(dm[k]);
+    }
+    keys[i] = lin;
+    if (bad) atomicMin(first_bad, static_cast<unsigned long long>(base + i));
+  }
+}
+
+// After a stable sort by key: each run head sums its run left to right (the
+// input order, as the host path's stable sort), flags nonzero sums.
+__global__ void run_sum_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ vals,
+                               int64_t n, double* __restrict__ sums, uint8_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[i];
+    uint8_t f = 0;
+    double s = 0.0;
+    if (i == 0 || keys[i - 1] != k) {
+      s = vals[i];
+      for (int64_t j = i + 1; j < n && keys[j] == k; ++j) s = __dadd_rn(s, vals[j]);
+      f = s != 0.0 ? 1 : 0;
+    }
+    sums[i] = s;
+    keep[i] = f;
+  }
+}
+
+}  // namespace gcpb
