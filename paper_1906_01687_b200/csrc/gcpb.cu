@@ -238,6 +238,13 @@ struct gcpb_ctx {
   DBuf s_idx, s_x, s_w, s_flag, s_m, s_y, s_aux;
   DBuf dims_dev;
 
+  // factor-sized host<->device transfers: pinned staging + device staging
+  // (unpadded fp64 rows), packed/unpacked by a kernel; one copy per call
+  double* xfer_host = nullptr;
+  size_t xfer_cap = 0;
+  DBuf xfer_dev;
+  cudaEvent_t xfer_done = nullptr;
+
   ~gcpb_ctx() {
     for (auto& pr : tevents) {
       cudaEventDestroy(pr.first);
@@ -248,6 +255,11 @@ struct gcpb_ctx {
       cudaStreamSynchronize(stream);
       cudaFreeHost(pinned_params);
     }
+    if (xfer_host) {
+      cudaStreamSynchronize(stream);
+      cudaFreeHost(xfer_host);
+    }
+    if (xfer_done) cudaEventDestroy(xfer_done);
     if (comm) ncclCommDestroy(comm);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
@@ -320,34 +332,65 @@ void check_index_host(const gcpb_ctx* c, const int64_t* idx) {
 }
 
 // Host-side factor layout conversion: n_k x r double <-> padded n_k x rp T.
+// Rows of modes [k0, k1) are contiguous in both layouts: unpadded n_k x r
+// (host, GradientSet order) and padded n_k x rp (device, from off[k0]).
+void xfer_reserve(gcpb_ctx* c, size_t elems) {
+  if (!c->xfer_done) CK(cudaEventCreateWithFlags(&c->xfer_done, cudaEventDisableTiming));
+  if (elems > c->xfer_cap) {
+    if (c->xfer_host) {
+      CK(cudaEventSynchronize(c->xfer_done));
+      CK(cudaFreeHost(c->xfer_host));
+      c->xfer_host = nullptr;
+    }
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->xfer_host), elems * sizeof(double)));
+    c->xfer_cap = elems;
+  }
+  c->xfer_dev.alloc(std::max<size_t>(elems, 1) * sizeof(double));
+}
+
+void mode_rows(const gcpb_ctx* c, int mode, int* k0, int* k1, int64_t* rows) {
+  *k0 = mode < 0 ? 0 : mode;
+  *k1 = mode < 0 ? c->d : mode + 1;
+  *rows = 0;
+  for (int k = *k0; k < *k1; ++k) *rows += c->dims[k];
+}
+
 template <typename T>
 void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values) {
-  const int k0 = mode < 0 ? 0 : mode, k1 = mode < 0 ? c->d : mode + 1;
-  const double* src = values;
-  for (int k = k0; k < k1; ++k) {
-    std::vector<T> host(static_cast<size_t>(c->dims[k] * c->rp), static_cast<T>(0));
-    for (int64_t i = 0; i < c->dims[k]; ++i)
-      for (int64_t j = 0; j < c->r; ++j) host[i * c->rp + j] = static_cast<T>(src[i * c->r + j]);
-    src += c->dims[k] * c->r;
-    CK(cudaMemcpyAsync(buf.as<T>() + c->off[k], host.data(), host.size() * sizeof(T),
-                       cudaMemcpyHostToDevice, c->stream));
-    c->sync();  // host vector goes out of scope
-  }
+  int k0, k1;
+  int64_t rows;
+  mode_rows(c, mode, &k0, &k1, &rows);
+  const size_t n = static_cast<size_t>(rows * c->r);
+  xfer_reserve(c, n);
+  CK(cudaEventSynchronize(c->xfer_done));  // the previous transfer left the staging block
+  std::memcpy(c->xfer_host, values, n * sizeof(double));
+  CK(cudaMemcpyAsync(c->xfer_dev.p, c->xfer_host, n * sizeof(double), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaEventRecord(c->xfer_done, c->stream));
+  const int64_t total = rows * c->rp;
+  unpack_rows_kernel<T><<<grid_for(total, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+      c->xfer_dev.as<double>(), buf.as<T>() + c->off[k0], total, static_cast<int>(c->r),
+      static_cast<int>(c->rp));
+  CK(cudaGetLastError());
 }
 
 template <typename T>
 void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out) {
-  const int k0 = mode < 0 ? 0 : mode, k1 = mode < 0 ? c->d : mode + 1;
-  double* dst = out;
-  for (int k = k0; k < k1; ++k) {
-    std::vector<T> host(static_cast<size_t>(c->dims[k] * c->rp));
-    CK(cudaMemcpyAsync(host.data(), buf.as<T>() + c->off[k], host.size() * sizeof(T),
-                       cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    for (int64_t i = 0; i < c->dims[k]; ++i)
-      for (int64_t j = 0; j < c->r; ++j) dst[i * c->r + j] = static_cast<double>(host[i * c->rp + j]);
-    dst += c->dims[k] * c->r;
-  }
+  int k0, k1;
+  int64_t rows;
+  mode_rows(c, mode, &k0, &k1, &rows);
+  const size_t n = static_cast<size_t>(rows * c->r);
+  xfer_reserve(c, n);
+  CK(cudaEventSynchronize(c->xfer_done));
+  pack_rows_kernel<T><<<grid_for(static_cast<int64_t>(n), 256, c->num_sms, 8), 256, 0, c->stream>>>(
+      buf.as<T>() + c->off[k0], c->xfer_dev.as<double>(), static_cast<int64_t>(n),
+      static_cast<int>(c->r), static_cast<int>(c->rp));
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->xfer_host, c->xfer_dev.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaEventRecord(c->xfer_done, c->stream));
+  CK(cudaEventSynchronize(c->xfer_done));
+  std::memcpy(out, c->xfer_host, n * sizeof(double));
 }
 
 void upload(gcpb_ctx* c, DBuf& buf, int mode, const double* v) {

@@ -768,4 +768,27 @@ __global__ void domain_scan_kernel(const V* __restrict__ v, int64_t n, unsigned*
   if (f) atomicOr(flags, f);
 }
 
+// Factor transfers: unpadded fp64 rows <-> padded device rows (padding
+// columns written as zero, so the "padding stays zero" invariant holds).
+template <typename T>
+__global__ void unpack_rows_kernel(const double* __restrict__ src, T* __restrict__ dst,
+                                   int64_t total, int r, int rp) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / rp;
+    const int col = static_cast<int>(i - row * rp);
+    dst[i] = col < r ? static_cast<T>(src[row * r + col]) : static_cast<T>(0);
+  }
+}
+
+template <typename T>
+__global__ void pack_rows_kernel(const T* __restrict__ src, double* __restrict__ dst, int64_t n,
+                                 int r, int rp) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / r;
+    dst[i] = static_cast<double>(src[row * rp + (i - row * r)]);
+  }
+}
+
 }  // namespace gcpb
