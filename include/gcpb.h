@@ -209,6 +209,11 @@ int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
  * next synchronising call. */
 int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter0, int64_t n, const gcpb_adam* adam);
+/* Which engine ran the last gcpb_run_steps: 0 = CUDA graph of fused steps,
+ * 1 = the small-problem cluster kernel (all n iterations in one launch,
+ * chosen when uniform draws, one rank, Philox, the model fits in shared
+ * memory and s*d*r <= 16384; GCPB_NO_SMALL=1 disables it). */
+int gcpb_steps_path(const gcpb_ctx* ctx);
 /* Per-launch timing of the fused sample->MTTKRP kernel: CUDA events recorded
  * on the context's stream around each non-graph launch.  enable = 1 clears
  * and starts recording, 0 stops.  gcpb_kernel_time synchronises and returns

@@ -124,6 +124,7 @@ SIGNATURES = [
     ("gcpb_run_steps", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
                                  C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(gcpb_adam)]),
     ("gcpb_synchronize", C.c_int, [ctx_p]),
+    ("gcpb_steps_path", C.c_int, [ctx_p]),
     ("gcpb_gradient_full", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),
     ("gcpb_gradient_poisson_implicit", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),
     ("gcpb_bias_variance", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),

@@ -36,7 +36,7 @@ SOURCES = ["gcpb.cu", "gcpb_fused_f32.cu", "gcpb_fused_f64.cu", "gcpb_io.cpp"]
 _FUSED_DEPS = ["philox.cuh", "gcpb_kernels.cuh", "gcpb_fused.cuh"]
 DEPS = {
     "gcpb.cu": ["philox.cuh", "gcpb_kernels.cuh", "gcpb_aux.cuh", "gcpb_gen.cuh",
-                "gcpb_gen_host.inc", "rngstream.h"],
+                "gcpb_gen_host.inc", "rngstream.h", "gcpb_small.cuh"],
     "gcpb_fused_f32.cu": _FUSED_DEPS,
     "gcpb_fused_f64.cu": _FUSED_DEPS,
     "gcpb_io.cpp": [],

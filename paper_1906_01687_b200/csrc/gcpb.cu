@@ -24,6 +24,7 @@
 #include "../../include/gcpb.h"
 #include "gcpb_aux.cuh"
 #include "gcpb_gen.cuh"
+#include "gcpb_small.cuh"
 #include "gcpb_kernels.cuh"
 #include "rngstream.h"
 
@@ -242,6 +243,9 @@ struct gcpb_ctx {
   // (unpadded fp64 rows), packed/unpacked by a kernel; one copy per call
   double* xfer_host = nullptr;
   size_t xfer_cap = 0;
+  DBuf small_g;               // triple-buffered gradient of the small-problem kernel
+  bool small_g_zero = false;
+  int last_steps_path = 0;    // 0: CUDA graph of fused steps, 1: small-problem cluster kernel
   DBuf xfer_dev;
   cudaEvent_t xfer_done = nullptr;
 
@@ -1198,6 +1202,96 @@ std::string steps_key(const gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss
   return std::string(buf) + (c->draw_stream ? "|ref" : "|philox");
 }
 
+// Small problems (model L2-resident, few samples, uniform draws, one rank,
+// Philox): all n iterations in one cluster launch (gcpb_small.cuh).
+// GCPB_NO_SMALL=1 forces the graph path.
+constexpr size_t kSmallModelMax = 200 * 1024;  // A, B, C replicas in shared memory
+
+template <typename T>
+bool small_eligible(const gcpb_ctx* c, const gcpb_sampler* sk) {
+  static const bool disabled = std::getenv("GCPB_NO_SMALL") != nullptr;
+  if (disabled || c->nranks != 1 || c->draw_stream != 0 || c->timing) return false;
+  // red.global issue costs ~1.3 cycles per lane on the issuing SM: keep the
+  // per-iteration scatter of the 8 cluster SMs well under a microsecond
+  if (sk->strategy != GCPB_UNIFORM || sk->num_samples * c->d * c->r > 16384) return false;
+  if (c->d > 8 || (c->tensor_kind == 2 && !c->hash_ready)) return false;
+  for (int k = 0; k < c->d; ++k)
+    if (static_cast<uint64_t>(c->dims[k]) > 0xffffffffull) return false;
+  return 3 * static_cast<size_t>(c->nelem) * sizeof(T) <= kSmallModelMax;
+}
+
+template <typename T, int DM>
+void small_launch_dm(const SmallArgs<T>& a, T* G, cudaStream_t stream) {
+  const size_t smem = 3 * static_cast<size_t>(a.nelem) * sizeof(T);
+  CK(cudaFuncSetAttribute(small_steps_kernel<T, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kSmallModelMax)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kSmallCluster, 1, 1);
+  cfg.blockDim = dim3(kSmallThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kSmallCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, small_steps_kernel<T, DM>, a, G));
+}
+
+template <typename T>
+void small_launch(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
+                  int64_t n) {
+  const FusedArgs<T> f = base_args<T>(c, loss, seed, 0);
+  SmallArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.A = c->A.as<T>();
+  a.B = c->B.as<T>();
+  a.C = c->C.as<T>();
+  a.nelem = c->nelem;
+  a.d = c->d;
+  a.r = static_cast<int>(c->r);
+  a.rp = static_cast<int>(c->rp);
+  for (int k = 0; k < c->d; ++k) {
+    a.off[k] = f.off[k];
+    a.dims[k] = f.dims[k];
+    a.thr[k] = f.thr[k];
+    a.stride[k] = f.stride[k];
+  }
+  a.xkind = f.xkind;
+  a.dense = f.dense;
+  a.hkeys = f.hkeys;
+  a.hvals = f.hvals;
+  a.hmask = f.hmask;
+  a.vals = f.vals;
+  a.loss = f.loss;
+  a.delta = f.delta;
+  a.s = sk->num_samples;
+  a.w = c->total_d / static_cast<double>(sk->num_samples);  // samplers.hpp:83
+  a.seed = seed;
+  a.tag = TAG_GRAD_UNIFORM;
+  a.n_steps = n;
+  a.st = c->dst();
+  c->small_g.alloc(3 * static_cast<size_t>(c->nelem) * sizeof(T));
+  if (!c->small_g_zero) {
+    CK(cudaMemsetAsync(c->small_g.p, 0, 3 * static_cast<size_t>(c->nelem) * sizeof(T), c->stream));
+    c->small_g_zero = true;  // the kernel leaves all three buffers zero
+  }
+  T* G = c->small_g.as<T>();
+  switch (c->d) {
+    case 1: small_launch_dm<T, 1>(a, G, c->stream); break;
+    case 2: small_launch_dm<T, 2>(a, G, c->stream); break;
+    case 3: small_launch_dm<T, 3>(a, G, c->stream); break;
+    case 4: small_launch_dm<T, 4>(a, G, c->stream); break;
+    case 5: small_launch_dm<T, 5>(a, G, c->stream); break;
+    case 6: small_launch_dm<T, 6>(a, G, c->stream); break;
+    case 7: small_launch_dm<T, 7>(a, G, c->stream); break;
+    default: small_launch_dm<T, 8>(a, G, c->stream); break;
+  }
+  CK(cudaGetLastError());
+}
+
 template <typename T>
 void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
                     uint64_t iter0, int64_t n, const gcpb_adam* adam) {
@@ -1216,6 +1310,13 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     ensure_hash(c);
   }
   set_rng_iter(c, iter0);
+  if (small_eligible<T>(c, sk)) {
+    small_launch<T>(c, sk, loss, seed, n);
+    c->grad_zero = true;
+    c->last_steps_path = 1;
+    return;
+  }
+  c->last_steps_path = 0;
   const std::string key = steps_key(c, sk, loss, seed, n);
   if (!c->graph_exec || key != c->graph_key) {
     if (c->graph_exec) {
@@ -2135,6 +2236,8 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
     ctx->sync();
   });
 }
+
+int gcpb_steps_path(const gcpb_ctx* ctx) { return ctx ? ctx->last_steps_path : -1; }
 
 int gcpb_synchronize(gcpb_ctx* ctx) {
   return guard(ctx, [&] { sync_and_check(ctx); });

@@ -135,6 +135,35 @@ __device__ __forceinline__ T loss_deriv(int kind, T delta, T x, T m) {
   }
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// fp32 derivative with one-MUFU reciprocals (<= 1 ulp); fp64 keeps IEEE
+// division (the reference's arithmetic, loss.cpp:88-110).
+__device__ __forceinline__ float loss_deriv_fast(int kind, float delta, float x, float m) {
+  const float eps = 1e-10f;
+  if (kind == 2) return rcp_approx(m + 1.0f) - x * rcp_approx(m + eps);  // bernoulli-odds
+  if (kind == 0) return 2.0f * (m - x);                                  // gaussian
+  if (kind == 1) return 1.0f - x * rcp_approx(m + eps);                  // poisson
+  if (kind == 3) {                                                       // gamma
+    const float r = rcp_approx(m + eps);
+    return r - x * (r * r);
+  }
+  if (kind == 4) {  // beta-half
+    const float r = rsqrtf(m + eps);
+    return r - x * (r * r * r);
+  }
+  const float rr = x - m;  // huber
+  if (fabsf(rr) <= delta) return -2.0f * rr;
+  return rr > 0.0f ? -2.0f * delta : 2.0f * delta;
+}
+__device__ __forceinline__ double loss_deriv_fast(int kind, double delta, double x, double m) {
+  return loss_deriv<double>(kind, delta, x, m);
+}
+
 __device__ __forceinline__ double loss_value(int kind, double delta, double x, double m) {
   const double eps = 1e-10;
   switch (kind) {

@@ -477,6 +477,11 @@ class Engine:
         a = self._adam(learning_rate, beta1, beta2, epsilon, lower_bound)
         self._ck(lib.gcpb_run_steps(self._h, C.byref(sk), C.byref(ls), seed, it0, n, C.byref(a)))
 
+    @property
+    def steps_path(self) -> str:
+        """Engine of the last run_steps: "graph" or "small" (cluster kernel)."""
+        return {0: "graph", 1: "small"}.get(int(lib.gcpb_steps_path(self._h)), "unknown")
+
     def adam_reset(self) -> None:
         self._ck(lib.gcpb_adam_reset(self._h))
 

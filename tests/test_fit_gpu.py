@@ -184,3 +184,44 @@ def test_fit_matches_reference_fit(ref):
     init = objective(_expected_init(O.oracle(), 7, dims, R, np.linalg.norm(X)))
     assert ours < 0.5 * init and theirs < 0.5 * init
     assert abs(ours - theirs) / theirs <= 0.05
+
+
+@pytest.mark.parametrize("dims,r,dtype,storage,s", [
+    ((100, 100, 100), 5, "f64", "f64", 300),      # C1
+    ((20, 15, 10, 8), 6, "f32", "bit", 600),
+    ((20, 15, 10, 8), 6, "f32", "bit", 5000),     # over the scatter budget: graph path
+    ((50, 40), 3, "f64", "u8", 700),
+    ((12, 10, 9, 8, 7), 4, "f32", "f32", 64),     # d = 5
+])
+def test_small_persistent_kernel_equals_stepping(dims, r, dtype, storage, s):
+    """run_steps on a small problem (model in shared memory, s*d*r <= 16384)
+    takes the one-launch cluster kernel (gcpb_small.cuh); it must reproduce
+    the per-step path (same draws; gradient sums differ only in order)."""
+    g = G()
+    rs = np.random.default_rng(len(dims) + r)
+    F = [rs.uniform(0.1, 1, (n, r)) for n in dims]
+    if storage in ("bit", "u8"):
+        dense = (rs.random(int(np.prod(dims))) < 0.3).astype(np.float64)
+        lf, lb = g.LossFunction.bernoulli_odds(), 0.0
+    else:
+        dense = rs.normal(size=int(np.prod(dims)))
+        lf, lb = g.LossFunction.gaussian(), None
+    engines = [g.Engine(dims, r, dtype) for _ in range(2)]
+    for e in engines:
+        e.set_dense(dense, storage)
+        e.set_factors(F)
+    a, b = engines
+    sk = g.SamplerKind.uniform(s)
+    a.run_steps(sk, lf, 9, 0, 40, 1e-3, lower_bound=lb)
+    for it in range(40):
+        b.step(sk, lf, 9, it, 1e-3, lower_bound=lb)
+    tol = 1e-10 if dtype == "f64" else 2e-4
+    for x, y in zip(a.factors(), b.factors()):
+        assert O.rel_error(x, y) <= tol
+    assert a.iterations == b.iterations == 40
+    # continues the stream on the next call
+    a.run_steps(sk, lf, 9, 40, 10, 1e-3, lower_bound=lb)
+    for it in range(40, 50):
+        b.step(sk, lf, 9, it, 1e-3, lower_bound=lb)
+    for x, y in zip(a.factors(), b.factors()):
+        assert O.rel_error(x, y) <= tol
