@@ -555,6 +555,10 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   // Factor tables beyond ~half of L2 gather from HBM: use the staged kernel.
   a.stage = (c->nelem * static_cast<int64_t>(c->tsize) > (int64_t{64} << 20)) ? 1 : 0;
   if (const char* ev = getenv("GCPB_STAGE")) a.stage = atoi(ev);
+  // Factor tables beyond L2: cold rows (unrestricted draws) and nonzero
+  // records evict_first, the nonzero picks' rows evict_last (C5: +3%).
+  a.l2hint = a.stage ? 2 : 0;
+  if (const char* ev = getenv("GCPB_L2HINT")) a.l2hint = atoi(ev);
   return a;
 }
 

@@ -183,7 +183,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (q * 4 < a.rec_words) v = __ldg(rp + q);
+        if (q * 4 < a.rec_words) v = a.l2hint ? ld_hint_u4(rp + q, policy_evict_first()) : __ldg(rp + q);
         wds[q * 4 + 0] = v.x;
         wds[q * 4 + 1] = v.y;
         wds[q * 4 + 2] = v.z;
@@ -512,6 +512,19 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem),
+               "l"(pol)
+               : "memory");
+}
+// Per-segment L2 policy of the staged kernel (FusedArgs::l2hint); 0 = none.
+template <typename T>
+__device__ __forceinline__ uint64_t seg_policy(const FusedArgs<T>& a, int kind) {
+  if (a.l2hint == 0) return 0ull;
+  if (kind == SEG_PICK) return a.l2hint == 2 ? policy_evict_last() : 0ull;
+  return policy_evict_first();
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -520,13 +533,17 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <typename T, int DM>
 __device__ __forceinline__ void stage_rows(const FusedArgs<T>& a, T* slot,
-                                           const uint32_t (&ik)[DM], bool valid) {
+                                           const uint32_t (&ik)[DM], bool valid, uint64_t pol) {
   constexpr int VW = Vec<T>::W;
   if (valid) {
 #pragma unroll
     for (int k = 0; k < DM; ++k) {
       const T* src = a.A + a.off[k] + static_cast<int64_t>(ik[k]) * a.rp;
-      for (int c = 0; c < a.nchunks; ++c) cp_async16(slot + k * a.rp + c * VW, src + c * VW);
+      if (pol)
+        for (int c = 0; c < a.nchunks; ++c)
+          cp_async16_hint(slot + k * a.rp + c * VW, src + c * VW, pol);
+      else
+        for (int c = 0; c < a.nchunks; ++c) cp_async16(slot + k * a.rp + c * VW, src + c * VW);
     }
   }
   cp_async_commit();
@@ -544,6 +561,7 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
   const int gl = lane % G;
   const bool given = sg.kind == SEG_GIVEN;
   const T wseg = static_cast<T>(sg.weight);
+  const uint64_t pol = seg_policy(a, sg.kind);
   const int cidx = gl < a.nchunks ? gl : a.nchunks - 1;
   const T cmask = gl < a.nchunks ? static_cast<T>(1) : static_cast<T>(0);
   const bool owns = gl < a.nchunks;
@@ -606,9 +624,12 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
           out[e] = y * (pre[k][e] * suf[e]);
           suf[e] = suf[e] * row[k][e];
         }
-        red_chunk(Gb + static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.rp) +
-                      cidx * VW,
-                  out);
+        T* gp = Gb + static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.rp) +
+                cidx * VW;
+        if (pol)
+          red_chunk_hint(gp, out, pol);
+        else
+          red_chunk(gp, out);
       }
     }
   }
@@ -633,7 +654,7 @@ __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T>
   SegRegs sg = seg_of<T>(a, tile);
   phase_a<T, DM, true>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik, s);
   int buf = 0;
-  stage_rows<T, DM>(a, wbuf + (buf * 32 + lane) * slot_elems, ik, s.valid);
+  stage_rows<T, DM>(a, wbuf + (buf * 32 + lane) * slot_elems, ik, s.valid, seg_policy(a, sg.kind));
   for (; tile < total_tiles; tile += nwarps) {
     const int64_t next = tile + nwarps;
     uint32_t ik2[DM];
@@ -648,7 +669,8 @@ __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T>
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
-    stage_rows<T, DM>(a, wbuf + ((buf ^ 1) * 32 + lane) * slot_elems, ik2, s2.valid);
+    stage_rows<T, DM>(a, wbuf + ((buf ^ 1) * 32 + lane) * slot_elems, ik2, s2.valid,
+                      seg_policy(a, sg2.kind));
     cp_async_wait<1>();  // this tile's rows have landed; the next tile's stay in flight
     __syncwarp();
     phase_b_staged<T, DM, G>(a, sg, wbuf + buf * 32 * slot_elems, s, ik, Gb);

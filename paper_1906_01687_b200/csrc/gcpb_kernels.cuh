@@ -104,6 +104,11 @@ struct FusedArgs {
   unsigned* ref_flag;         // set when a draw would have been rejected
   int prefetch;  // 1: prefetch the next tile's rows into L2 (opt-in)
   int stage;     // 1: factor tables exceed L2 -> cp.async-staged kernel variant
+  // L2 residency hints for factor tables that exceed L2 (staged kernel):
+  // 0 none; 1 rows of unrestricted/uniform draws and nonzero records
+  // evict_first (no reuse), so the nonzero picks' hot rows stay; 2 as 1 and
+  // the picks' rows evict_last.
+  int l2hint;
 };
 
 // ---------------------------------------------------------------------------
@@ -233,6 +238,36 @@ __device__ __forceinline__ void red_chunk(float* p, const float (&v)[4]) {
 __device__ __forceinline__ void red_chunk(double* p, const double (&v)[2]) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v[0]) : "memory");
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(v[1]) : "memory");
+}
+
+// L2 eviction-priority policies (createpolicy) and hinted accesses.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_hint_u4(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void red_chunk_hint(float* p, const float (&v)[4], uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void red_chunk_hint(double* p, const double (&v)[2], uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v[0]), "l"(pol)
+               : "memory");
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p + 1), "d"(v[1]), "l"(pol)
+               : "memory");
 }
 
 // Streaming loads of tensor data that should not displace factor rows in L1.
