@@ -393,42 +393,38 @@ def run_ours(args, w):
                                             "scattered factor rows)",
                 "units_per_launch": w.samples_per_step, "peak_source": peak_src}
 
-    # e2e through the C-ABI with host buffers: factors H2D, step, factors D2H
+    # e2e through the C-ABI with host buffers: every step copies the model in
+    # from pinned host memory, runs the iteration, and copies the updated
+    # model out (gcpb_step_host: the reference's loop body on a host model)
     e2e = None
     if not args.no_e2e:
-        host_F = e.factors()
+        nflat = sum(n * w.rank for n in w.dims)
+        pin_in = torch.empty(nflat, dtype=torch.float64, pin_memory=True).numpy()
+        pin_out = torch.empty(nflat, dtype=torch.float64, pin_memory=True).numpy()
+        pin_in[:] = np.concatenate([f.ravel() for f in e.factors()])
         Ke = max(3, min(K, 20))
         for it in range(2):
-            e.set_factors(host_F)
-            e.stoch_grad(sk, loss, seed, 60_000 + it, want_stats=False)
-            if world > 1:
-                e.allreduce_grad()
-            e.adam_step(lr, lower_bound=lb)
-            host_F = e.factors()
+            e.step_host(sk, loss, seed, 60_000 + it, lr, pin_in, pin_out, lower_bound=lb)
+            pin_in[:] = pin_out
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for it in range(Ke):
-            e.set_factors(host_F)
-            e.stoch_grad(sk, loss, seed, 70_000 + it, want_stats=False)
-            if world > 1:
-                e.allreduce_grad()
-            e.adam_step(lr, lower_bound=lb)
-            host_F = e.factors()
+            e.step_host(sk, loss, seed, 70_000 + it, lr, pin_in, pin_out, lower_bound=lb)
+            pin_in, pin_out = pin_out, pin_in
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         if dist:
             t = torch.tensor([el], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t[0])
-        pad = 8 if w.dtype == "f32" else 4
-        rp = (w.rank + pad - 1) // pad * pad
-        nbytes = sum(n * rp * (4 if w.dtype == "f32" else 8) for n in w.dims)
+        nbytes = nflat * 8
         e2e = {"value": samples_per_step * Ke / el, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes,
-               "what": "per step through the C-ABI with host buffers: gcpb_set_factors(host) + "
-                       "gcpb_stoch_grad + gcpb_adam_step + gcpb_get_factors(host), wall clock"}
+               "what": "per step through the C-ABI with pinned host buffers: gcpb_step_host = "
+                       "model H2D + sample/eval/MTTKRP (+ all-reduce) + Adam + model D2H, one "
+                       "call and one synchronisation per step, wall clock"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -201,6 +201,15 @@ int gcpb_set_iterations(gcpb_ctx* ctx, int64_t iterations);
  * reduction folded into the Adam update.  No host synchronisation. */
 int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss, uint64_t seed,
               uint64_t iter, const gcpb_adam* adam);
+/* The same iteration on a HOST-resident model, as the reference's loop body
+ * sees it (draw_gradient_samples(x, model, ...) + adam_step(model&, ...) on a
+ * host KruskalModel): model_in (flattened factors, GradientSet order) is
+ * copied in before the step and the updated factors copied out to model_out
+ * after it (either may be NULL).  One call, one pinned-staged copy each way,
+ * one synchronisation. */
+int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                   uint64_t seed, uint64_t iter, const gcpb_adam* adam, const double* model_in,
+                   double* model_out);
 /* n iterations iter0 .. iter0+n-1 replayed as one CUDA graph (captured once per
  * sampler/loss/seed/n configuration; the draw-stream iteration and Adam's
  * counter advance on the device).  Equivalent to n calls of gcpb_step.  For

@@ -121,6 +121,8 @@ SIGNATURES = [
     ("gcpb_set_iterations", C.c_int, [ctx_p, C.c_int64]),
     ("gcpb_step", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss), C.c_uint64,
                             C.c_uint64, C.POINTER(gcpb_adam)]),
+    ("gcpb_step_host", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss), C.c_uint64,
+                                 C.c_uint64, C.POINTER(gcpb_adam), f64p, f64p]),
     ("gcpb_run_steps", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
                                  C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(gcpb_adam)]),
     ("gcpb_synchronize", C.c_int, [ctx_p]),

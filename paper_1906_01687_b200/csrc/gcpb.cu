@@ -1352,18 +1352,18 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
 // Synchronise and surface deferred device-side failures (graph-mode
 // stratified shortfalls).
 void sync_and_check(gcpb_ctx* c) {
+  // both flags come back with the one synchronisation the caller needs
+  uint32_t* flags = reinterpret_cast<uint32_t*>(&c->pinned_params[12]);
+  CK(cudaMemcpyAsync(&flags[0], &c->dst()->ref_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&flags[1], &c->dst()->z_incomplete, 4, cudaMemcpyDeviceToHost, c->stream));
   c->sync();
+  const uint32_t rf = flags[0];
+  const int32_t inc = static_cast<int32_t>(flags[1]);
   if (c->draw_stream == 1) {
-    uint32_t rf = 0;
-    CK(cudaMemcpyAsync(&rf, &c->dst()->ref_flag, 4, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
     if (rf)
       throw std::runtime_error("RefStream: a draw fell in RngStream::next_below's rejection "
                                "region (p <= n/2^64); the reference would have redrawn");
   }
-  int32_t inc = 0;
-  CK(cudaMemcpyAsync(&inc, &c->dst()->z_incomplete, 4, cudaMemcpyDeviceToHost, c->stream));
-  c->sync();
   if (inc != 0) {
     const int32_t zero = 0;
     CK(cudaMemcpyAsync(&c->dst()->z_incomplete, &zero, 4, cudaMemcpyHostToDevice, c->stream));
@@ -2184,6 +2184,22 @@ int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
       step_impl<float>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
     else
       step_impl<double>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
+  });
+}
+
+int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                   uint64_t seed, uint64_t iter, const gcpb_adam* adam, const double* model_in,
+                   double* model_out) {
+  return guard(ctx, [&] {
+    check_step_args(ctx, sampler, loss);
+    if (model_in) upload(ctx, ctx->A, -1, model_in);
+    set_adam_params(ctx, adam);
+    ensure_grad_zero(ctx);
+    if (ctx->dtype == GCPB_F32)
+      step_impl<float>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
+    else
+      step_impl<double>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
+    if (model_out) download(ctx, ctx->A, -1, model_out);
   });
 }
 

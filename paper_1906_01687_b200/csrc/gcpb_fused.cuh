@@ -464,9 +464,13 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
   bool given = false;  // any segment beyond the samplers needs the general kernel
   for (int s = 0; s < a.nseg; ++s) given = given || a.seg[s].kind >= SEG_GIVEN;
   auto go = [&](auto kern) -> cudaError_t {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-    if (per_sm < 1) per_sm = 1;
+    // resident blocks per SM: queried once per kernel instantiation (the
+    // query costs microseconds, and small steps are launch-bound)
+    static const int per_sm = [&] {
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 256, 0);
+      return v < 1 ? 1 : v;
+    }();
     int64_t blocks = (total_tiles + 7) / 8;
     const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
     if (blocks > cap) blocks = cap;

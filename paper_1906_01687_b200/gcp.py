@@ -469,6 +469,16 @@ class Engine:
         a = self._adam(learning_rate, beta1, beta2, epsilon, lower_bound)
         self._ck(lib.gcpb_step(self._h, C.byref(sk), C.byref(ls), seed, it, C.byref(a)))
 
+    def step_host(self, sampler: SamplerKind, loss: LossFunction, seed: int, it: int,
+                  learning_rate: float, model_in: Optional[np.ndarray], model_out: Optional[np.ndarray],
+                  beta1=0.9, beta2=0.999, epsilon=1e-8, lower_bound: Optional[float] = None) -> None:
+        """One iteration on a host-resident model (flattened factors in/out)."""
+        sk, ls = sampler.c(), loss.c()
+        a = self._adam(learning_rate, beta1, beta2, epsilon, lower_bound)
+        self._ck(lib.gcpb_step_host(self._h, C.byref(sk), C.byref(ls), seed, it, C.byref(a),
+                                    _f64(model_in) if model_in is not None else None,
+                                    _f64(model_out) if model_out is not None else None))
+
     def run_steps(self, sampler: SamplerKind, loss: LossFunction, seed: int, it0: int, n: int,
                   learning_rate: float, beta1=0.9, beta2=0.999, epsilon=1e-8,
                   lower_bound: Optional[float] = None) -> None:

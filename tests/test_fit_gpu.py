@@ -225,3 +225,27 @@ def test_small_persistent_kernel_equals_stepping(dims, r, dtype, storage, s):
         b.step(sk, lf, 9, it, 1e-3, lower_bound=lb)
     for x, y in zip(a.factors(), b.factors()):
         assert O.rel_error(x, y) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_step_host_equals_set_step_get(dtype):
+    """gcpb_step_host (model in, one iteration, model out) is exactly
+    set_factors + step + factors."""
+    g = G()
+    rs = np.random.default_rng(3)
+    dims, r = (30, 20, 10), 4
+    coords, vals = _sparse(rs, dims, 0.05)
+    F = [rs.uniform(0.1, 1, (n, r)) for n in dims]
+    a, b = g.Engine(dims, r, dtype), g.Engine(dims, r, dtype)
+    for e in (a, b):
+        e.set_sparse(coords, vals)
+    sk, lf = g.SamplerKind.semi_stratified(300, 300), g.LossFunction.bernoulli_odds()
+    flat = np.concatenate([f.ravel() for f in F])
+    out = np.zeros_like(flat)
+    for it in range(3):
+        a.step_host(sk, lf, 4, it, 1e-2, flat, out, lower_bound=0.0)
+        b.set_factors(F if it == 0 else b.factors())
+        b.step(sk, lf, 4, it, 1e-2, lower_bound=0.0)
+        want = np.concatenate([f.ravel() for f in b.factors()])
+        assert O.rel_error(out, want) <= (1e-12 if dtype == "f64" else 1e-6)
+        flat = out.copy()
