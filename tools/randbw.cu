@@ -60,7 +60,8 @@ __global__ void kern(float* tab, int64_t rows, int64_t n, float* sink, uint64_t 
 }
 
 int main() {
-  const int64_t bytes = int64_t(1) << 30, rows = bytes / 64;
+  const int64_t bytes = (getenv("TABMB") ? int64_t(atoi(getenv("TABMB"))) << 20 : int64_t(1) << 30),
+                rows = bytes / 64;
   float* tab;
   float* sink;
   cudaMalloc(&tab, bytes);
