@@ -197,6 +197,18 @@ def sampler_of(w, G, nranks=1):
     return G.SamplerKind.semi_stratified(w.p * nranks, w.q * nranks)
 
 
+ROOFLINE_NOTES = {
+    "c1": "latency-bound (300 samples/step); one cluster launch runs all K iterations",
+    "c2": "factor rows are L1/L2-resident (51 KB), so B_alg/s exceeds HBM peak; the binding "
+          "limit is L2 reduction throughput (ncu: L1->L2 request interface 85% busy, 4.1 GB of "
+          "red.global.add.v4.f32 per launch), see DESIGN.md section 5",
+    "c3": "factors (512 KB) L2-resident; bound by L2 reductions and the hash probes",
+    "c4": "latency-bound: 2e5 samples per step (1.3 tiles per warp)",
+    "c5": "random 64-byte HBM access: measured bound for this pattern is 4.9e9 samples/s "
+          "(tools/randbw.cu, profiles/r01_randbw.md), i.e. frac 0.30 of streaming peak",
+}
+
+
 def launches_per_step(w):
     # fused kernel + adam; the stratified zero sampler adds 3 x (plan +
     # candidate) + a shortfall check
@@ -391,7 +403,8 @@ def run_ours(args, w):
                 "bytes_per_sample": bps,
                 "bytes_per_sample_formula": "4d + 2*d*r*F (int32 index/mode + gathered + "
                                             "scattered factor rows)",
-                "units_per_launch": w.samples_per_step, "peak_source": peak_src}
+                "units_per_launch": w.samples_per_step, "peak_source": peak_src,
+                "note": ROOFLINE_NOTES.get(w.name, "")}
 
     # e2e through the C-ABI with host buffers: every step copies the model in
     # from pinned host memory, runs the iteration, and copies the updated
