@@ -332,6 +332,7 @@ class Reference:
                                     u64p]
         L.ref_gen_binary.argtypes = [C.c_int, i64p, C.c_int64, C.c_double, C.c_double, C.c_double,
                                      C.c_uint64, C.POINTER(vp), f64p, u64p]
+        L.ref_variance_ordering.argtypes = [f64p, f64p]
         L.ref_read_tns.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
         L.ref_write_tns.argtypes = [vp, C.c_char_p]
         L.ref_read_dense.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
@@ -400,6 +401,13 @@ class Reference:
         self._ck(self.lib.ref_gen_binary(len(dims), _i64(dims), r, delta, p_high, p_low, seed,
                                          C.byref(h), _f64(truth), C.byref(nxt)))
         return RefTensor(self, h, dims), truth, nxt.value
+
+    def variance_ordering(self):
+        """acceptance.cpp criterion 5: (model factors flat, [var_uni, var_strat, var_semi])."""
+        model = np.zeros((40 + 30 + 20) * 3)
+        var = np.zeros(3)
+        self._ck(self.lib.ref_variance_ordering(_f64(model), _f64(var)))
+        return model, var
 
     def read_tns(self, path):
         h, d, dims = C.c_void_p(), C.c_int(), np.zeros(16, dtype=np.int64)

@@ -269,6 +269,33 @@ int ref_gen_binary(int d, const std::int64_t* dims, std::int64_t r, double delta
   });
 }
 
+// acceptance.cpp:215-250 (criterion 5, variance ordering), restated through
+// the public API: the instance, the scaled model it evaluates, and the three
+// empirical variances (uniform, stratified, semi-stratified).
+int ref_variance_ordering(double* model_out, double* var_out) {
+  return guard([&] {
+    gcp::BinaryProblemSpec spec;
+    spec.shape = gcp::Shape({40, 30, 20});
+    spec.rank = 3;
+    spec.delta = 0.15;
+    spec.p_high = 0.9;
+    spec.p_low = 0.0025;
+    gcp::RngStream rng(1005);
+    const auto [x, truth] = gcp::gen_binary_problem(spec, rng);
+    gcp::KruskalModel model = gcp::KruskalModel::random_uniform(spec.shape, 3, rng);
+    if (x.norm() > 0.0) model.scale_norm_to(0.5 * x.norm());
+    flatten_model(model, model_out);
+    const gcp::LossFunction loss = gcp::LossFunction::bernoulli_odds();
+    const char* tokens[3] = {"uniform", "stratified", "semi-stratified"};
+    for (int i = 0; i < 3; ++i) {
+      gcp::RngStream r = rng.split(tokens[i]);
+      var_out[i] = gcp::empirical_bias_variance(gcp::SamplerKind::from_token(tokens[i], 90),
+                                                gcp::TensorView(x), model, loss, 1000, r)
+                       .variance;
+    }
+  });
+}
+
 // ---- tensor files (io.cpp) ------------------------------------------------------------
 namespace {
 void shape_out(const gcp::Shape& s, int* d, std::int64_t* dims) {
