@@ -259,6 +259,12 @@ int gcpb_gradient_poisson_implicit(gcpb_ctx* ctx, const gcpb_loss* loss);
 int gcpb_bias_variance(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                        int64_t trials, uint64_t seed, const double* exact, double* bias,
                        double* variance);
+/* Per-coordinate moments of the same `trials` stochastic gradients: mean and
+ * unbiased sample variance (M2 / (trials - 1)), GradientSet order; either
+ * output may be NULL (acceptance.cpp:166-213 checks each coordinate's mean
+ * against 3 standard errors). */
+int gcpb_gradient_moments(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                          int64_t trials, uint64_t seed, double* mean, double* variance);
 
 /* ---- fit driver -------------------------------------------------------------------
  * fit_gcp_adam (src/optimizer.cpp:68-158) with the epoch loop on the device:

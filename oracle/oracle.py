@@ -333,6 +333,8 @@ class Reference:
         L.ref_gen_binary.argtypes = [C.c_int, i64p, C.c_int64, C.c_double, C.c_double, C.c_double,
                                      C.c_uint64, C.POINTER(vp), f64p, u64p]
         L.ref_variance_ordering.argtypes = [f64p, f64p]
+        L.ref_acceptance_instance.argtypes = [C.c_int, C.POINTER(vp), f64p]
+        L.ref_similarity.argtypes = [C.c_int, i64p, C.c_int64, f64p, C.c_int64, f64p, f64p]
         L.ref_read_tns.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
         L.ref_write_tns.argtypes = [vp, C.c_char_p]
         L.ref_read_dense.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
@@ -408,6 +410,21 @@ class Reference:
         var = np.zeros(3)
         self._ck(self.lib.ref_variance_ordering(_f64(model), _f64(var)))
         return model, var
+
+    def acceptance_instance(self, criterion):
+        """(RefTensor, model flat) of acceptance criterion 4 or 10."""
+        dims = {4: (6, 5, 4), 10: (10, 8, 6)}[criterion]
+        h = C.c_void_p()
+        model = np.zeros(sum(dims) * 2)
+        self._ck(self.lib.ref_acceptance_instance(criterion, C.byref(h), _f64(model)))
+        return RefTensor(self, h, np.array(dims, dtype=np.int64)), model
+
+    def similarity(self, dims, est, r_est, truth, r_true):
+        dims = np.ascontiguousarray(dims, dtype=np.int64)
+        out = C.c_double()
+        self._ck(self.lib.ref_similarity(len(dims), _i64(dims), r_est, _f64(Oracle.flat(est)),
+                                         r_true, _f64(Oracle.flat(truth)), C.byref(out)))
+        return out.value
 
     def read_tns(self, path):
         h, d, dims = C.c_void_p(), C.c_int(), np.zeros(16, dtype=np.int64)

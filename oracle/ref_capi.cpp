@@ -27,7 +27,9 @@
 #include "gcp/rng.hpp"
 #include "gcp/samplers.hpp"
 #include "gcp/shape.hpp"
+#include "gcp/scoring.hpp"
 #include "gcp/synthetic.hpp"
+#include "oracles.hpp"  // the reference's own test fixtures (tests/oracles.hpp)
 #include "gcp/tensor.hpp"
 
 namespace {
@@ -266,6 +268,42 @@ int ref_gen_binary(int d, const std::int64_t* dims, std::int64_t r, double delta
     flatten_model(model, truth);
     *next_draw = rng.next_u64();
     *out = h.release();
+  });
+}
+
+// The seeded instances of acceptance.cpp criteria 4 (:166-213) and 10
+// (:432-461), built by the reference's own fixtures: the sparse tensor and
+// the model (flattened).
+int ref_acceptance_instance(int criterion, void** tensor_out, double* model_out) {
+  return guard([&] {
+    auto h = std::make_unique<TensorH>();
+    if (criterion == 4) {
+      const gcp::Shape shape({6, 5, 4});
+      gcp::RngStream rng(1004);
+      const gcp::KruskalModel model = oracles::random_model(shape, 2, rng, 0.1, 1.0);
+      h->sparse = std::make_unique<gcp::SparseTensor>(oracles::random_sparse(
+          shape, 0.25, [](gcp::RngStream& r) { return 1.0 + r.next_double(); }, rng));
+      flatten_model(model, model_out);
+    } else if (criterion == 10) {
+      const gcp::Shape shape({10, 8, 6});
+      gcp::RngStream rng(1010);
+      h->sparse = std::make_unique<gcp::SparseTensor>(oracles::random_sparse(
+          shape, 0.25, [](gcp::RngStream& r) { return 0.5 + r.next_double(); }, rng));
+      const gcp::KruskalModel model = oracles::random_model(shape, 2, rng, 0.1, 1.0);
+      flatten_model(model, model_out);
+    } else {
+      throw std::invalid_argument("ref_acceptance_instance: criterion 4 or 10");
+    }
+    *tensor_out = h.release();
+  });
+}
+
+// cosine_similarity_score (scoring.cpp:23-60) of an estimate against a truth.
+int ref_similarity(int d, const std::int64_t* dims, std::int64_t r_est, const double* est,
+                   std::int64_t r_true, const double* truth, double* out) {
+  return guard([&] {
+    *out = gcp::cosine_similarity_score(make_model(d, dims, r_est, est),
+                                        make_model(d, dims, r_true, truth));
   });
 }
 

@@ -129,6 +129,8 @@ SIGNATURES = [
     ("gcpb_steps_path", C.c_int, [ctx_p]),
     ("gcpb_gradient_full", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),
     ("gcpb_gradient_poisson_implicit", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),
+    ("gcpb_gradient_moments", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
+                                        C.c_int64, C.c_uint64, f64p, f64p]),
     ("gcpb_bias_variance", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),
                                      C.c_int64, C.c_uint64, f64p, f64p, f64p]),
     ("gcpb_set_draw_stream", C.c_int, [ctx_p, C.c_int, C.c_uint64]),

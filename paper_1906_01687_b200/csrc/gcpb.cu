@@ -1460,6 +1460,55 @@ void poisson_implicit_impl(gcpb_ctx* c, const gcpb_loss* loss) {
   c->grad_zero = false;
 }
 
+// Per-element running moments (Welford, fp64) of `trials` stochastic
+// gradients: trial t = Philox iteration t, or in RefStream mode the stream
+// split(t) of the key `seed` from counter 0 (samplers.cpp:140-141).
+template <typename T>
+void trial_moments(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, int64_t trials,
+                   uint64_t seed, DBuf& mean, DBuf& m2) {
+  const int64_t n = c->nelem;
+  mean.alloc(n * 8);
+  m2.alloc(n * 8);
+  CK(cudaMemsetAsync(mean.p, 0, n * 8, c->stream));
+  CK(cudaMemsetAsync(m2.p, 0, n * 8, c->stream));
+  const HostRngStream parent = HostRngStream::from_key(seed);
+  for (int64_t t = 0; t < trials; ++t) {
+    uint64_t key = seed, it = static_cast<uint64_t>(t);
+    if (c->draw_stream == 1) {
+      key = parent.split(static_cast<uint64_t>(t)).key();
+      const uint64_t zero = 0;
+      CK(cudaMemcpyAsync(&c->dst()->ref_ctr, &zero, 8, cudaMemcpyHostToDevice, c->stream));
+      it = 0;
+    }
+    ensure_grad_zero(c);
+    stoch_grad_impl<T>(c, sk, loss, key, it, true, false, true, false, -1);
+    c->grad_zero = false;
+    welford_kernel<T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
+        c->Gr.as<T>(), mean.as<double>(), m2.as<double>(), n, static_cast<double>(t + 1));
+    CK(cudaGetLastError());
+  }
+}
+
+// Padded device fp64 -> unpadded host (GradientSet order), optional scale.
+void padded_to_host(gcpb_ctx* c, const DBuf& src, double* out, double scale) {
+  std::vector<double> h(static_cast<size_t>(c->nelem));
+  CK(cudaMemcpyAsync(h.data(), src.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  for (int k = 0; k < c->d; ++k)
+    for (int64_t i = 0; i < c->dims[k]; ++i)
+      for (int64_t j = 0; j < c->r; ++j) *out++ = h[c->off[k] + i * c->rp + j] * scale;
+}
+
+template <typename T>
+void gradient_moments_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss,
+                           int64_t trials, uint64_t seed, double* mean_out, double* var_out) {
+  if (trials < 2) throw std::invalid_argument("gradient moments: need >= 2 trials");
+  DBuf mean, m2;
+  trial_moments<T>(c, sk, loss, trials, seed, mean, m2);
+  if (mean_out) padded_to_host(c, mean, mean_out, 1.0);
+  if (var_out) padded_to_host(c, m2, var_out, 1.0 / static_cast<double>(trials - 1));
+}
+
 template <typename T>
 void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss,
                         int64_t trials, uint64_t seed, const double* exact, double* bias,
@@ -1483,24 +1532,7 @@ void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* lo
     to_double_kernel<T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(c->Gr.as<T>(),
                                                                               E.as<double>(), n);
   }
-  CK(cudaMemsetAsync(mean.p, 0, n * 8, c->stream));
-  CK(cudaMemsetAsync(m2.p, 0, n * 8, c->stream));
-  const HostRngStream parent = HostRngStream::from_key(seed);
-  for (int64_t t = 0; t < trials; ++t) {
-    uint64_t key = seed, it = static_cast<uint64_t>(t);
-    if (c->draw_stream == 1) {  // samplers.cpp:140-141: trial stream = rng.split(t), from counter 0
-      key = parent.split(static_cast<uint64_t>(t)).key();
-      const uint64_t zero = 0;
-      CK(cudaMemcpyAsync(&c->dst()->ref_ctr, &zero, 8, cudaMemcpyHostToDevice, c->stream));
-      it = 0;
-    }
-    ensure_grad_zero(c);
-    stoch_grad_impl<T>(c, sk, loss, key, it, true, false, true, false, -1);
-    c->grad_zero = false;
-    welford_kernel<T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
-        c->Gr.as<T>(), mean.as<double>(), m2.as<double>(), n, static_cast<double>(t + 1));
-    CK(cudaGetLastError());
-  }
+  trial_moments<T>(c, sk, loss, trials, seed, mean, m2);
   constexpr int kGrid = 296;
   parts.alloc(2 * kGrid * 8);
   sqdiff_sum_kernel<<<kGrid, 256, 0, c->stream>>>(mean.as<double>(), E.as<double>(),
@@ -2281,6 +2313,17 @@ int gcpb_gradient_poisson_implicit(gcpb_ctx* ctx, const gcpb_loss* loss) {
       poisson_implicit_impl<float>(ctx, loss);
     else
       poisson_implicit_impl<double>(ctx, loss);
+  });
+}
+
+int gcpb_gradient_moments(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
+                          int64_t trials, uint64_t seed, double* mean, double* variance) {
+  return guard(ctx, [&] {
+    check_step_args(ctx, sampler, loss);
+    if (ctx->dtype == GCPB_F32)
+      gradient_moments_impl<float>(ctx, sampler, loss, trials, seed, mean, variance);
+    else
+      gradient_moments_impl<double>(ctx, sampler, loss, trials, seed, mean, variance);
   });
 }
 

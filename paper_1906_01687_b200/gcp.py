@@ -541,6 +541,16 @@ class Engine:
         ls = loss.c()
         self._ck(lib.gcpb_gradient_poisson_implicit(self._h, C.byref(ls)))
 
+    def gradient_moments(self, sampler: SamplerKind, loss: LossFunction, trials: int,
+                         seed: int) -> tuple[np.ndarray, np.ndarray]:
+        """Per-coordinate mean and sample variance of `trials` stochastic gradients."""
+        sk, ls = sampler.c(), loss.c()
+        n = sum(self._mode_sizes())
+        mean, var = np.zeros(n), np.zeros(n)
+        self._ck(lib.gcpb_gradient_moments(self._h, C.byref(sk), C.byref(ls), trials, seed,
+                                           _f64(mean), _f64(var)))
+        return mean, var
+
     def bias_variance(self, sampler: SamplerKind, loss: LossFunction, trials: int, seed: int,
                       exact: Optional[np.ndarray] = None) -> tuple[float, float]:
         """empirical_bias_variance (samplers.cpp:134-168) on the device."""
