@@ -399,6 +399,17 @@ int gcpb_dense_shape(const char* path, int* d, int64_t* dims);
 int gcpb_dense_read(const char* path, int64_t n, double* values);
 int gcpb_dense_write(const char* path, int d, const int64_t* dims, const double* values);
 
+/* read_model / write_model (io.cpp:153-193): a 'd r' line, a dims line, then
+ * each factor row by row, values %.17g (bit-exact round trip).  Read the
+ * header first (d, dims[<=16], rank), then the factors (sum_k n_k*rank
+ * doubles, GradientSet order). */
+int gcpb_model_read_header(const char* path, int* d, int64_t* dims, int64_t* rank);
+int gcpb_model_read(const char* path, double* factors);
+int gcpb_model_write(const char* path, int d, const int64_t* dims, int64_t rank,
+                     const double* factors);
+/* write_trace_csv (io.cpp:252-260): epoch,loss_estimate,learning_rate,seconds,accepted. */
+int gcpb_trace_write_csv(const char* path, const gcpb_trace_record* records, int64_t n);
+
 /* ---- host-only helpers (no device needed) ----------------------------------------- */
 /* Product Philox stream: bounded draw in [0, n). */
 uint64_t gcpb_philox_bounded(uint64_t seed, uint32_t tag, uint64_t iter, uint64_t t, int slot,

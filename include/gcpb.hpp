@@ -221,6 +221,34 @@ inline void write_coo(const CooTensor& t, const std::string& path) {
   check(gcpb_coo_write(path.c_str(), &c));
 }
 
+// read_model / write_model (io.cpp:153-193): factors as n_k x r row-major.
+inline std::vector<std::vector<double>> read_model(const std::string& path,
+                                                   std::vector<int64_t>* dims_out = nullptr) {
+  int d = 0;
+  int64_t dims[16] = {};
+  int64_t r = 0;
+  check(gcpb_model_read_header(path.c_str(), &d, dims, &r));
+  size_t n = 0;
+  for (int k = 0; k < d; ++k) n += static_cast<size_t>(dims[k] * r);
+  std::vector<double> flat(n);
+  check(gcpb_model_read(path.c_str(), flat.data()));
+  std::vector<std::vector<double>> out(static_cast<size_t>(d));
+  size_t at = 0;
+  for (int k = 0; k < d; ++k) {
+    out[k].assign(flat.begin() + at, flat.begin() + at + dims[k] * r);
+    at += static_cast<size_t>(dims[k] * r);
+  }
+  if (dims_out) dims_out->assign(dims, dims + d);
+  return out;
+}
+inline void write_model(const std::vector<std::vector<double>>& factors,
+                        const std::vector<int64_t>& dims, int64_t rank, const std::string& path) {
+  std::vector<double> flat;
+  for (const auto& f : factors) flat.insert(flat.end(), f.begin(), f.end());
+  check(gcpb_model_write(path.c_str(), static_cast<int>(dims.size()), dims.data(), rank,
+                         flat.data()));
+}
+
 // One stochastic-GCP problem on one GPU.
 class Engine {
  public:
@@ -332,6 +360,14 @@ struct FitResult {
   std::vector<FitTraceRecord> trace;
   double final_loss_estimate = 0.0;
 };
+
+// write_trace_csv (io.cpp:252-260).
+inline void write_trace_csv(const std::vector<FitTraceRecord>& trace, const std::string& path) {
+  std::vector<gcpb_trace_record> recs;
+  for (const auto& t : trace)
+    recs.push_back({t.epoch, t.loss_estimate, t.learning_rate, t.seconds, t.accepted ? 1 : 0});
+  check(gcpb_trace_write_csv(path.c_str(), recs.data(), static_cast<int64_t>(recs.size())));
+}
 
 // fit_gcp_adam (src/optimizer.cpp:68-158), device-resident epochs.
 inline FitResult fit_gcp_adam(Engine& e, const LossFunction& loss, const FitConfig& cfg) {

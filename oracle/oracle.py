@@ -333,6 +333,10 @@ class Reference:
         L.ref_gen_binary.argtypes = [C.c_int, i64p, C.c_int64, C.c_double, C.c_double, C.c_double,
                                      C.c_uint64, C.POINTER(vp), f64p, u64p]
         L.ref_variance_ordering.argtypes = [f64p, f64p]
+        L.ref_write_model.argtypes = [C.c_int, i64p, C.c_int64, f64p, C.c_char_p]
+        L.ref_read_model.argtypes = [C.c_char_p, C.POINTER(C.c_int), i64p, i64p, f64p, C.c_int64]
+        L.ref_write_trace.argtypes = [C.c_char_p, C.c_int64, i64p, f64p, f64p, f64p,
+                                      C.POINTER(C.c_int)]
         L.ref_acceptance_instance.argtypes = [C.c_int, C.POINTER(vp), f64p]
         L.ref_similarity.argtypes = [C.c_int, i64p, C.c_int64, f64p, C.c_int64, f64p, f64p]
         L.ref_read_tns.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(C.c_int), i64p]
@@ -425,6 +429,32 @@ class Reference:
         self._ck(self.lib.ref_similarity(len(dims), _i64(dims), r_est, _f64(Oracle.flat(est)),
                                          r_true, _f64(Oracle.flat(truth)), C.byref(out)))
         return out.value
+
+    def write_model(self, factors, path):
+        dims = np.array([len(f) for f in factors], dtype=np.int64)
+        self._ck(self.lib.ref_write_model(len(dims), _i64(dims), factors[0].shape[1],
+                                          _f64(Oracle.flat(factors)), str(path).encode()))
+
+    def read_model(self, path, cap=1 << 22):
+        d, r = C.c_int(), C.c_int64()
+        dims = np.zeros(16, dtype=np.int64)
+        flat = np.zeros(cap)
+        self._ck(self.lib.ref_read_model(str(path).encode(), C.byref(d), _i64(dims), C.byref(r),
+                                         _f64(flat), cap))
+        out, at = [], 0
+        for n in dims[:d.value]:
+            out.append(flat[at:at + n * r.value].reshape(n, r.value).copy())
+            at += n * r.value
+        return out
+
+    def write_trace(self, path, epoch, loss, lr, secs, accepted):
+        n = len(epoch)
+        acc = (C.c_int * max(n, 1))(*[int(a) for a in accepted])
+        self._ck(self.lib.ref_write_trace(str(path).encode(), n,
+                                          _i64(np.asarray(epoch, dtype=np.int64)),
+                                          _f64(np.asarray(loss, dtype=np.float64)),
+                                          _f64(np.asarray(lr, dtype=np.float64)),
+                                          _f64(np.asarray(secs, dtype=np.float64)), acc))
 
     def read_tns(self, path):
         h, d, dims = C.c_void_p(), C.c_int(), np.zeros(16, dtype=np.int64)

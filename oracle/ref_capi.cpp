@@ -363,6 +363,35 @@ int ref_read_dense(const char* path, void** out, int* d, std::int64_t* dims) {
 int ref_write_dense(void* h, const char* path) {
   return guard([&] { gcp::write_dense(*static_cast<TensorH*>(h)->dense, path); });
 }
+int ref_write_model(int d, const std::int64_t* dims, std::int64_t r, const double* factors,
+                    const char* path) {
+  return guard([&] { gcp::write_model(make_model(d, dims, r, factors), path); });
+}
+int ref_read_model(const char* path, int* d, std::int64_t* dims, std::int64_t* r,
+                   double* factors, std::int64_t cap) {
+  return guard([&] {
+    const gcp::KruskalModel m = gcp::read_model(path);
+    *d = m.ndims();
+    *r = m.rank();
+    std::int64_t n = 0;
+    for (int k = 0; k < m.ndims(); ++k) {
+      dims[k] = m.shape().dim(k);
+      n += dims[k] * m.rank();
+    }
+    if (n > cap) throw std::length_error("ref_read_model: capacity");
+    flatten_model(m, factors);
+  });
+}
+int ref_write_trace(const char* path, std::int64_t n, const std::int64_t* epoch,
+                    const double* loss, const double* lr, const double* secs,
+                    const int* accepted) {
+  return guard([&] {
+    gcp::FitTrace t;
+    for (std::int64_t i = 0; i < n; ++i)
+      t.records.push_back({epoch[i], loss[i], lr[i], secs[i], accepted[i] != 0});
+    gcp::write_trace_csv(t, path);
+  });
+}
 int ref_dense_export(void* h, double* out) {
   return guard([&] {
     const auto v = static_cast<TensorH*>(h)->dense->values();

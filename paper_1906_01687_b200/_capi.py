@@ -165,6 +165,10 @@ SIGNATURES = [
     ("gcpb_dense_shape", C.c_int, [C.c_char_p, i32p, i64p]),
     ("gcpb_dense_read", C.c_int, [C.c_char_p, C.c_int64, f64p]),
     ("gcpb_dense_write", C.c_int, [C.c_char_p, C.c_int, i64p, f64p]),
+    ("gcpb_model_read_header", C.c_int, [C.c_char_p, i32p, i64p, i64p]),
+    ("gcpb_model_read", C.c_int, [C.c_char_p, f64p]),
+    ("gcpb_model_write", C.c_int, [C.c_char_p, C.c_int, i64p, C.c_int64, f64p]),
+    ("gcpb_trace_write_csv", C.c_int, [C.c_char_p, C.POINTER(gcpb_trace_record), C.c_int64]),
     ("gcpb_philox_bounded", C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                          C.c_uint64]),
     ("gcpb_zero_batch_size", C.c_int64, [C.c_double, C.c_double, C.c_double, C.c_int64]),

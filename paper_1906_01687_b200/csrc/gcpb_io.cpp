@@ -635,6 +635,67 @@ std::vector<int64_t> dense_shape(const std::string& path) {
   return dims;
 }
 
+// ---- model text files (io.cpp:153-193) and the trace CSV (io.cpp:252-260) ----
+// A cursor over a whole file with the two extraction rules read_model uses:
+// `in >> int64` (skip whitespace, sign + digits, stop at the first non-digit)
+// and `in >> string` (skip whitespace, read to the next whitespace).
+struct Cursor {
+  const char* p;
+  const char* e;
+  void skip() {
+    while (p < e && is_ws(*p)) ++p;
+  }
+  bool int64(int64_t* out) {
+    skip();
+    const char* q = p;
+    bool neg = false;
+    if (q < e && (*q == '+' || *q == '-')) neg = *q++ == '-';
+    const char* d0 = q;
+    unsigned long long v = 0;
+    bool overflow = false;
+    for (; q < e && *q >= '0' && *q <= '9'; ++q) {
+      const unsigned dig = static_cast<unsigned>(*q - '0');
+      if (v > (0xffffffffffffffffull - dig) / 10) overflow = true;
+      v = v * 10 + dig;
+    }
+    if (q == d0) return false;
+    const unsigned long long lim = neg ? (1ull << 63) : (1ull << 63) - 1;
+    if (overflow || v > lim) return false;
+    *out = neg ? static_cast<int64_t>(0 - v) : static_cast<int64_t>(v);
+    p = q;
+    return true;
+  }
+  bool token(Token* t) {
+    skip();
+    if (p == e) return false;
+    const char* q = p;
+    while (q < e && !is_ws(*q)) ++q;
+    *t = {p, q};
+    p = q;
+    return true;
+  }
+};
+
+struct ModelHeader {
+  int64_t d = 0, r = 0;
+  std::vector<int64_t> dims;
+};
+
+ModelHeader read_model_header(const std::string& path, Cursor& c) {
+  ModelHeader h;
+  if (!c.int64(&h.d) || !c.int64(&h.r)) fail(path, "bad header: expected mode count and rank");
+  if (h.d < 1 || h.r < 1) fail(path, "bad header: mode count and rank must be >= 1");
+  if (h.d > kMaxModes)
+    throw std::invalid_argument("Shape: at most " + std::to_string(kMaxModes) +
+                                " modes supported");
+  h.dims.resize(static_cast<size_t>(h.d));
+  for (auto& n : h.dims)
+    if (!c.int64(&n)) fail(path, "bad header: missing extents");
+  for (int64_t n : h.dims)  // KruskalModel(factors) -> Shape (shape.cpp:38-39)
+    if (n < 1) throw std::invalid_argument("Shape: every extent must be positive");
+  return h;
+}
+
 }  // namespace
 
 extern "C" {
@@ -725,4 +786,80 @@ int gcpb_dense_write(const char* path, int d, const int64_t* dims, const double*
   });
 }
 
+int gcpb_model_read_header(const char* path, int* d, int64_t* dims, int64_t* rank) {
+  return io_guard([&] {
+    if (!path || !d || !dims || !rank) throw std::invalid_argument("gcpb_model_read_header: null");
+    Mapped m(path);
+    Cursor c{m.p, m.p + m.n};
+    const ModelHeader h = read_model_header(path, c);
+    *d = static_cast<int>(h.d);
+    *rank = h.r;
+    for (int64_t k = 0; k < h.d; ++k) dims[k] = h.dims[static_cast<size_t>(k)];
+  });
+}
+
+int gcpb_model_read(const char* path, double* factors) {
+  return io_guard([&] {
+    if (!path || !factors) throw std::invalid_argument("gcpb_model_read: null");
+    Mapped m(path);
+    Cursor c{m.p, m.p + m.n};
+    const ModelHeader h = read_model_header(path, c);
+    int64_t n = 0;
+    for (int64_t k : h.dims) n += k * h.r;
+    for (int64_t i = 0; i < n; ++i) {
+      Token t{};
+      if (!c.token(&t)) fail(path, "truncated factor data");
+      if (!parse_double(t, factors + i))  // parse_double(tok, path, 0) (io.cpp:172)
+        throw io_error(std::string(path) + ":0: expected a number, got '" + t.str() + "'");
+    }
+  });
+}
+
+int gcpb_model_write(const char* path, int d, const int64_t* dims, int64_t rank,
+                     const double* factors) {
+  return io_guard([&] {
+    if (!path || !dims || !factors || d < 1 || rank < 1)
+      throw std::invalid_argument("gcpb_model_write: bad argument");
+    std::string out = std::to_string(d) + " " + std::to_string(rank) + "\n";
+    for (int k = 0; k < d; ++k) out += std::to_string(dims[k]) + (k + 1 < d ? " " : "\n");
+    char buf[40];
+    const double* f = factors;
+    for (int k = 0; k < d; ++k)
+      for (int64_t i = 0; i < dims[k]; ++i)
+        for (int64_t j = 0; j < rank; ++j) {
+          out.append(buf, static_cast<size_t>(fmt17(buf, *f++)));
+          out += j + 1 < rank ? ' ' : '\n';
+        }
+    FILE* fp = std::fopen(path, "wb");
+    if (!fp) fail(path, "cannot open for writing");
+    bool ok = std::fwrite(out.data(), 1, out.size(), fp) == out.size();
+    ok = (std::fclose(fp) == 0) && ok;
+    if (!ok) fail(path, "write error");
+  });
+}
+
+int gcpb_trace_write_csv(const char* path, const gcpb_trace_record* recs, int64_t n) {
+  return io_guard([&] {
+    if (!path || (n > 0 && !recs)) throw std::invalid_argument("gcpb_trace_write_csv: null");
+    std::string out = "epoch,loss_estimate,learning_rate,seconds,accepted\n";
+    char buf[40];
+    for (int64_t i = 0; i < n; ++i) {
+      const gcpb_trace_record& t = recs[i];
+      out += std::to_string(t.epoch) + ',';
+      out.append(buf, static_cast<size_t>(fmt17(buf, t.loss_estimate)));
+      out += ',';
+      out.append(buf, static_cast<size_t>(fmt17(buf, t.learning_rate)));
+      out += ',';
+      out.append(buf, static_cast<size_t>(fmt17(buf, t.seconds)));
+      out += t.accepted ? ",1\n" : ",0\n";
+    }
+    FILE* fp = std::fopen(path, "wb");
+    if (!fp) fail(path, "cannot open for writing");
+    bool ok = std::fwrite(out.data(), 1, out.size(), fp) == out.size();
+    ok = (std::fclose(fp) == 0) && ok;
+    if (!ok) fail(path, "write error");
+  });
+}
+
 }  // extern "C"
+

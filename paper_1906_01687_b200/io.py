@@ -119,6 +119,43 @@ def write_dense(dims: Sequence[int], values, path: str | os.PathLike) -> None:
                                 vals.ctypes.data_as(_capi.f64p)))
 
 
+def read_model(path: str | os.PathLike):
+    """read_model (io.cpp:153-177) -> list of n_k x r factor matrices."""
+    d = C.c_int32()
+    dims = np.zeros(16, dtype=np.int64)
+    r = C.c_int64()
+    _check(lib.gcpb_model_read_header(os.fsencode(path), C.byref(d), dims.ctypes.data_as(_capi.i64p),
+                                      C.byref(r)))
+    dims = [int(n) for n in dims[:d.value]]
+    flat = np.zeros(sum(dims) * r.value)
+    _check(lib.gcpb_model_read(os.fsencode(path), flat.ctypes.data_as(_capi.f64p)))
+    out, at = [], 0
+    for n in dims:
+        out.append(flat[at:at + n * r.value].reshape(n, r.value).copy())
+        at += n * r.value
+    return out
+
+
+def write_model(factors, path: str | os.PathLike) -> None:
+    """write_model (io.cpp:179-193): %.17g values, bit-exact round trip."""
+    factors = [np.ascontiguousarray(f, dtype=np.float64) for f in factors]
+    dims = np.array([f.shape[0] for f in factors], dtype=np.int64)
+    r = factors[0].shape[1]
+    flat = np.concatenate([f.reshape(-1) for f in factors])
+    _check(lib.gcpb_model_write(os.fsencode(path), len(dims), dims.ctypes.data_as(_capi.i64p), r,
+                                flat.ctypes.data_as(_capi.f64p)))
+
+
+def write_trace_csv(trace, path: str | os.PathLike) -> None:
+    """write_trace_csv (io.cpp:252-260) from FitResult.trace records."""
+    arr = (_capi.gcpb_trace_record * max(len(trace), 1))()
+    for i, t in enumerate(trace):
+        arr[i].epoch, arr[i].loss_estimate = int(t.epoch), float(t.loss_estimate)
+        arr[i].learning_rate, arr[i].seconds = float(t.learning_rate), float(t.seconds)
+        arr[i].accepted = 1 if t.accepted else 0
+    _check(lib.gcpb_trace_write_csv(os.fsencode(path), arr, len(trace)))
+
+
 def engine_from_file(path: str | os.PathLike, rank: int, dtype: str = "f64", device: int = 0,
                      storage: Optional[str] = None) -> Engine:
     """Load a .tns / GCPBCOO1 / dense file straight into a device engine."""

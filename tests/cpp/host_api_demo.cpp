@@ -75,6 +75,10 @@ int main() {
   const auto res = gcpb::fit_gcp_adam(e, gcpb::LossFunction::bernoulli_odds(), cfg);
   EXPECT(!res.trace.empty() && res.trace.front().epoch == 0);
   EXPECT(res.final_loss_estimate <= res.trace.front().loss_estimate);
+  gcpb::write_trace_csv(res.trace, "/tmp/gcpb_demo_trace.csv");
+  gcpb::write_model(res.model, dims, r, "/tmp/gcpb_demo.model");
+  std::vector<int64_t> mdims;
+  EXPECT(gcpb::read_model("/tmp/gcpb_demo.model", &mdims) == res.model && mdims == dims);
   // .tns round trip through the native reader/writer
   gcpb::CooTensor t{dims, coords, vals};
   gcpb::write_tns(t, "/tmp/gcpb_demo.tns");

@@ -228,3 +228,50 @@ def test_dense_roundtrip_matches_reference(ref, tmp_path):
         with pytest.raises(O.RefError) as theirs:
             ref.read_dense(q)
         assert _msg(ours.value) == _msg(theirs.value)
+
+
+# ---- model text files and the trace CSV (io.cpp:153-193, 252-260) ----------
+def test_model_files_match_reference(ref, tmp_path):
+    io = IO()
+    rs = np.random.default_rng(4)
+    F = [rs.normal(size=(n, 3)) * 10.0 ** rs.integers(-30, 30, (n, 3)) for n in (5, 4, 6)]
+    p, q = tmp_path / "ours.model", tmp_path / "ref.model"
+    io.write_model(F, p)
+    ref.write_model(F, q)
+    assert p.read_bytes() == q.read_bytes()
+    for got, want in zip(io.read_model(q), F):
+        assert np.array_equal(got, want)  # %.17g round trip is bit-exact
+    for got, want in zip(ref.read_model(p), F):
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name,text", [
+    ("no_header", ""),
+    ("bad_header", "3 x\n"),
+    ("zero_rank", "2 0\n3 4\n"),
+    ("missing_dims", "2 1\n3\n"),
+    ("truncated", "2 1\n2 2\n1.0 2.0 3.0\n"),
+    ("bad_number", "1 2\n2\n1.0 2.0\n3.0 nope\n"),
+])
+def test_model_read_errors_match_reference(ref, tmp_path, name, text):
+    p = tmp_path / f"{name}.model"
+    p.write_text(text)
+    g = G()
+    with pytest.raises(g.GcpError) as ours:
+        IO().read_model(p)
+    with pytest.raises(O.RefError) as theirs:
+        ref.read_model(p)
+    assert _msg(ours.value) == _msg(theirs.value)
+
+
+def test_trace_csv_matches_reference(ref, tmp_path):
+    from paper_1906_01687_b200.fit import FitTraceRecord
+    rs = np.random.default_rng(5)
+    recs = [FitTraceRecord(i, float(rs.normal() * 1e5), 0.01 * 0.1 ** (i // 3),
+                           float(rs.random()), bool(i % 4)) for i in range(12)]
+    p, q = tmp_path / "ours.csv", tmp_path / "ref.csv"
+    IO().write_trace_csv(recs, p)
+    ref.write_trace(q, [t.epoch for t in recs], [t.loss_estimate for t in recs],
+                    [t.learning_rate for t in recs], [t.seconds for t in recs],
+                    [t.accepted for t in recs])
+    assert p.read_bytes() == q.read_bytes()
