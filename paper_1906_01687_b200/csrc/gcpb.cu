@@ -203,6 +203,15 @@ struct gcpb_ctx {
   uint64_t hmask = 0;
   bool hash_ready = false;
   int domain_flags = -1;  // cached domain scan of the stored data
+  // hot rows (FusedArgs::hslot / Ghot): selected from the nonzeros' per-mode
+  // row counts on the first sparse scatter after the tensor changes
+  DBuf hslot, Ghot, hot_off;
+  int64_t hot_version = -1;  // tensor_version the selection belongs to
+  int hot_n = 0;             // hot rows over all modes
+  int hot_rh_cap = 0;        // copies allocated per hot row
+  uint32_t hot_base[kMaxModes + 1] = {};
+  uint32_t row_base[kMaxModes + 1] = {};
+  double hot_fmax[kMaxModes] = {};  // largest share of the nonzeros in one row, per mode
 
   // fused-kernel event timing (gcpb_kernel_timing)
   bool timing = false;
@@ -588,6 +597,111 @@ int replicas_for(const gcpb_ctx* c, int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, c->nrep_cap)));
 }
 
+// Hot-row selection: per mode, up to kHotRows rows holding at
+// least 1/1024 of the nonzeros each, from a device histogram of the records.
+constexpr int kHotRows = 32;
+constexpr int kHotCopiesMax = 256;
+
+void ensure_hot(gcpb_ctx* c) {
+  if (c->hot_version == c->tensor_version) return;
+  c->hot_version = c->tensor_version;
+  c->hot_n = 0;
+  if (c->tensor_kind != 2 || c->nnz <= 0 || c->d > 4) return;
+  int64_t rows = 0;
+  for (int k = 0; k < c->d; ++k) {
+    c->row_base[k] = static_cast<uint32_t>(rows);
+    rows += c->dims[k];
+  }
+  if (rows >= (int64_t{1} << 31)) return;
+  c->row_base[c->d] = static_cast<uint32_t>(rows);
+  DBuf hist;
+  hist.alloc(static_cast<size_t>(rows) * sizeof(uint32_t));
+  CK(cudaMemsetAsync(hist.p, 0, static_cast<size_t>(rows) * sizeof(uint32_t), c->stream));
+  RowBase rb;
+  std::memset(&rb, 0, sizeof(rb));
+  for (int k = 0; k < c->d; ++k) rb.v[k] = c->row_base[k];
+  row_hist_kernel<<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
+      c->nzrec.as<uint32_t>(), c->rec_words, static_cast<int>(c->tsize / 4), c->nnz, c->d, rb,
+      hist.as<uint32_t>());
+  CK(cudaGetLastError());
+  std::vector<uint32_t> h(static_cast<size_t>(rows));
+  CK(cudaMemcpyAsync(h.data(), hist.p, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<uint8_t> slot(static_cast<size_t>(rows), 0xFF);
+  std::vector<int64_t> hoff;
+  const double nnz = static_cast<double>(c->nnz);
+  for (int k = 0; k < c->d; ++k) {
+    c->hot_base[k] = static_cast<uint32_t>(hoff.size());
+    c->hot_fmax[k] = 0.0;
+    std::vector<std::pair<uint32_t, uint32_t>> cand;  // (count, row)
+    for (int64_t i = 0; i < c->dims[k]; ++i) {
+      const uint32_t n = h[c->row_base[k] + i];
+      if (static_cast<double>(n) * 1024.0 >= nnz) cand.emplace_back(n, static_cast<uint32_t>(i));
+    }
+    const size_t keep = std::min<size_t>(cand.size(), kHotRows);
+    std::partial_sort(cand.begin(), cand.begin() + keep, cand.end(),
+                      [](const auto& x, const auto& y) {
+                        return x.first != y.first ? x.first > y.first : x.second < y.second;
+                      });
+    for (size_t j = 0; j < keep; ++j) {
+      slot[c->row_base[k] + cand[j].second] = static_cast<uint8_t>(j);
+      hoff.push_back(c->off[k] + static_cast<int64_t>(cand[j].second) * c->rp);
+    }
+    if (keep > 0) c->hot_fmax[k] = static_cast<double>(cand[0].first) / nnz;
+  }
+  c->hot_base[c->d] = static_cast<uint32_t>(hoff.size());
+  c->hot_n = static_cast<int>(hoff.size());
+  if (c->hot_n == 0) return;
+  // copies per hot row: up to kHotCopiesMax within 8 MB (the copies stay in L2)
+  const int64_t row_bytes = c->rp * static_cast<int64_t>(c->tsize);
+  int cap = kHotCopiesMax;
+  while (cap > 2 && static_cast<int64_t>(cap) * c->hot_n * row_bytes > (int64_t{8} << 20)) cap >>= 1;
+  c->hot_rh_cap = cap;
+  c->hslot.alloc(slot.size());
+  CK(cudaMemcpyAsync(c->hslot.p, slot.data(), slot.size(), cudaMemcpyHostToDevice, c->stream));
+  c->hot_off.alloc(hoff.size() * sizeof(int64_t));
+  CK(cudaMemcpyAsync(c->hot_off.p, hoff.data(), hoff.size() * sizeof(int64_t),
+                     cudaMemcpyHostToDevice, c->stream));
+  const size_t gbytes = static_cast<size_t>(cap) * c->hot_n * row_bytes;
+  c->Ghot.alloc(gbytes);
+  CK(cudaMemsetAsync(c->Ghot.p, 0, gbytes, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // host vectors die here
+}
+
+// Copies per hot row for one scatter (0 = hot rows off): the busiest row's
+// expected reductions per step, picks at the mode's largest nonzero share
+// plus its share of the unrestricted draws, over a target of kHotTarget
+// reductions per address (GCPB_HOT_T), when that beats the block replicas.
+template <typename T>
+int hot_copies(gcpb_ctx* c, const FusedArgs<T>& a, int nrep) {
+  static const double target = [] {
+    const char* e = getenv("GCPB_HOT_T");
+    return e ? atof(e) : 256.0;
+  }();
+  if (target <= 0.0 || c->tensor_kind != 2 || c->d > 4) return 0;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (cs == cudaStreamCaptureStatusNone)
+    ensure_hot(c);
+  else if (c->hot_version != c->tensor_version)
+    return 0;
+  if (c->hot_n == 0) return 0;
+  double picks = 0.0, unif = 0.0;
+  for (int s = 0; s < a.nseg; ++s) {
+    const double len = static_cast<double>(std::max<int64_t>(0, a.seg[s].t_end - a.seg[s].t_begin));
+    if (a.seg[s].kind == SEG_PICK) picks += len;
+    else if (a.seg[s].kind <= SEG_ZERO_LIST) unif += len;
+    else return 0;
+  }
+  double load = 0.0;
+  for (int k = 0; k < c->d; ++k)
+    load = std::max(load, picks * c->hot_fmax[k] + unif / static_cast<double>(c->dims[k]));
+  int rh = 1;
+  while (rh < c->hot_rh_cap && static_cast<double>(rh) * target < load) rh <<= 1;
+  return rh > nrep ? rh : 0;
+}
+
 template <typename T>
 void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   const int64_t tiles = finish_segments(a);
@@ -613,12 +727,30 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     c->nrep = replicas_for(c, n);
     a.nrep = c->nrep;
     a.G = c->nrep > 1 ? c->Grep.as<T>() : c->Gr.as<T>();
+    if (!record) {
+      a.rh = hot_copies<T>(c, a, c->nrep);
+      if (a.rh > 0) {
+        a.hslot = c->hslot.as<uint8_t>();
+        a.Ghot = c->Ghot.as<T>();
+        for (int k = 0; k < c->d; ++k) {
+          a.rowbase[k] = c->row_base[k];
+          a.hbase[k] = c->hot_base[k];
+        }
+      }
+    }
   }
-  CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms));
+  bool used_hot = false;
+  CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot));
   if (ev1) CK(cudaEventRecord(ev1, c->stream));
   if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
     grad_reduce_kernel<T><<<grid_for(c->nelem, 256, c->num_sms, 4), 256, 0, c->stream>>>(
         c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride);
+    CK(cudaGetLastError());
+  }
+  if (used_hot) {  // hot rows' copies into the gradient (or replica 0 when Adam folds)
+    hot_fold_kernel<T><<<c->hot_n, 256, 0, c->stream>>>(
+        c->Ghot.as<T>(), a.rh, static_cast<int>(c->rp), c->hot_off.as<int64_t>(),
+        (fold && c->nrep > 1) ? c->Grep.as<T>() : c->Gr.as<T>());
     CK(cudaGetLastError());
   }
 }
@@ -1313,6 +1445,7 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
   } else if (sk->strategy == GCPB_UNIFORM && c->tensor_kind == 2) {
     ensure_hash(c);
   }
+  if (c->tensor_kind == 2) ensure_hot(c);  // host work: not inside the capture
   set_rng_iter(c, iter0);
   if (small_eligible<T>(c, sk)) {
     small_launch<T>(c, sk, loss, seed, n);

@@ -516,6 +516,91 @@ __global__ void grad_reduce_kernel(T* __restrict__ G, T* __restrict__ reps, int6
   }
 }
 
+// ---------------------------------------------------------------------------
+// Hot rows (FusedArgs::hslot / Ghot)
+// ---------------------------------------------------------------------------
+struct RowBase {
+  uint32_t v[kMaxModes];
+};
+
+// Per-mode row counts of the stored nonzeros (hist[rowbase[k] + i_k]).  Lanes
+// holding the same row are merged with match.any first, so a Zipf-hot row
+// costs one atomic per warp instead of up to 32.
+__global__ void row_hist_kernel(const uint32_t* __restrict__ rec, int rec_words, int vwd,
+                                int64_t n, int d, RowBase rb, uint32_t* __restrict__ hist) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += stride) {
+    const uint32_t* r = rec + e * rec_words + vwd;
+    for (int k = 0; k < d; ++k) {
+      const uint32_t key = rb.v[k] + __ldg(r + k);
+      const unsigned peers = __match_any_sync(__activemask(), key);
+      if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
+        atomicAdd(hist + key, static_cast<uint32_t>(__popc(peers)));
+    }
+  }
+}
+
+// Coherent (non-__ldg) 16-byte loads: the fold reads data it then re-zeroes.
+__device__ __forceinline__ Vec<float> ld_chunk_rw(const float* p) {
+  const float4 q = *reinterpret_cast<const float4*>(p);
+  return Vec<float>{{q.x, q.y, q.z, q.w}};
+}
+__device__ __forceinline__ Vec<double> ld_chunk_rw(const double* p) {
+  const double2 q = *reinterpret_cast<const double2*>(p);
+  return Vec<double>{{q.x, q.y}};
+}
+
+// G[row of slot] += sum of the slot's rh copies; copies re-zeroed.  One block
+// per hot row: thread (j, c) sums copies j, j+J, ... of 16-byte chunk c, then
+// the J partial chunks are combined in shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int rh, int rp,
+                                                       const int64_t* __restrict__ hot_off,
+                                                       T* __restrict__ G) {
+  constexpr int VW = Vec<T>::W;
+  __shared__ Vec<T> part[256];
+  const int ch = rp / VW;  // chunks per padded row
+  const int J = blockDim.x / ch;
+  const int c = threadIdx.x % ch;
+  const int j0 = threadIdx.x / ch;
+  Vec<T> acc;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) acc.v[e] = static_cast<T>(0);
+  if (j0 < J) {
+    T* base = Ghot + static_cast<int64_t>(blockIdx.x) * rh * rp + c * VW;
+    int j = j0;
+    for (; j + 3 * J < rh; j += 4 * J) {  // four copies in flight
+      Vec<T> x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = ld_chunk_rw(base + (j + u * J) * rp);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc.v[e] += x[u].v[e];
+        store_chunk(base + (j + u * J) * rp, Vec<T>{});
+      }
+    }
+    for (; j < rh; j += J) {
+      const Vec<T> x = ld_chunk_rw(base + j * rp);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) acc.v[e] += x.v[e];
+      store_chunk(base + j * rp, Vec<T>{});
+    }
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < ch) {
+    for (int j = 1; j < J; ++j) {
+#pragma unroll
+      for (int e = 0; e < VW; ++e) acc.v[e] += part[j * ch + c].v[e];
+    }
+    T* g = G + hot_off[blockIdx.x] + c * VW;
+#pragma unroll
+    for (int e = 0; e < VW; ++e) g[e] += acc.v[e];
+  }
+}
+
 template <typename T>
 struct ModelDesc {
   const T* A;

@@ -42,6 +42,10 @@
 #ifndef GCPB_MINB_SLIM
 #define GCPB_MINB_SLIM 4
 #endif
+// Same for the slim hot-row variants (one more live register per sample).
+#ifndef GCPB_MINB_HOT
+#define GCPB_MINB_HOT 3
+#endif
 
 namespace gcpb {
 
@@ -52,6 +56,7 @@ struct Drawn {
   double w;
   int flag;
   double yg;
+  uint32_t hs;  // hot slot per mode (8 bits each, 0xFF = not hot); HOT kernels only
 };
 
 // Segment fields of one tile, resolved once (not per pass).
@@ -84,11 +89,12 @@ __device__ __forceinline__ SegRegs seg_of(const FusedArgs<T>& a, int64_t tile) {
 }
 
 // Phase A: lane-per-sample draw of ordinal t of segment sg.
-template <typename T, int DM, bool EXACT, bool GV = true>
+template <typename T, int DM, bool EXACT, bool GV = true, bool HOT = false>
 __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg, int64_t t,
                                         uint64_t iter, uint32_t (&ik)[DM], Drawn<T>& s) {
   const int d = EXACT ? DM : a.d;
   s.valid = t < sg.t_end;
+  if (HOT) s.hs = 0xFFFFFFFFu;
   s.x = static_cast<T>(0);
   if (GV) {
     s.w = sg.weight;
@@ -251,6 +257,14 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
       s.flag = a.g_flag ? a.g_flag[t] : 0;
     }
   }
+  if (HOT && s.valid) {
+    static_assert(!HOT || DM <= 4, "hot-row slots pack 8 bits per mode");
+    uint32_t hs = 0;
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+      hs |= static_cast<uint32_t>(__ldg(a.hslot + a.rowbase[k] + ik[k])) << (8 * k);
+    s.hs = hs | (DM < 4 ? (0xFFFFFFFFu << (8 * DM)) : 0u);
+  }
   // Factor tables larger than L2 (C5: 531 MB): pull this sample's rows (and
   // its gradient rows, so the reductions hit L2) in while the previous tile
   // computes.  Rows are 32-byte aligned; one line prefetch per 128 bytes.
@@ -268,10 +282,24 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
-template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, bool GV>
+// Reduction target of one (mode, row): the hot-row copy rsel of the row's
+// slot when it is hot, else the block's gradient replica.
+template <typename T, bool HOT>
+__device__ __forceinline__ T* grad_row(const FusedArgs<T>& a, T* Gb, uint32_t roff, uint32_t hsv,
+                                       int k, uint32_t rsel) {
+  if (HOT) {
+    const uint32_t sl = (hsv >> (8 * k)) & 0xFFu;
+    if (sl != 0xFFu)
+      return a.Ghot + ((a.hbase[k] + sl) * static_cast<uint32_t>(a.rh) + rsel) *
+                          static_cast<uint32_t>(a.rp);
+  }
+  return Gb + roff;
+}
+
+template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, bool GV, bool HOT = false>
 __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg, int64_t tile,
                                         const uint32_t (&ik)[DM], const Drawn<T>& s,
-                                        T* __restrict__ Gb) {
+                                        T* __restrict__ Gb, uint32_t rsel = 0) {
   constexpr int VW = Vec<T>::W;
   constexpr int NGRP = 32 / G;
   constexpr int SL = VPL * VW;  // elements of one lane's row slice
@@ -302,6 +330,7 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
     for (int k = 0; k < DM; ++k) ii[k] = __shfl_sync(FULL, ik[k], src);
     const T xv = __shfl_sync(FULL, s.x, src);
+    const uint32_t hsv = HOT ? __shfl_sync(FULL, s.hs, src) : 0xFFFFFFFFu;
     T wv = wseg;
     double wd = sg.weight;
     int fv = sg.flag;
@@ -389,13 +418,14 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
       for (int k = DM - 1; k >= 0; --k) {
         const bool mk = EXACT || k < d;
+        T* gk = grad_row<T, HOT>(a, Gb, roff[k], hsv, k, rsel);
 #pragma unroll
         for (int c = 0; c < VPL; ++c) {
           T out[VW];
 #pragma unroll
           for (int e = 0; e < VW; ++e) out[e] = y * (pre[k][c * VW + e] * suf[c * VW + e]);
           if (act && mk && cmask[c] != static_cast<T>(0))
-            red_chunk(Gb + roff[k] + cidx[c] * VW, out);
+            red_chunk(gk + cidx[c] * VW, out);
         }
 #pragma unroll
         for (int e = 0; e < SL; ++e) suf[e] = suf[e] * row[k][e];
@@ -404,7 +434,8 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
-template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true>
+template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true,
+          bool HOT = false>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
                                                                int64_t total_tiles) {
   const int lane = threadIdx.x & 31;
@@ -418,9 +449,10 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
   if (tile >= total_tiles) return;
   uint32_t ik[DM];
   Drawn<T> s;
+  const uint32_t rsel = HOT ? static_cast<uint32_t>(warp0) & static_cast<uint32_t>(a.rh - 1) : 0u;
   SegRegs sg = seg_of<T>(a, tile);
-  phase_a<T, DM, EXACT, GV>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik,
-                            s);
+  phase_a<T, DM, EXACT, GV, HOT>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter,
+                                 ik, s);
   for (; tile < total_tiles; tile += nwarps) {
     const int64_t next = tile + nwarps;
     uint32_t ik2[DM];
@@ -428,14 +460,15 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
     SegRegs sg2 = sg;
     if (next < total_tiles) {  // prefetch: next tile's draws + tensor gathers in flight
       sg2 = seg_of<T>(a, next);
-      phase_a<T, DM, EXACT, GV>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, iter,
-                                ik2, s2);
+      phase_a<T, DM, EXACT, GV, HOT>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane,
+                                     iter, ik2, s2);
     } else {
       s2.valid = false;
+      if (HOT) s2.hs = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
-    phase_b<T, DM, EXACT, G, VPL, REC, GV>(a, sg, tile, ik, s, Gb);
+    phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT>(a, sg, tile, ik, s, Gb, rsel);
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
     s = s2;
@@ -453,7 +486,7 @@ inline int pow2ceil(int v) {
 
 template <typename T, int DM, bool EXACT, bool REC>
 cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
-                            int num_sms) {
+                            int num_sms, bool* used_hot) {
   const int nchunks = a.nchunks;
   int G = pow2ceil(nchunks);
   int vpl = 1;
@@ -481,6 +514,19 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
   if (vpl == 1) {
     if constexpr (!REC && EXACT) {
       if (!given) {  // hot path: no host-given samples -> slim live state
+        if constexpr (DM <= 4) {
+          if (a.rh > 0) {  // hot rows privatized (sparse, skewed modes)
+            *used_hot = true;
+            switch (G) {
+              case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, GCPB_MINB_HOT, false, true>);
+              case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, GCPB_MINB_HOT, false, true>);
+              case 4: return go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, GCPB_MINB_HOT, false, true>);
+              case 8: return go(fused_grad_kernel<T, DM, EXACT, 8, 1, REC, GCPB_MINB_HOT, false, true>);
+              case 16: return go(fused_grad_kernel<T, DM, EXACT, 16, 1, REC, GCPB_MINB_HOT, false, true>);
+              default: return go(fused_grad_kernel<T, DM, EXACT, 32, 1, REC, GCPB_MINB_HOT, false, true>);
+            }
+          }
+        }
         switch (G) {
           case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, GCPB_MINB_SLIM, false>);
           case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, GCPB_MINB_SLIM, false>);
@@ -553,10 +599,11 @@ __device__ __forceinline__ void stage_rows(const FusedArgs<T>& a, T* slot,
   cp_async_commit();
 }
 
-template <typename T, int DM, int G>
+template <typename T, int DM, int G, bool HOT = false>
 __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegRegs& sg,
                                                const T* wbuf, const Drawn<T>& s,
-                                               const uint32_t (&ik)[DM], T* __restrict__ Gb) {
+                                               const uint32_t (&ik)[DM], T* __restrict__ Gb,
+                                               uint32_t rsel = 0) {
   constexpr int VW = Vec<T>::W;
   constexpr int NGRP = 32 / G;
   constexpr unsigned FULL = 0xffffffffu;
@@ -577,6 +624,7 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
 #pragma unroll
     for (int k = 0; k < DM; ++k) ii[k] = __shfl_sync(FULL, ik[k], src);
     const T xv = __shfl_sync(FULL, s.x, src);
+    const uint32_t hsv = HOT ? __shfl_sync(FULL, s.hs, src) : 0xFFFFFFFFu;
     T wv = wseg;
     int fv = sg.flag;
     if (given) {
@@ -628,7 +676,10 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
           out[e] = y * (pre[k][e] * suf[e]);
           suf[e] = suf[e] * row[k][e];
         }
-        T* gp = Gb + static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.rp) +
+        T* gp = grad_row<T, HOT>(a, Gb,
+                                 static_cast<uint32_t>(a.off[k]) +
+                                     ii[k] * static_cast<uint32_t>(a.rp),
+                                 hsv, k, rsel) +
                 cidx * VW;
         if (pol)
           red_chunk_hint(gp, out, pol);
@@ -639,7 +690,7 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
   }
 }
 
-template <typename T, int DM, int G>
+template <typename T, int DM, int G, bool HOT = false>
 __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T> a,
                                                               int64_t total_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -655,8 +706,10 @@ __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T>
   if (tile >= total_tiles) return;
   uint32_t ik[DM];
   Drawn<T> s;
+  const uint32_t rsel = HOT ? static_cast<uint32_t>(warp0) & static_cast<uint32_t>(a.rh - 1) : 0u;
   SegRegs sg = seg_of<T>(a, tile);
-  phase_a<T, DM, true>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter, ik, s);
+  phase_a<T, DM, true, true, HOT>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter,
+                                  ik, s);
   int buf = 0;
   stage_rows<T, DM>(a, wbuf + (buf * 32 + lane) * slot_elems, ik, s.valid, seg_policy(a, sg.kind));
   for (; tile < total_tiles; tile += nwarps) {
@@ -666,10 +719,11 @@ __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T>
     SegRegs sg2 = sg;
     if (next < total_tiles) {
       sg2 = seg_of<T>(a, next);
-      phase_a<T, DM, true>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane, iter, ik2,
-                           s2);
+      phase_a<T, DM, true, true, HOT>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane,
+                                      iter, ik2, s2);
     } else {
       s2.valid = false;
+      if (HOT) s2.hs = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
@@ -677,7 +731,7 @@ __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T>
                       seg_policy(a, sg2.kind));
     cp_async_wait<1>();  // this tile's rows have landed; the next tile's stay in flight
     __syncwarp();
-    phase_b_staged<T, DM, G>(a, sg, wbuf + buf * 32 * slot_elems, s, ik, Gb);
+    phase_b_staged<T, DM, G, HOT>(a, sg, wbuf + buf * 32 * slot_elems, s, ik, Gb, rsel);
     __syncwarp();        // the buffer is restaged two tiles later
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
@@ -690,7 +744,7 @@ __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T>
 
 template <typename T, int DM>
 bool launch_staged(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream, int num_sms,
-                   cudaError_t* err) {
+                   cudaError_t* err, bool* used_hot) {
   const int G = pow2ceil(a.nchunks);
   const size_t smem = static_cast<size_t>(8) * 2 * 32 * DM * a.rp * sizeof(T);
   if (G > 8 || smem > 110 * 1024) return false;
@@ -706,6 +760,16 @@ bool launch_staged(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stre
     kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(a, total_tiles);
     *err = cudaGetLastError();
   };
+  if (a.rh > 0) {
+    *used_hot = true;
+    switch (G) {
+      case 1: go(fused_staged_kernel<T, DM, 1, true>); break;
+      case 2: go(fused_staged_kernel<T, DM, 2, true>); break;
+      case 4: go(fused_staged_kernel<T, DM, 4, true>); break;
+      default: go(fused_staged_kernel<T, DM, 8, true>); break;
+    }
+    return true;
+  }
   switch (G) {
     case 1: go(fused_staged_kernel<T, DM, 1>); break;
     case 2: go(fused_staged_kernel<T, DM, 2>); break;
@@ -717,32 +781,37 @@ bool launch_staged(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stre
 
 template <typename T, bool REC>
 cudaError_t launch_fused_rec(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
-                             int num_sms) {
+                             int num_sms, bool* used_hot) {
   switch (a.d) {
-    case 3: return launch_fused_dm<T, 3, true, REC>(a, total_tiles, stream, num_sms);
-    case 4: return launch_fused_dm<T, 4, true, REC>(a, total_tiles, stream, num_sms);
+    case 3: return launch_fused_dm<T, 3, true, REC>(a, total_tiles, stream, num_sms, used_hot);
+    case 4: return launch_fused_dm<T, 4, true, REC>(a, total_tiles, stream, num_sms, used_hot);
     case 1:
-    case 2: return launch_fused_dm<T, 2, false, REC>(a, total_tiles, stream, num_sms);
+    case 2: return launch_fused_dm<T, 2, false, REC>(a, total_tiles, stream, num_sms, used_hot);
     default:
-      if (a.d <= 8) return launch_fused_dm<T, 8, false, REC>(a, total_tiles, stream, num_sms);
-      return launch_fused_dm<T, 16, false, REC>(a, total_tiles, stream, num_sms);
+      if (a.d <= 8)
+        return launch_fused_dm<T, 8, false, REC>(a, total_tiles, stream, num_sms, used_hot);
+      return launch_fused_dm<T, 16, false, REC>(a, total_tiles, stream, num_sms, used_hot);
   }
 }
 
+// *used_hot reports whether the launched variant sent hot rows to a.Ghot
+// (only the hot-path variants do; the caller folds Ghot back only then).
 template <typename T>
 cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
-                         cudaStream_t stream, int num_sms) {
+                         cudaStream_t stream, int num_sms, bool* used_hot) {
+  *used_hot = false;
   if (total_tiles <= 0) return cudaSuccess;
   bool special = false;
   for (int s = 0; s < a.nseg; ++s) special = special || a.seg[s].kind >= SEG_GIVEN;
   if (!record && a.stage && !special && (a.d == 3 || a.d == 4)) {
     cudaError_t err = cudaSuccess;
-    const bool done = a.d == 3 ? launch_staged<T, 3>(a, total_tiles, stream, num_sms, &err)
-                               : launch_staged<T, 4>(a, total_tiles, stream, num_sms, &err);
+    const bool done =
+        a.d == 3 ? launch_staged<T, 3>(a, total_tiles, stream, num_sms, &err, used_hot)
+                 : launch_staged<T, 4>(a, total_tiles, stream, num_sms, &err, used_hot);
     if (done) return err;
   }
-  if (record) return launch_fused_rec<T, true>(a, total_tiles, stream, num_sms);
-  return launch_fused_rec<T, false>(a, total_tiles, stream, num_sms);
+  if (record) return launch_fused_rec<T, true>(a, total_tiles, stream, num_sms, used_hot);
+  return launch_fused_rec<T, false>(a, total_tiles, stream, num_sms, used_hot);
 }
 
 }  // namespace gcpb

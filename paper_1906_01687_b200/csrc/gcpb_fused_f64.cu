@@ -3,5 +3,6 @@
 #include "gcpb_fused.cuh"
 
 namespace gcpb {
-template cudaError_t launch_fused<double>(const FusedArgs<double>&, int64_t, bool, cudaStream_t, int);
+template cudaError_t launch_fused<double>(const FusedArgs<double>&, int64_t, bool, cudaStream_t, int,
+                                                 bool*);
 }  // namespace gcpb

@@ -109,6 +109,15 @@ struct FusedArgs {
   // evict_first (no reuse), so the nonzero picks' hot rows stay; 2 as 1 and
   // the picks' rows evict_last.
   int l2hint;
+  // Hot rows: the most frequent rows of each mode among the
+  // nonzeros (C3-C5 draw Zipf-skewed coordinates, so one row can take 12 % of
+  // all picks) receive their reductions in rh privatized copies instead of the
+  // gradient, which the L2 atomic units would otherwise serialise per address.
+  const uint8_t* hslot;         // per row: hot slot within its mode, 0xFF = not hot
+  uint32_t rowbase[kMaxModes];  // mode k's rows start at hslot + rowbase[k]
+  uint32_t hbase[kMaxModes];    // mode k's first slot in Ghot
+  T* Ghot;                      // [slot][rh][rp]
+  int rh;                       // copies per hot row (power of two); 0 = off
 };
 
 // ---------------------------------------------------------------------------
@@ -337,6 +346,6 @@ __device__ __forceinline__ int64_t hash_find(const uint64_t* __restrict__ keys, 
 // ---------------------------------------------------------------------------
 template <typename T>
 cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
-                         cudaStream_t stream, int num_sms);
+                         cudaStream_t stream, int num_sms, bool* used_hot);
 
 }  // namespace gcpb
