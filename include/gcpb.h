@@ -223,6 +223,12 @@ int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
  * chosen when uniform draws, one rank, Philox, the model fits in shared
  * memory and s*d*r <= 16384; GCPB_NO_SMALL=1 disables it). */
 int gcpb_steps_path(const gcpb_ctx* ctx);
+/* Hot rows of the sparse tensor: *rows = rows selected over
+ * all modes (the most frequent rows of each mode among the nonzeros, up to 32
+ * per mode), *copies = privatized copies per hot row used by the last fused
+ * scatter (0 = that scatter used none).  GCPB_HOT_T sets the target
+ * reductions per address (default 256; 0 disables hot rows). */
+int gcpb_hot_rows(const gcpb_ctx* ctx, int* rows, int* copies);
 /* Per-launch timing of the fused sample->MTTKRP kernel: CUDA events recorded
  * on the context's stream around each non-graph launch.  enable = 1 clears
  * and starts recording, 0 stops.  gcpb_kernel_time synchronises and returns

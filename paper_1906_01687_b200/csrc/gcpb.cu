@@ -209,6 +209,7 @@ struct gcpb_ctx {
   int64_t hot_version = -1;  // tensor_version the selection belongs to
   int hot_n = 0;             // hot rows over all modes
   int hot_rh_cap = 0;        // copies allocated per hot row
+  int hot_last = 0;          // copies used by the last fused scatter
   uint32_t hot_base[kMaxModes + 1] = {};
   uint32_t row_base[kMaxModes + 1] = {};
   double hot_fmax[kMaxModes] = {};  // largest share of the nonzeros in one row, per mode
@@ -675,10 +676,8 @@ void ensure_hot(gcpb_ctx* c) {
 // reductions per address (GCPB_HOT_T), when that beats the block replicas.
 template <typename T>
 int hot_copies(gcpb_ctx* c, const FusedArgs<T>& a, int nrep) {
-  static const double target = [] {
-    const char* e = getenv("GCPB_HOT_T");
-    return e ? atof(e) : 256.0;
-  }();
+  const char* te = getenv("GCPB_HOT_T");
+  const double target = te ? atof(te) : 256.0;
   if (target <= 0.0 || c->tensor_kind != 2 || c->d > 4) return 0;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cs);
@@ -741,6 +740,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   }
   bool used_hot = false;
   CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot));
+  if (a.scatter) c->hot_last = used_hot ? a.rh : 0;
   if (ev1) CK(cudaEventRecord(ev1, c->stream));
   if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
     grad_reduce_kernel<T><<<grid_for(c->nelem, 256, c->num_sms, 4), 256, 0, c->stream>>>(
@@ -2423,6 +2423,13 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
 }
 
 int gcpb_steps_path(const gcpb_ctx* ctx) { return ctx ? ctx->last_steps_path : -1; }
+
+int gcpb_hot_rows(const gcpb_ctx* ctx, int* rows, int* copies) {
+  if (!ctx) return GCPB_ERR_USAGE;
+  if (rows) *rows = ctx->hot_version == ctx->tensor_version ? ctx->hot_n : 0;
+  if (copies) *copies = ctx->hot_last;
+  return GCPB_OK;
+}
 
 int gcpb_synchronize(gcpb_ctx* ctx) {
   return guard(ctx, [&] { sync_and_check(ctx); });

@@ -492,6 +492,13 @@ class Engine:
         """Engine of the last run_steps: "graph" or "small" (cluster kernel)."""
         return {0: "graph", 1: "small"}.get(int(lib.gcpb_steps_path(self._h)), "unknown")
 
+    @property
+    def hot_rows(self) -> tuple:
+        """(hot rows selected, copies per hot row used by the last scatter)."""
+        rows, copies = C.c_int(), C.c_int()
+        self._ck(lib.gcpb_hot_rows(self._h, C.byref(rows), C.byref(copies)))
+        return rows.value, copies.value
+
     def adam_reset(self) -> None:
         self._ck(lib.gcpb_adam_reset(self._h))
 
