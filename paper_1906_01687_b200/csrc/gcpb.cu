@@ -678,7 +678,7 @@ template <typename T>
 int hot_copies(gcpb_ctx* c, const FusedArgs<T>& a, int nrep) {
   const char* te = getenv("GCPB_HOT_T");
   const double target = te ? atof(te) : 256.0;
-  if (target <= 0.0 || c->tensor_kind != 2 || c->d > 4) return 0;
+  if (target <= 0.0 || c->tensor_kind != 2 || c->d > 4 || c->rp / c->vw > 64) return 0;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cs);
   if (cs == cudaStreamCaptureStatusNone)

@@ -305,30 +305,51 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       block_valid += s_warp_valid[w];
     }
     const int thread_excl = warp_excl + incl - cnt;
-    if (threadIdx.x == 0) {
+    if (wid == 0) {
+      // Decoupled look-back, one warp wide: lane i inspects chunk - 1 - i;
+      // the window's aggregates up to the nearest inclusive prefix are summed
+      // in one step instead of walking predecessors one L2 round trip each.
       unsigned long long excl = 0;
       if (chunk == 0) {
-        st_release_u64(&a.status[chunk], pack_status(btag, 2u, block_total));
+        if (lane == 0) st_release_u64(&a.status[0], pack_status(btag, 2u, block_total));
       } else {
-        st_release_u64(&a.status[chunk], pack_status(btag, 1u, block_total));
-        int64_t pred = chunk - 1;
+        if (lane == 0) st_release_u64(&a.status[chunk], pack_status(btag, 1u, block_total));
+        int64_t top = chunk - 1;
         for (;;) {
-          const unsigned long long v = ld_acquire_u64(&a.status[pred]);
-          const unsigned flag = static_cast<unsigned>((v >> 46) & 3u);
-          if (static_cast<uint32_t>(v >> 48) != (btag & 0xFFFFu) || flag == 0) continue;
-          excl += v & ((1ull << 46) - 1);
-          if (flag == 2u) break;
-          --pred;
+          const int64_t pred = top - lane;
+          unsigned flag = 2u;
+          unsigned long long cnt = 0;
+          if (pred >= 0) {
+            const unsigned long long v = ld_acquire_u64(&a.status[pred]);
+            flag = static_cast<uint32_t>(v >> 48) == (btag & 0xFFFFu)
+                       ? static_cast<unsigned>((v >> 46) & 3u)
+                       : 0u;
+            cnt = v & ((1ull << 46) - 1);
+          }
+          const unsigned inc = __ballot_sync(0xffffffffu, flag == 2u);
+          const unsigned pending = __ballot_sync(0xffffffffu, flag == 0u);
+          const int first = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive in the window
+          const unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+          if (pending & need) continue;  // a predecessor has not published yet
+          unsigned long long part = lane <= first ? cnt : 0ull;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          excl += part;
+          if (inc) break;
+          top -= 32;
         }
-        st_release_u64(&a.status[chunk], pack_status(btag, 2u, excl + block_total));
+        if (lane == 0)
+          st_release_u64(&a.status[chunk], pack_status(btag, 2u, excl + block_total));
       }
-      s_excl = static_cast<long long>(excl);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_tested),
-                static_cast<unsigned long long>(block_valid));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_accepted),
-                static_cast<unsigned long long>(block_total));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_rejected),
-                static_cast<unsigned long long>(block_valid - block_total));
+      if (lane == 0) {
+        s_excl = static_cast<long long>(excl);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_tested),
+                  static_cast<unsigned long long>(block_valid));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_accepted),
+                  static_cast<unsigned long long>(block_total));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_rejected),
+                  static_cast<unsigned long long>(block_valid - block_total));
+      }
     }
     __syncthreads();
     int64_t rank = acc_before + s_excl + thread_excl;
@@ -365,6 +386,19 @@ __global__ void hash_build_kernel(const uint64_t* __restrict__ keys, int64_t n,
   }
 }
 
+// Read-then-zero of gradient replicas / hot copies: L2-coherent loads
+// (ld.global.cg).  A read-only (.nc) load is NOT ordered against a later
+// store to the same address — ptxas schedules it past the store (seen in the
+// SASS) — so the re-zeroing pattern must not use __ldg.
+__device__ __forceinline__ void load_chunk_cg(const float* p, Vec<float>& out) {
+  const float4 q = __ldcg(reinterpret_cast<const float4*>(p));
+  out.v[0] = q.x, out.v[1] = q.y, out.v[2] = q.z, out.v[3] = q.w;
+}
+__device__ __forceinline__ void load_chunk_cg(const double* p, Vec<double>& out) {
+  const double2 q = __ldcg(reinterpret_cast<const double2*>(p));
+  out.v[0] = q.x, out.v[1] = q.y;
+}
+
 // adam_step (optimizer.cpp:47-66) fused with zeroing the gradient; padding
 // columns (j >= r) are left untouched.  With nrep > 0 the gradient is read
 // as the sum of the privatized replicas (folding grad_reduce_kernel into the
@@ -386,10 +420,22 @@ __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr
   if (nrep > 0) {
 #pragma unroll
     for (int e = 0; e < VW; ++e) g.v[e] = static_cast<T>(0);
-    for (int q = 0; q < nrep; ++q) {
+    int q = 0;
+    for (; q + 4 <= nrep; q += 4) {  // four replicas' loads in flight
+      Vec<T> x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_chunk_cg(reps + (q + u) * rep_stride + i0, x[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) g.v[e] += x[u].v[e];
+        store_chunk(reps + (q + u) * rep_stride + i0, Vec<T>{});
+      }
+    }
+    for (; q < nrep; ++q) {
       T* p = reps + q * rep_stride + i0;
       Vec<T> x;
-      load_chunk(p, x);
+      load_chunk_cg(p, x);
 #pragma unroll
       for (int e = 0; e < VW; ++e) g.v[e] += x.v[e];
       store_chunk(p, Vec<T>{});
@@ -541,19 +587,10 @@ __global__ void row_hist_kernel(const uint32_t* __restrict__ rec, int rec_words,
   }
 }
 
-// Coherent (non-__ldg) 16-byte loads: the fold reads data it then re-zeroes.
-__device__ __forceinline__ Vec<float> ld_chunk_rw(const float* p) {
-  const float4 q = *reinterpret_cast<const float4*>(p);
-  return Vec<float>{{q.x, q.y, q.z, q.w}};
-}
-__device__ __forceinline__ Vec<double> ld_chunk_rw(const double* p) {
-  const double2 q = *reinterpret_cast<const double2*>(p);
-  return Vec<double>{{q.x, q.y}};
-}
-
 // G[row of slot] += sum of the slot's rh copies; copies re-zeroed.  One block
-// per hot row: thread (j, c) sums copies j, j+J, ... of 16-byte chunk c, then
-// the J partial chunks are combined in shared memory.
+// per hot row: thread (j, c) sums copies j, j+J, ... of 16-byte chunk c (four
+// loads in flight), then the J partial chunks are combined by a shared-memory
+// tree.
 template <typename T>
 __global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int rh, int rp,
                                                        const int64_t* __restrict__ hot_off,
@@ -570,19 +607,21 @@ __global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int
   if (j0 < J) {
     T* base = Ghot + static_cast<int64_t>(blockIdx.x) * rh * rp + c * VW;
     int j = j0;
-    for (; j + 3 * J < rh; j += 4 * J) {  // four copies in flight
+    for (; j + 3 * J < rh; j += 4 * J) {
       Vec<T> x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = ld_chunk_rw(base + (j + u * J) * rp);
+      for (int u = 0; u < 4; ++u) load_chunk_cg(base + (j + u * J) * rp, x[u]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
 #pragma unroll
         for (int e = 0; e < VW; ++e) acc.v[e] += x[u].v[e];
-        store_chunk(base + (j + u * J) * rp, Vec<T>{});
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) store_chunk(base + (j + u * J) * rp, Vec<T>{});
     }
     for (; j < rh; j += J) {
-      const Vec<T> x = ld_chunk_rw(base + j * rp);
+      Vec<T> x;
+      load_chunk_cg(base + j * rp, x);
 #pragma unroll
       for (int e = 0; e < VW; ++e) acc.v[e] += x.v[e];
       store_chunk(base + j * rp, Vec<T>{});
@@ -590,14 +629,20 @@ __global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int
   }
   part[threadIdx.x] = acc;
   __syncthreads();
-  if (threadIdx.x < ch) {
-    for (int j = 1; j < J; ++j) {
+  // tree over the J partials of each chunk (J need not be a power of two)
+  int Jp = 1;
+  while (Jp < J) Jp <<= 1;
+  for (int h = Jp >> 1; h > 0; h >>= 1) {
+    if (j0 < h && j0 + h < J) {
 #pragma unroll
-      for (int e = 0; e < VW; ++e) acc.v[e] += part[j * ch + c].v[e];
+      for (int e = 0; e < VW; ++e) part[threadIdx.x].v[e] += part[threadIdx.x + h * ch].v[e];
     }
+    __syncthreads();
+  }
+  if (static_cast<int>(threadIdx.x) < ch) {
     T* g = G + hot_off[blockIdx.x] + c * VW;
 #pragma unroll
-    for (int e = 0; e < VW; ++e) g[e] += acc.v[e];
+    for (int e = 0; e < VW; ++e) g[e] += part[threadIdx.x].v[e];
   }
 }
 
