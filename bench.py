@@ -209,10 +209,10 @@ ROOFLINE_NOTES = {
 }
 
 
-def launches_per_step(w):
-    # fused kernel + adam; the stratified zero sampler adds 3 x (plan +
-    # candidate) + a shortfall check
-    return 2 + (7 if w.sampler == "stratified" else 0)
+def launches_per_step(w, hot):
+    # fused kernel + adam (+ the hot-row fold); the stratified zero sampler
+    # adds 3 x (plan + candidate test + scatter) + a shortfall check
+    return 2 + (1 if hot else 0) + (10 if w.sampler == "stratified" else 0)
 
 
 # ---------------------------------------------------------------------------
@@ -363,6 +363,7 @@ def run_ours(args, w):
         total_ms = float(t[0])
     ms_per_step = total_ms / K
     steps_path = e.steps_path
+    hot_copies = e.hot_rows[1] if w.kind == "sparse" else 0
     samples_per_step = w.samples_per_step * world
     value = samples_per_step / (ms_per_step / 1e3)
 
@@ -465,7 +466,7 @@ def run_ours(args, w):
                             "fused sample+eval+MTTKRP kernel + (all-reduce) + fused Adam; K steps "
                             "replayed as one CUDA graph")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w) * K, "clocks": clk,
+        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w, hot_copies > 0) * K, "clocks": clk,
         "impl": "ours",
     }
     if rank == 0:

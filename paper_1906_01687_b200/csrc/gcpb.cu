@@ -201,6 +201,8 @@ struct gcpb_ctx {
   int rec_words = 4;
   DBuf hkeys, hvals;
   uint64_t hmask = 0;
+  DBuf bloom;          // blocked Bloom prefilter of the keys (32-byte blocks)
+  uint64_t bmask = 0;
   bool hash_ready = false;
   int domain_flags = -1;  // cached domain scan of the stored data
   // hot rows (FusedArgs::hslot / Ghot): selected from the nonzeros' per-mode
@@ -238,7 +240,7 @@ struct gcpb_ctx {
   int64_t zscratch_cap = 0;
 
   // stratified zero sampler
-  DBuf zero_list, zstatus;
+  DBuf zero_list, zstatus, ztbits;
   int64_t zero_cap = 0, zstatus_cap = 0, z_nchunks_first = 0;
 
   // estimator
@@ -444,6 +446,18 @@ void ensure_hash(gcpb_ctx* c) {
     hash_build_kernel<<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
         c->keys.as<uint64_t>(), c->nnz, c->hkeys.as<unsigned long long>(),
         c->hvals.as<uint32_t>(), c->hmask);
+    CK(cudaGetLastError());
+  }
+  // Bloom prefilter: at most 32 keys per 32-byte block on average (C3: 16 MB,
+  // 19 keys per block, ~1 % false positives with 3 bits per key).
+  uint64_t blocks = 1;
+  while (blocks * 32 < static_cast<uint64_t>(c->nnz)) blocks <<= 1;
+  c->bmask = blocks - 1;
+  c->bloom.alloc(blocks * 32);
+  CK(cudaMemsetAsync(c->bloom.p, 0, blocks * 32, c->stream));
+  if (c->nnz > 0) {
+    bloom_build_kernel<<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
+        c->keys.as<uint64_t>(), c->nnz, c->bloom.as<uint32_t>(), c->bmask);
     CK(cudaGetLastError());
   }
   c->hash_ready = true;
@@ -783,6 +797,7 @@ void prepare_zero_sampler(gcpb_ctx* c, int64_t q, double rho) {
   }
   if (c->zstatus_cap < nchunks) {
     c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
+    c->ztbits.alloc(static_cast<size_t>(nchunks) * kZcThreads * sizeof(uint32_t));
     c->zstatus_cap = nchunks;
   }
   c->z_nchunks_first = nchunks;
@@ -822,9 +837,6 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
                       const uint64_t* iter_base, uint32_t tag, int mode, int64_t p_ref = 0) {
   if (mode != ZERO_CAPTURE) prepare_zero_sampler(c, q, rho);
   const int64_t nchunks = c->z_nchunks_first;
-  // Look-back words from earlier calls must not alias this call's batch tags.
-  CK(cudaMemsetAsync(c->zstatus.p, 0, static_cast<size_t>(std::max<int64_t>(nchunks, 1)) * 8,
-                     c->stream));
   DevState* st = c->dst();
   ZeroArgs za;
   std::memset(&za, 0, sizeof(za));
@@ -842,14 +854,18 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   za.tag = tag;
   za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
   za.hmask = c->hmask;
+  za.bloom = c->nnz > 0 && getenv("GCPB_NO_BLOOM") == nullptr ? c->bloom.as<uint32_t>() : nullptr;
+  za.bmask = c->bmask;
   za.st = st;
   za.status = c->zstatus.as<unsigned long long>();
+  za.tbits = c->ztbits.as<uint32_t>();
   za.zero_list = c->zero_list.as<uint64_t>();
   fill_refstream(c, za, seed, p_ref);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
   for (int b = 0; b < 3; ++b) {
     zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, b == 0 ? 1 : 0);
     zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
   }
   CK(cudaGetLastError());
   if (mode == ZERO_CAPTURE) {
@@ -864,6 +880,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
     if (std::min(c->host_state.z_accepted, q) >= q) break;
     zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, 0);
     zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
     CK(cudaGetLastError());
   }
 }
@@ -945,6 +962,8 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
   za.tag = tag;
   za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
   za.hmask = c->hmask;
+  za.bloom = c->nnz > 0 && getenv("GCPB_NO_BLOOM") == nullptr ? c->bloom.as<uint32_t>() : nullptr;
+  za.bmask = c->bmask;
   za.st = st;
   fill_refstream(c, za, seed, p_ref);
   int64_t tested = 0, accepted = 0, kept_local = 0;
@@ -958,21 +977,23 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
       const int64_t nchunks = (size + kZcChunk - 1) / kZcChunk;
       if (c->zstatus_cap < nchunks) {
         c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
+        c->ztbits.alloc(static_cast<size_t>(nchunks) * kZcThreads * sizeof(uint32_t));
         c->zstatus_cap = nchunks;
       }
       if (c->zscratch_cap < size) {
         c->zscratch.alloc(static_cast<size_t>(size) * sizeof(uint64_t));
         c->zscratch_cap = size;
       }
-      CK(cudaMemsetAsync(c->zstatus.p, 0, static_cast<size_t>(nchunks) * 8, c->stream));
       CK(cudaMemcpyAsync(&st->z_status_cap, &c->zstatus_cap, 8, cudaMemcpyHostToDevice,
                          c->stream));
       zero_plan_slice_kernel<<<1, 1, 0, c->stream>>>(st, tested + lo, size, nchunks);
       za.status = c->zstatus.as<unsigned long long>();
+      za.tbits = c->ztbits.as<uint32_t>();
       za.zero_list = c->zscratch.as<uint64_t>();
       const int grid =
           static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
       zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+      zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(&mine, &st->z_accepted, 8, cudaMemcpyDeviceToHost, c->stream));
       c->sync();

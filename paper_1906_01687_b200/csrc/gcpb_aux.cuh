@@ -48,8 +48,11 @@ struct ZeroArgs {
   uint32_t tag;
   const uint64_t* hkeys;
   uint64_t hmask;
+  const uint32_t* bloom;  // blocked Bloom prefilter of the keys (nullptr = none)
+  uint64_t bmask;         // Bloom blocks - 1
   DevState* st;
-  unsigned long long* status;
+  unsigned long long* status;  // per chunk: non-hit count
+  uint32_t* tbits;             // per thread of a chunk: non-hit bits | offset << 8
   uint64_t* zero_list;
   int refstream;
   uint64_t ref_key;
@@ -209,48 +212,59 @@ __global__ void zero_check_kernel(DevState* st) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && st->z_accepted < st->z_q) st->z_incomplete += 1;
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+// Blocked Bloom filter over the nonzero keys (one 32-byte block per key, 3
+// bits inside it): a zero candidate — almost every candidate at C3's density
+// of 1e-5 — is rejected from one L2-resident sector instead of a random HBM
+// probe of the 4-way hash; the ~1 % false positives and the true hits fall
+// through to the exact hash lookup.
+__device__ __forceinline__ uint64_t bloom_hash(uint64_t key) {
+  return mix64(key ^ 0x5bd1e9955bd1e995ull);
 }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__global__ void bloom_build_kernel(const uint64_t* __restrict__ keys, int64_t n, uint32_t* bloom,
+                                   uint64_t bmask) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h = bloom_hash(keys[e]);
+    uint32_t* blk = bloom + (h & bmask) * 8;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const uint32_t pos = static_cast<uint32_t>(h >> (40 + 8 * b)) & 255u;
+      atomicOr(blk + (pos >> 5), 1u << (pos & 31u));
+    }
+  }
+}
+__device__ __forceinline__ bool bloom_maybe(const uint32_t* __restrict__ bloom, uint64_t bmask,
+                                            uint64_t key) {
+  const uint64_t h = bloom_hash(key);
+  const uint32_t* blk = bloom + (h & bmask) * 8;
+  bool all = true;
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const uint32_t pos = static_cast<uint32_t>(h >> (40 + 8 * b)) & 255u;
+    all = all && ((__ldg(blk + (pos >> 5)) >> (pos & 31u)) & 1u);
+  }
+  return all;
 }
 
-// Status word: [63:48] batch tag, [47:46] flag (1 aggregate, 2 inclusive
-// prefix), [45:0] count.
-__device__ __forceinline__ unsigned long long pack_status(uint32_t tag, unsigned flag,
-                                                          unsigned long long v) {
-  return (static_cast<unsigned long long>(tag & 0xFFFFu) << 48) |
-         (static_cast<unsigned long long>(flag) << 46) | (v & ((1ull << 46) - 1));
-}
-
-// Tests one batch of zero candidates against the nonzero hash and appends the
-// accepted ones, in candidate order, to zero_list (ranks < q only) — the
-// reference's "test the whole batch, keep the first q non-hits"
-// (samplers.hpp:117-133) as one pass with a decoupled look-back scan.
+// Tests one batch of zero candidates against the nonzero keys (Bloom
+// prefilter, then the exact hash) — the reference's "test the whole batch,
+// keep the first q non-hits" (samplers.hpp:117-133) in two kernels without an
+// inter-block dependency: zero_cand_kernel writes each chunk's non-hit count
+// and, per thread, its non-hit bits and offset inside the chunk;
+// zero_scatter_kernel ranks them (prefix over the chunk counts) and appends
+// the accepted ordinals, in candidate order, to zero_list (ranks < q only).
 __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a) {
-  __shared__ long long s_chunk;
   __shared__ int s_warp_sum[kZcThreads / 32];
   __shared__ int s_warp_valid[kZcThreads / 32];
-  __shared__ long long s_excl;
   DevState* st = a.st;
   const int64_t nchunks = st->z_nchunks;
   const int64_t bbeg = st->z_batch_begin;
   const int64_t bend = bbeg + st->z_batch_size;
-  const int64_t acc_before = st->z_acc_before;
-  const int64_t q = st->z_q;
-  const uint32_t btag = st->z_batch_tag;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const uint64_t iter = a.iter + (a.iter_base ? *a.iter_base : 0ull);
   const uint64_t rbase = a.refstream ? st->ref_ctr : 0ull;
-  for (;;) {
-    if (threadIdx.x == 0) s_chunk = static_cast<long long>(atomicAdd(&st->z_ticket, 1ull));
-    __syncthreads();
-    const int64_t chunk = s_chunk;
-    if (chunk >= nchunks) break;
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
     const int64_t cbeg = bbeg + chunk * kZcChunk + static_cast<int64_t>(threadIdx.x) * kZcItems;
     uint32_t bits = 0;
     int nvalid = 0;
@@ -262,8 +276,8 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       uint64_t lin = 0;
       if (a.refstream) {
         for (int k = 0; k < a.d; ++k) {
-          const uint64_t j = static_cast<uint64_t>(a.ref_off + c * a.d + k);
-          lin += refstream_below(a.ref_key, rbase + j + 1, a.dims[k], a.thr64[k], &st->ref_flag) *
+          const uint64_t jj = static_cast<uint64_t>(a.ref_off + c * a.d + k);
+          lin += refstream_below(a.ref_key, rbase + jj + 1, a.dims[k], a.thr64[k], &st->ref_flag) *
                  a.stride[k];
         }
       }
@@ -281,7 +295,9 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
           lin += static_cast<uint64_t>(ik) * a.stride[k];
         }
       }
-      const bool hit = a.hkeys != nullptr && hash_find(a.hkeys, a.hmask, lin) >= 0;
+      const bool hit = a.hkeys != nullptr &&
+                       (a.bloom == nullptr || bloom_maybe(a.bloom, a.bmask, lin)) &&
+                       hash_find(a.hkeys, a.hmask, lin) >= 0;
       if (!hit) bits |= 1u << j;
     }
     const int cnt = __popc(bits);
@@ -305,61 +321,48 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       block_valid += s_warp_valid[w];
     }
     const int thread_excl = warp_excl + incl - cnt;
-    if (wid == 0) {
-      // Decoupled look-back, one warp wide: lane i inspects chunk - 1 - i;
-      // the window's aggregates up to the nearest inclusive prefix are summed
-      // in one step instead of walking predecessors one L2 round trip each.
-      unsigned long long excl = 0;
-      if (chunk == 0) {
-        if (lane == 0) st_release_u64(&a.status[0], pack_status(btag, 2u, block_total));
-      } else {
-        if (lane == 0) st_release_u64(&a.status[chunk], pack_status(btag, 1u, block_total));
-        int64_t top = chunk - 1;
-        for (;;) {
-          const int64_t pred = top - lane;
-          unsigned flag = 2u;
-          unsigned long long cnt = 0;
-          if (pred >= 0) {
-            const unsigned long long v = ld_acquire_u64(&a.status[pred]);
-            flag = static_cast<uint32_t>(v >> 48) == (btag & 0xFFFFu)
-                       ? static_cast<unsigned>((v >> 46) & 3u)
-                       : 0u;
-            cnt = v & ((1ull << 46) - 1);
-          }
-          const unsigned inc = __ballot_sync(0xffffffffu, flag == 2u);
-          const unsigned pending = __ballot_sync(0xffffffffu, flag == 0u);
-          const int first = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive in the window
-          const unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
-          if (pending & need) continue;  // a predecessor has not published yet
-          unsigned long long part = lane <= first ? cnt : 0ull;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-          excl += part;
-          if (inc) break;
-          top -= 32;
-        }
-        if (lane == 0)
-          st_release_u64(&a.status[chunk], pack_status(btag, 2u, excl + block_total));
-      }
-      if (lane == 0) {
-        s_excl = static_cast<long long>(excl);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_tested),
-                  static_cast<unsigned long long>(block_valid));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_accepted),
-                  static_cast<unsigned long long>(block_total));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_rejected),
-                  static_cast<unsigned long long>(block_valid - block_total));
-      }
+    a.tbits[chunk * kZcThreads + threadIdx.x] = bits | (static_cast<uint32_t>(thread_excl) << 8);
+    if (threadIdx.x == 0) {
+      a.status[chunk] = static_cast<unsigned long long>(block_total);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_tested),
+                static_cast<unsigned long long>(block_valid));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_accepted),
+                static_cast<unsigned long long>(block_total));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->z_rejected),
+                static_cast<unsigned long long>(block_valid - block_total));
     }
+    __syncthreads();  // s_warp_* reused by the next chunk
+  }
+}
+
+__global__ void __launch_bounds__(kZcThreads) zero_scatter_kernel(const ZeroArgs a) {
+  __shared__ unsigned long long s_part[kZcThreads / 32];
+  DevState* st = a.st;
+  const int64_t nchunks = st->z_nchunks;
+  const int64_t bbeg = st->z_batch_begin;
+  const int64_t acc_before = st->z_acc_before;
+  const int64_t q = st->z_q;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+    unsigned long long part = 0;  // non-hits of the chunks before this one
+    for (int64_t i = threadIdx.x; i < chunk; i += kZcThreads) part += a.status[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) s_part[wid] = part;
     __syncthreads();
-    int64_t rank = acc_before + s_excl + thread_excl;
+    unsigned long long excl = 0;
+    for (int w = 0; w < kZcThreads / 32; ++w) excl += s_part[w];
+    const uint32_t tb = a.tbits[chunk * kZcThreads + threadIdx.x];
+    const int64_t cbeg = bbeg + chunk * kZcChunk + static_cast<int64_t>(threadIdx.x) * kZcItems;
+    int64_t rank = acc_before + static_cast<int64_t>(excl) + static_cast<int64_t>(tb >> 8);
     for (int j = 0; j < kZcItems; ++j) {
-      if ((bits >> j) & 1u) {
+      if ((tb >> j) & 1u) {
         if (rank < q) a.zero_list[rank] = static_cast<uint64_t>(cbeg + j);
         ++rank;
       }
     }
-    __syncthreads();
+    __syncthreads();  // s_part reused by the next chunk
   }
 }
 
