@@ -209,10 +209,11 @@ ROOFLINE_NOTES = {
 }
 
 
-def launches_per_step(w, hot):
-    # fused kernel + adam (+ the hot-row fold); the stratified zero sampler
-    # adds 3 x (plan + candidate test + scatter) + a shortfall check
-    return 2 + (1 if hot else 0) + (10 if w.sampler == "stratified" else 0)
+def launches_per_step(w, hot, world):
+    # fused kernel + adam (which folds the hot-row copies; sharded steps fold
+    # them before the all-reduce instead); the stratified zero sampler adds
+    # 3 x (plan + candidate test + scatter) + a shortfall check
+    return 2 + (1 if hot and world > 1 else 0) + (10 if w.sampler == "stratified" else 0)
 
 
 # ---------------------------------------------------------------------------
@@ -466,7 +467,7 @@ def run_ours(args, w):
                             "fused sample+eval+MTTKRP kernel + (all-reduce) + fused Adam; K steps "
                             "replayed as one CUDA graph")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w, hot_copies > 0) * K, "clocks": clk,
+        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w, hot_copies > 0, world) * K, "clocks": clk,
         "impl": "ours",
     }
     if rank == 0:

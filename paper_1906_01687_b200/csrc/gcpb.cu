@@ -212,6 +212,7 @@ struct gcpb_ctx {
   int hot_n = 0;             // hot rows over all modes
   int hot_rh_cap = 0;        // copies allocated per hot row
   int hot_last = 0;          // copies used by the last fused scatter
+  int hot_pending = 0;       // copies the next adam_launch folds (0 = none)
   uint32_t hot_base[kMaxModes + 1] = {};
   uint32_t row_base[kMaxModes + 1] = {};
   double hot_fmax[kMaxModes] = {};  // largest share of the nonzeros in one row, per mode
@@ -761,10 +762,12 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
         c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride);
     CK(cudaGetLastError());
   }
-  if (used_hot) {  // hot rows' copies into the gradient (or replica 0 when Adam folds)
+  c->hot_pending = 0;
+  if (used_hot && fold) {  // the fused Adam folds the hot rows' copies itself
+    c->hot_pending = a.rh;
+  } else if (used_hot) {   // hot rows' copies into the gradient
     hot_fold_kernel<T><<<c->hot_n, 256, 0, c->stream>>>(
-        c->Ghot.as<T>(), a.rh, static_cast<int>(c->rp), c->hot_off.as<int64_t>(),
-        (fold && c->nrep > 1) ? c->Grep.as<T>() : c->Gr.as<T>());
+        c->Ghot.as<T>(), a.rh, static_cast<int>(c->rp), c->hot_off.as<int64_t>(), c->Gr.as<T>());
     CK(cudaGetLastError());
   }
 }
@@ -1153,11 +1156,26 @@ int64_t expected_samples(const gcpb_ctx* c, const gcpb_sampler* s) {
 // fold_reps > 0: the gradient is the sum of that many replicas (read and
 // re-zeroed by the kernel).  advance_rng: also step the device draw-stream base.
 template <typename T>
-void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0) {
-  const int grid = grid_for(c->nelem / c->vw, 256, c->num_sms, 8);
+void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0, int hot_rh = 0) {
+  HotAdam<T> hot;
+  std::memset(&hot, 0, sizeof(hot));
+  if (hot_rh > 0) {  // hot rows' copies folded by extra blocks
+    hot.hslot = c->hslot.as<uint8_t>();
+    hot.Ghot = c->Ghot.as<T>();
+    hot.hot_off = c->hot_off.as<int64_t>();
+    hot.rh = hot_rh;
+    hot.n = c->hot_n;
+    hot.d = c->d;
+    for (int k = 0; k < c->d; ++k) {
+      hot.rowbase[k] = c->row_base[k];
+      hot.off[k] = c->off[k];
+    }
+  }
+  const int grid = grid_for(c->nelem / c->vw, 256, c->num_sms, 8) + hot.n;
   adam_kernel<T><<<grid, 256, 0, c->stream>>>(
       c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
-      static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride, advance_rng);
+      static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride, advance_rng,
+      hot);
   CK(cudaGetLastError());
 }
 
@@ -1335,7 +1353,8 @@ void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint6
   } else if (c->nrep > 1) {
     fold = c->nrep;
   }
-  adam_launch<T>(c, fold, iter_base ? 1 : 0);
+  adam_launch<T>(c, fold, iter_base ? 1 : 0, c->hot_pending);
+  c->hot_pending = 0;
   c->grad_zero = true;
 }
 

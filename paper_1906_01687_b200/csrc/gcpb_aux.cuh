@@ -402,6 +402,91 @@ __device__ __forceinline__ void load_chunk_cg(const double* p, Vec<double>& out)
   out.v[0] = q.x, out.v[1] = q.y;
 }
 
+// Hot-row copies folded inside the Adam launch (FusedArgs::Ghot): block
+// main_blocks + s sums the rh copies of hot slot s and the row's gradient
+// replicas in parallel and updates that row; the main blocks skip hot rows.
+template <typename T>
+struct HotAdam {
+  const uint8_t* hslot;
+  T* Ghot;
+  const int64_t* hot_off;  // element offset of each slot's row
+  int rh, n, d;
+  uint32_t rowbase[4];
+  int64_t off[4];
+};
+
+template <typename T>
+__device__ __forceinline__ bool hot_chunk(const HotAdam<T>& h, int64_t i0, int rp) {
+  int64_t base = h.off[0];
+  uint32_t rb = h.rowbase[0];
+#pragma unroll
+  for (int k = 1; k < 4; ++k)  // static indices keep the parameter arrays in the constant bank
+    if (k < h.d && i0 >= h.off[k]) {
+      base = h.off[k];
+      rb = h.rowbase[k];
+    }
+  const uint32_t row = static_cast<uint32_t>((i0 - base) / rp);
+  return __ldg(h.hslot + rb + row) != 0xFFu;
+}
+
+// Sum over the rh copies of hot slot `slot` (and, with reps, the row's nrep
+// gradient replicas) of 16-byte chunk c = threadIdx % (rp / VW), re-zeroing
+// them: thread (j, c) takes sources j, j + J, ..., four loads in flight, then
+// a shared-memory tree combines the J partials.  Valid in threads < rp / VW.
+template <typename T>
+__device__ __forceinline__ Vec<T> hot_rows_sum(T* __restrict__ Ghot, int slot, int rh, int rp,
+                                               T* __restrict__ reps, int nrep,
+                                               int64_t rep_stride, int64_t row_off) {
+  constexpr int VW = Vec<T>::W;
+  __shared__ Vec<T> part[256];
+  const int ch = rp / VW;
+  const int J = blockDim.x / ch;
+  const int c = threadIdx.x % ch;
+  const int j0 = threadIdx.x / ch;
+  Vec<T> acc;
+#pragma unroll
+  for (int e = 0; e < VW; ++e) acc.v[e] = static_cast<T>(0);
+  const int nsrc = rh + nrep;
+  auto src = [&](int j) -> T* {
+    return j < rh ? Ghot + (static_cast<int64_t>(slot) * rh + j) * rp + c * VW
+                  : reps + (j - rh) * rep_stride + row_off + c * VW;
+  };
+  if (j0 < J) {
+    int j = j0;
+    for (; j + 3 * J < nsrc; j += 4 * J) {
+      Vec<T> x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_chunk_cg(src(j + u * J), x[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc.v[e] += x[u].v[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) store_chunk(src(j + u * J), Vec<T>{});
+    }
+    for (; j < nsrc; j += J) {
+      Vec<T> x;
+      load_chunk_cg(src(j), x);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) acc.v[e] += x.v[e];
+      store_chunk(src(j), Vec<T>{});
+    }
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  int Jp = 1;
+  while (Jp < J) Jp <<= 1;
+  for (int h = Jp >> 1; h > 0; h >>= 1) {
+    if (j0 < h && j0 + h < J) {
+#pragma unroll
+      for (int e = 0; e < VW; ++e) part[threadIdx.x].v[e] += part[threadIdx.x + h * ch].v[e];
+    }
+    __syncthreads();
+  }
+  return part[threadIdx.x % (ch > 0 ? ch : 1)];
+}
+
 // adam_step (optimizer.cpp:47-66) fused with zeroing the gradient; padding
 // columns (j >= r) are left untouched.  With nrep > 0 the gradient is read
 // as the sum of the privatized replicas (folding grad_reduce_kernel into the
@@ -409,12 +494,13 @@ __device__ __forceinline__ void load_chunk_cg(const double* p, Vec<double>& out)
 // 16-byte chunk per array per iteration (rows are padded to 32 bytes, so a
 // chunk never straddles rows), two chunks in flight.  The last block advances
 // t (and the draw-stream base when advance_rng).
-template <typename T>
+template <typename T, bool EXTRA = false>
 __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr,
                                            T* __restrict__ B, T* __restrict__ C, int64_t i0,
                                            int col0, int r, T* __restrict__ reps, int nrep,
                                            int64_t rep_stride, T c1, T c2, T lr, T b1, T b2,
-                                           T ob1, T ob2, T eps, bool has_lb, T lb) {
+                                           T ob1, T ob2, T eps, bool has_lb, T lb,
+                                           Vec<T> extra = Vec<T>{}) {
   constexpr int VW = Vec<T>::W;
   Vec<T> a, g, b, c;
   load_chunk(A + i0, a);
@@ -444,8 +530,12 @@ __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr
       store_chunk(p, Vec<T>{});
     }
   } else {
-    load_chunk(Gr + i0, g);
+    load_chunk_cg(Gr + i0, g);
     store_chunk(Gr + i0, Vec<T>{});
+  }
+  if (EXTRA) {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) g.v[e] += extra.v[e];
   }
   Vec<T> ao = a, bo = b, co = c;  // padding columns keep their (zero) values
 #pragma unroll
@@ -471,7 +561,8 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
                                                    T* __restrict__ B, T* __restrict__ C,
                                                    int64_t n, int rp, int r, DevState* st,
                                                    T* __restrict__ reps, int nrep,
-                                                   int64_t rep_stride, int advance_rng) {
+                                                   int64_t rep_stride, int advance_rng,
+                                                   const HotAdam<T> hot) {
   constexpr int VW = Vec<T>::W;
   __shared__ double s_c1, s_c2;
   if (threadIdx.x == 0) {
@@ -488,10 +579,20 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
   const bool has_lb = st->has_lb != 0;
   const T lb = static_cast<T>(st->lb);
   const uint32_t nchunk = static_cast<uint32_t>(n / VW);  // n < 2^31, multiple of VW
-  const uint32_t stride = gridDim.x * blockDim.x;
-  if (nrep > 0) {  // small problems: replicas folded, simple loop
+  const int main_blocks = static_cast<int>(gridDim.x) - hot.n;
+  const uint32_t stride = static_cast<uint32_t>(main_blocks) * blockDim.x;
+  if (static_cast<int>(blockIdx.x) >= main_blocks) {  // one hot row per extra block
+    const int slot = static_cast<int>(blockIdx.x) - main_blocks;
+    const int64_t row_off = hot.hot_off[slot];
+    const Vec<T> hs = hot_rows_sum(hot.Ghot, slot, hot.rh, rp, reps, nrep, rep_stride, row_off);
+    if (static_cast<int>(threadIdx.x) < rp / VW)  // gradient = copies + replicas (+ Gr)
+      adam_chunk<T, true>(A, Gr, B, C, row_off + threadIdx.x * VW,
+                          static_cast<int>(threadIdx.x) * VW, r, nullptr, 0, 0, c1, c2, lr, b1,
+                          b2, ob1, ob2, eps, has_lb, lb, hs);
+  } else if (nrep > 0) {  // small problems: replicas folded, simple loop
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nchunk; q += stride)
-      adam_chunk<T>(A, Gr, B, C, static_cast<int64_t>(q) * VW,
+      if (hot.n == 0 || !hot_chunk(hot, static_cast<int64_t>(q) * VW, rp))
+        adam_chunk<T>(A, Gr, B, C, static_cast<int64_t>(q) * VW,
                     static_cast<int>((q * VW) % static_cast<uint32_t>(rp)), r, reps, nrep,
                     rep_stride, c1, c2, lr, b1, b2, ob1, ob2, eps, has_lb, lb);
   } else {
@@ -506,7 +607,7 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
         q = q < nchunk ? q : nchunk - 1;
         const int64_t i0 = static_cast<int64_t>(q) * VW;
         load_chunk(A + i0, a[u]);
-        load_chunk(Gr + i0, g[u]);
+        load_chunk_cg(Gr + i0, g[u]);
         load_chunk(B + i0, b[u]);
         load_chunk(C + i0, c[u]);
       }
@@ -515,6 +616,7 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
         const uint32_t q = q0 + u * stride;
         if (q >= nchunk) break;
         const int64_t i0 = static_cast<int64_t>(q) * VW;
+        if (hot.n > 0 && hot_chunk(hot, i0, rp)) continue;  // its hot block updates it
         const int col0 = static_cast<int>((q * VW) % static_cast<uint32_t>(rp));
         Vec<T> ao = a[u], bo = b[u], co = c[u];
 #pragma unroll
@@ -590,62 +692,19 @@ __global__ void row_hist_kernel(const uint32_t* __restrict__ rec, int rec_words,
   }
 }
 
-// G[row of slot] += sum of the slot's rh copies; copies re-zeroed.  One block
-// per hot row: thread (j, c) sums copies j, j+J, ... of 16-byte chunk c (four
-// loads in flight), then the J partial chunks are combined by a shared-memory
-// tree.
+// G[row of slot] += sum of the slot's rh copies; copies re-zeroed (the
+// gradient consumers other than the fused Adam: stoch_grad, the all-reduce).
 template <typename T>
 __global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int rh, int rp,
                                                        const int64_t* __restrict__ hot_off,
                                                        T* __restrict__ G) {
   constexpr int VW = Vec<T>::W;
-  __shared__ Vec<T> part[256];
-  const int ch = rp / VW;  // chunks per padded row
-  const int J = blockDim.x / ch;
-  const int c = threadIdx.x % ch;
-  const int j0 = threadIdx.x / ch;
-  Vec<T> acc;
+  const Vec<T> acc =
+      hot_rows_sum<T>(Ghot, static_cast<int>(blockIdx.x), rh, rp, nullptr, 0, 0, 0);
+  if (static_cast<int>(threadIdx.x) < rp / VW) {
+    T* g = G + hot_off[blockIdx.x] + threadIdx.x * VW;
 #pragma unroll
-  for (int e = 0; e < VW; ++e) acc.v[e] = static_cast<T>(0);
-  if (j0 < J) {
-    T* base = Ghot + static_cast<int64_t>(blockIdx.x) * rh * rp + c * VW;
-    int j = j0;
-    for (; j + 3 * J < rh; j += 4 * J) {
-      Vec<T> x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) load_chunk_cg(base + (j + u * J) * rp, x[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-#pragma unroll
-        for (int e = 0; e < VW; ++e) acc.v[e] += x[u].v[e];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) store_chunk(base + (j + u * J) * rp, Vec<T>{});
-    }
-    for (; j < rh; j += J) {
-      Vec<T> x;
-      load_chunk_cg(base + j * rp, x);
-#pragma unroll
-      for (int e = 0; e < VW; ++e) acc.v[e] += x.v[e];
-      store_chunk(base + j * rp, Vec<T>{});
-    }
-  }
-  part[threadIdx.x] = acc;
-  __syncthreads();
-  // tree over the J partials of each chunk (J need not be a power of two)
-  int Jp = 1;
-  while (Jp < J) Jp <<= 1;
-  for (int h = Jp >> 1; h > 0; h >>= 1) {
-    if (j0 < h && j0 + h < J) {
-#pragma unroll
-      for (int e = 0; e < VW; ++e) part[threadIdx.x].v[e] += part[threadIdx.x + h * ch].v[e];
-    }
-    __syncthreads();
-  }
-  if (static_cast<int>(threadIdx.x) < ch) {
-    T* g = G + hot_off[blockIdx.x] + c * VW;
-#pragma unroll
-    for (int e = 0; e < VW; ++e) g[e] += part[threadIdx.x].v[e];
+    for (int e = 0; e < VW; ++e) g[e] += acc.v[e];
   }
 }
 
