@@ -205,8 +205,9 @@ int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
  * sees it (draw_gradient_samples(x, model, ...) + adam_step(model&, ...) on a
  * host KruskalModel): model_in (flattened factors, GradientSet order) is
  * copied in before the step and the updated factors copied out to model_out
- * after it (either may be NULL).  One call, one pinned-staged copy each way,
- * one synchronisation. */
+ * after it (either may be NULL).  One call, one synchronisation; page-locked
+ * buffers (cudaHostAlloc / cudaHostRegister) are DMA'd in place, pageable
+ * ones through the context's pinned staging block. */
 int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter, const gcpb_adam* adam, const double* model_in,
                    double* model_out);

@@ -372,18 +372,36 @@ void mode_rows(const gcpb_ctx* c, int mode, int* k0, int* k1, int64_t* rows) {
   for (int k = *k0; k < *k1; ++k) *rows += c->dims[k];
 }
 
+// Page-locked (cudaHostAlloc / cudaHostRegister) host memory can be the DMA
+// source or target itself, skipping the staging copy.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// direct: `values` is pinned and the caller synchronises before returning
+// (gcpb_step_host), so the DMA reads it in place.
 template <typename T>
-void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values) {
+void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values, bool direct = false) {
   int k0, k1;
   int64_t rows;
   mode_rows(c, mode, &k0, &k1, &rows);
   const size_t n = static_cast<size_t>(rows * c->r);
   xfer_reserve(c, n);
-  CK(cudaEventSynchronize(c->xfer_done));  // the previous transfer left the staging block
-  std::memcpy(c->xfer_host, values, n * sizeof(double));
-  CK(cudaMemcpyAsync(c->xfer_dev.p, c->xfer_host, n * sizeof(double), cudaMemcpyHostToDevice,
-                     c->stream));
-  CK(cudaEventRecord(c->xfer_done, c->stream));
+  if (direct) {
+    CK(cudaMemcpyAsync(c->xfer_dev.p, values, n * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+  } else {
+    CK(cudaEventSynchronize(c->xfer_done));  // the previous transfer left the staging block
+    std::memcpy(c->xfer_host, values, n * sizeof(double));
+    CK(cudaMemcpyAsync(c->xfer_dev.p, c->xfer_host, n * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaEventRecord(c->xfer_done, c->stream));
+  }
   const int64_t total = rows * c->rp;
   unpack_rows_kernel<T><<<grid_for(total, 256, c->num_sms, 8), 256, 0, c->stream>>>(
       c->xfer_dev.as<double>(), buf.as<T>() + c->off[k0], total, static_cast<int>(c->r),
@@ -392,7 +410,7 @@ void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values) {
 }
 
 template <typename T>
-void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out) {
+void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out, bool direct = false) {
   int k0, k1;
   int64_t rows;
   mode_rows(c, mode, &k0, &k1, &rows);
@@ -403,24 +421,24 @@ void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out) {
       buf.as<T>() + c->off[k0], c->xfer_dev.as<double>(), static_cast<int64_t>(n),
       static_cast<int>(c->r), static_cast<int>(c->rp));
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(c->xfer_host, c->xfer_dev.p, n * sizeof(double), cudaMemcpyDeviceToHost,
-                     c->stream));
+  CK(cudaMemcpyAsync(direct ? static_cast<void*>(out) : static_cast<void*>(c->xfer_host),
+                     c->xfer_dev.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->xfer_done, c->stream));
   CK(cudaEventSynchronize(c->xfer_done));
-  std::memcpy(out, c->xfer_host, n * sizeof(double));
+  if (!direct) std::memcpy(out, c->xfer_host, n * sizeof(double));
 }
 
-void upload(gcpb_ctx* c, DBuf& buf, int mode, const double* v) {
+void upload(gcpb_ctx* c, DBuf& buf, int mode, const double* v, bool direct = false) {
   if (c->dtype == GCPB_F32)
-    upload_modes<float>(c, buf, mode, v);
+    upload_modes<float>(c, buf, mode, v, direct);
   else
-    upload_modes<double>(c, buf, mode, v);
+    upload_modes<double>(c, buf, mode, v, direct);
 }
-void download(gcpb_ctx* c, const DBuf& buf, int mode, double* v) {
+void download(gcpb_ctx* c, const DBuf& buf, int mode, double* v, bool direct = false) {
   if (c->dtype == GCPB_F32)
-    download_modes<float>(c, buf, mode, v);
+    download_modes<float>(c, buf, mode, v, direct);
   else
-    download_modes<double>(c, buf, mode, v);
+    download_modes<double>(c, buf, mode, v, direct);
 }
 
 void ensure_grad_zero(gcpb_ctx* c) {
@@ -2397,14 +2415,19 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
                    double* model_out) {
   return guard(ctx, [&] {
     check_step_args(ctx, sampler, loss);
-    if (model_in) upload(ctx, ctx->A, -1, model_in);
+    // pinned buffers are transferred in place: the call synchronises on the
+    // download before returning (without model_out, on the stream)
+    if (model_in) upload(ctx, ctx->A, -1, model_in, is_pinned(model_in));
     set_adam_params(ctx, adam);
     ensure_grad_zero(ctx);
     if (ctx->dtype == GCPB_F32)
       step_impl<float>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
     else
       step_impl<double>(ctx, sampler, loss, seed, iter, nullptr, ZERO_HOST_CHECK);
-    if (model_out) download(ctx, ctx->A, -1, model_out);
+    if (model_out)
+      download(ctx, ctx->A, -1, model_out, is_pinned(model_out));
+    else if (model_in)
+      CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
