@@ -301,7 +301,11 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
                                         const uint32_t (&ik)[DM], const Drawn<T>& s,
                                         T* __restrict__ Gb, uint32_t rsel = 0) {
   constexpr int VW = Vec<T>::W;
+  // G need not be a power of two (r = 20 fp32: 5 chunks -> 6 samples per pass
+  // instead of 4); lanes beyond NGRP * G idle.
   constexpr int NGRP = 32 / G;
+  constexpr int NPASS = (32 + NGRP - 1) / NGRP;
+  constexpr bool POW2 = (G & (G - 1)) == 0;
   constexpr int SL = VPL * VW;  // elements of one lane's row slice
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -323,9 +327,9 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   }
   const bool owns_any = gl * VPL < a.nchunks;
 #pragma unroll 1
-  for (int pass = 0; pass < G; ++pass) {
-    const int src = pass * NGRP + grp;
-    const bool v = __shfl_sync(FULL, s.valid, src);
+  for (int pass = 0; pass < NPASS; ++pass) {
+    const int src = (pass * NGRP + grp) & 31;
+    const bool v = __shfl_sync(FULL, s.valid, src) && (POW2 || (grp < NGRP && pass * NGRP + grp < 32));
     uint32_t ii[DM];
 #pragma unroll
     for (int k = 0; k < DM; ++k) ii[k] = __shfl_sync(FULL, ik[k], src);
@@ -382,8 +386,15 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
       }
       mp += cmask[c] * mc;
     }
+    if constexpr (POW2) {
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
+      for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
+    } else {  // every lane of the group sums the group in the same order
+      T tot = static_cast<T>(0);
+#pragma unroll
+      for (int j = 0; j < G; ++j) tot += __shfl_sync(FULL, mp, (grp * G + j) & 31);
+      mp = tot;
+    }
     const T m = mp;
     T y;
     if (ygiven) {
@@ -514,6 +525,21 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
   if (vpl == 1) {
     if constexpr (!REC && EXACT) {
       if (!given) {  // hot path: no host-given samples -> slim live state
+        if constexpr (sizeof(T) == 4) {  // 5 or 6 chunks: non-power-of-two lane groups
+          if (nchunks == 5 || nchunks == 6) {
+            if constexpr (DM <= 4) {
+              if (a.rh > 0) {
+                *used_hot = true;
+                return nchunks == 5
+                           ? go(fused_grad_kernel<T, DM, EXACT, 5, 1, REC, GCPB_MINB_HOT, false, true>)
+                           : go(fused_grad_kernel<T, DM, EXACT, 6, 1, REC, GCPB_MINB_HOT, false, true>);
+              }
+            }
+            return nchunks == 5
+                       ? go(fused_grad_kernel<T, DM, EXACT, 5, 1, REC, GCPB_MINB_SLIM, false>)
+                       : go(fused_grad_kernel<T, DM, EXACT, 6, 1, REC, GCPB_MINB_SLIM, false>);
+          }
+        }
         if constexpr (DM <= 4) {
           if (a.rh > 0) {  // hot rows privatized (sparse, skewed modes)
             *used_hot = true;

@@ -216,7 +216,8 @@ def _sparse_problem(rs, dims, nnz, a=1.1, values="binary"):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("strategy,loss,r", [(1, 2, 32), (2, 1, 20), (0, 0, 16), (2, 2, 8)])
+@pytest.mark.parametrize("strategy,loss,r", [(1, 2, 32), (2, 1, 20), (0, 0, 16), (2, 2, 8),
+                                             (1, 1, 24), (0, 2, 18)])
 def test_random_sparse_parity(orc, dtype, strategy, loss, r):
     g = G()
     rs = np.random.default_rng(strategy * 10 + loss + r)
