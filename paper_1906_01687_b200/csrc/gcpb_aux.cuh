@@ -452,25 +452,25 @@ __device__ __forceinline__ Vec<T> hot_rows_sum(T* __restrict__ Ghot, int slot, i
                   : reps + (j - rh) * rep_stride + row_off + c * VW;
   };
   if (j0 < J) {
-    int j = j0;
-    for (; j + 3 * J < nsrc; j += 4 * J) {
+    for (int j = j0; j < nsrc; j += 4 * J) {  // up to four sources' loads in flight
       Vec<T> x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load_chunk_cg(src(j + u * J), x[u]);
-#pragma unroll
       for (int u = 0; u < 4; ++u) {
+        if (j + u * J < nsrc) {
+          load_chunk_cg(src(j + u * J), x[u]);
+        } else {
 #pragma unroll
-        for (int e = 0; e < VW; ++e) acc.v[e] += x[u].v[e];
+          for (int e = 0; e < VW; ++e) x[u].v[e] = static_cast<T>(0);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) store_chunk(src(j + u * J), Vec<T>{});
-    }
-    for (; j < nsrc; j += J) {
-      Vec<T> x;
-      load_chunk_cg(src(j), x);
+      for (int u = 0; u < 4; ++u) {
+        if (j + u * J < nsrc) {
 #pragma unroll
-      for (int e = 0; e < VW; ++e) acc.v[e] += x.v[e];
-      store_chunk(src(j), Vec<T>{});
+          for (int e = 0; e < VW; ++e) acc.v[e] += x[u].v[e];
+          store_chunk(src(j + u * J), Vec<T>{});
+        }
+      }
     }
   }
   part[threadIdx.x] = acc;
@@ -509,25 +509,25 @@ __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr
   if (nrep > 0) {
 #pragma unroll
     for (int e = 0; e < VW; ++e) g.v[e] = static_cast<T>(0);
-    int q = 0;
-    for (; q + 4 <= nrep; q += 4) {  // four replicas' loads in flight
+    for (int q = 0; q < nrep; q += 4) {  // up to four replicas' loads in flight
       Vec<T> x[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load_chunk_cg(reps + (q + u) * rep_stride + i0, x[u]);
+      for (int u = 0; u < 4; ++u) {
+        if (q + u < nrep) {
+          load_chunk_cg(reps + (q + u) * rep_stride + i0, x[u]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) x[u].v[e] = static_cast<T>(0);
+        }
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        if (q + u < nrep) {
 #pragma unroll
-        for (int e = 0; e < VW; ++e) g.v[e] += x[u].v[e];
-        store_chunk(reps + (q + u) * rep_stride + i0, Vec<T>{});
+          for (int e = 0; e < VW; ++e) g.v[e] += x[u].v[e];
+          store_chunk(reps + (q + u) * rep_stride + i0, Vec<T>{});
+        }
       }
-    }
-    for (; q < nrep; ++q) {
-      T* p = reps + q * rep_stride + i0;
-      Vec<T> x;
-      load_chunk_cg(p, x);
-#pragma unroll
-      for (int e = 0; e < VW; ++e) g.v[e] += x.v[e];
-      store_chunk(p, Vec<T>{});
     }
   } else {
     load_chunk_cg(Gr + i0, g);
