@@ -854,6 +854,14 @@ void fill_refstream(const gcpb_ctx* c, ZeroArgs& za, uint64_t key, int64_t p_ref
   }
 }
 
+void launch_zero_cand(const gcpb_ctx* c, int grid, const ZeroArgs& za) {
+  switch (c->d) {
+    case 3: zero_cand_kernel<3><<<grid, kZcThreads, 0, c->stream>>>(za); break;
+    case 4: zero_cand_kernel<4><<<grid, kZcThreads, 0, c->stream>>>(za); break;
+    default: zero_cand_kernel<0><<<grid, kZcThreads, 0, c->stream>>>(za); break;
+  }
+}
+
 void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
                       const uint64_t* iter_base, uint32_t tag, int mode, int64_t p_ref = 0) {
   if (mode != ZERO_CAPTURE) prepare_zero_sampler(c, q, rho);
@@ -885,7 +893,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
   for (int b = 0; b < 3; ++b) {
     zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, b == 0 ? 1 : 0);
-    zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    launch_zero_cand(c, grid, za);
     zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
   }
   CK(cudaGetLastError());
@@ -900,7 +908,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
     if (c->host_state.z_overflow) throw std::logic_error("zero sampler: status overflow");
     if (std::min(c->host_state.z_accepted, q) >= q) break;
     zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, 0);
-    zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    launch_zero_cand(c, grid, za);
     zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
     CK(cudaGetLastError());
   }
@@ -1013,7 +1021,7 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
       za.zero_list = c->zscratch.as<uint64_t>();
       const int grid =
           static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
-      zero_cand_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+      launch_zero_cand(c, grid, za);
       zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(&mine, &st->z_accepted, 8, cudaMemcpyDeviceToHost, c->stream));

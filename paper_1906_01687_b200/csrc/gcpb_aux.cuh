@@ -253,7 +253,11 @@ __device__ __forceinline__ bool bloom_maybe(const uint32_t* __restrict__ bloom, 
 // and, per thread, its non-hit bits and offset inside the chunk;
 // zero_scatter_kernel ranks them (prefix over the chunk counts) and appends
 // the accepted ordinals, in candidate order, to zero_list (ranks < q only).
+// DM > 0: the mode count is a compile-time constant (d = 3, 4: every config),
+// so the per-mode loops unroll over constant-bank parameters.
+template <int DM>
 __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a) {
+  const int d = DM > 0 ? DM : a.d;
   __shared__ int s_warp_sum[kZcThreads / 32];
   __shared__ int s_warp_valid[kZcThreads / 32];
   DevState* st = a.st;
@@ -275,18 +279,21 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       ++nvalid;
       uint64_t lin = 0;
       if (a.refstream) {
-        for (int k = 0; k < a.d; ++k) {
-          const uint64_t jj = static_cast<uint64_t>(a.ref_off + c * a.d + k);
+        for (int k = 0; k < d; ++k) {
+          const uint64_t jj = static_cast<uint64_t>(a.ref_off + c * d + k);
           lin += refstream_below(a.ref_key, rbase + jj + 1, a.dims[k], a.thr64[k], &st->ref_flag) *
                  a.stride[k];
         }
       }
-      for (int g4 = 0; !a.refstream && g4 * 4 < a.d; ++g4) {
+#pragma unroll
+      for (int g4 = 0; g4 < (DM > 0 ? (DM + 3) / 4 : (kMaxModes + 3) / 4); ++g4) {
+        if (a.refstream || g4 * 4 >= d) break;
         const U4 b = philox_block(a.seed, a.tag, static_cast<uint32_t>(g4), 0u, iter,
                                   static_cast<uint64_t>(c));
+#pragma unroll
         for (int sl = 0; sl < 4; ++sl) {
           const int k = g4 * 4 + sl;
-          if (k >= a.d) break;
+          if (k >= d) break;
           const uint64_t prod = static_cast<uint64_t>(word_of(b, sl)) * a.dims[k];
           uint32_t ik = (static_cast<uint32_t>(prod) >= a.thr[k])
                             ? static_cast<uint32_t>(prod >> 32)
