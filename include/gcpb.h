@@ -230,6 +230,11 @@ int gcpb_steps_path(const gcpb_ctx* ctx);
  * scatter (0 = that scatter used none).  GCPB_HOT_T sets the target
  * reductions per address (default 256; 0 disables hot rows). */
 int gcpb_hot_rows(const gcpb_ctx* ctx, int* rows, int* copies);
+/* Interleaved factor/gradient table: *enabled = 1 when the
+ * context keeps one (factor tables beyond L2, or GCPB_IL=1; GCPB_IL=0
+ * disables), *last = 1 when the last fused scatter went to it (single-rank
+ * iterations: gcpb_step, gcpb_step_host, gcpb_run_steps, the fit). */
+int gcpb_interleaved(const gcpb_ctx* ctx, int* enabled, int* last);
 /* Per-launch timing of the fused sample->MTTKRP kernel: CUDA events recorded
  * on the context's stream around each non-graph launch.  enable = 1 clears
  * and starts recording, 0 stops.  gcpb_kernel_time synchronises and returns

@@ -128,6 +128,7 @@ SIGNATURES = [
     ("gcpb_synchronize", C.c_int, [ctx_p]),
     ("gcpb_steps_path", C.c_int, [ctx_p]),
     ("gcpb_hot_rows", C.c_int, [ctx_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("gcpb_interleaved", C.c_int, [ctx_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("gcpb_gradient_full", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),
     ("gcpb_gradient_poisson_implicit", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),
     ("gcpb_gradient_moments", C.c_int, [ctx_p, C.POINTER(gcpb_sampler), C.POINTER(gcpb_loss),

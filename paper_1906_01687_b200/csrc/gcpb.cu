@@ -181,6 +181,21 @@ struct gcpb_ctx {
   std::string err;
 
   DBuf A, Gr, B, C, As, Bs, Cs;
+  // Interleaved factor/gradient table for factor tables beyond L2 (C5):
+  // rows [A row | G row] (pitch 2 rp), so a sample's row gather and its row
+  // reduction share one 128-byte line (one DRAM burst) instead of two random
+  // 64-byte accesses (tools/randbw.cu: +21..40%).  Used by the fused step
+  // (scatter folded into Adam, one rank).  The IL Adam updates the factors in
+  // AG only; A is refreshed from AG (a_current) before anything else reads
+  // it.  ag_ok: AG's factor rows are current and its gradient rows zero;
+  // a_stale: A is older than AG (implies ag_ok); il_pending: the last fused
+  // scatter went to AG.
+  DBuf AG;
+  bool il_enabled = false;
+  bool ag_ok = false;
+  bool il_pending = false;
+  bool il_last = false;  // the last fused scatter used AG (gcpb_interleaved)
+  bool a_stale = false;
   DBuf Grep;            // privatized gradient replicas (L2-resident), zero at rest
   int nrep = 1;         // replicas used by the current call
   int nrep_cap = 1;     // replicas allocated
@@ -386,6 +401,23 @@ bool is_pinned(const void* p) {
 // direct: `values` is pinned and the caller synchronises before returning
 // (gcpb_step_host), so the DMA reads it in place.
 template <typename T>
+void a_current_t(gcpb_ctx* c) {
+  const int64_t nchunk = c->nelem / c->vw;
+  ag_unsync_kernel<T><<<grid_for(nchunk, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+      c->AG.as<T>(), c->A.as<T>(), nchunk, static_cast<int>(c->rp));
+  CK(cudaGetLastError());
+}
+// Refreshes A from the interleaved table when interleaved Adam updates left it stale.
+void a_current(gcpb_ctx* c) {
+  if (!c->a_stale) return;
+  if (c->dtype == GCPB_F32)
+    a_current_t<float>(c);
+  else
+    a_current_t<double>(c);
+  c->a_stale = false;
+}
+
+template <typename T>
 void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values, bool direct = false) {
   int k0, k1;
   int64_t rows;
@@ -429,12 +461,20 @@ void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out, bool di
 }
 
 void upload(gcpb_ctx* c, DBuf& buf, int mode, const double* v, bool direct = false) {
+  if (&buf == &c->A) {
+    if (mode < 0)
+      c->a_stale = false;  // every row is overwritten
+    else
+      a_current(c);        // the other modes' rows must be current
+    c->ag_ok = false;
+  }
   if (c->dtype == GCPB_F32)
     upload_modes<float>(c, buf, mode, v, direct);
   else
     upload_modes<double>(c, buf, mode, v, direct);
 }
 void download(gcpb_ctx* c, const DBuf& buf, int mode, double* v, bool direct = false) {
+  if (&buf == &c->A) a_current(c);
   if (c->dtype == GCPB_F32)
     download_modes<float>(c, buf, mode, v, direct);
   else
@@ -540,6 +580,7 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   a.rep_stride = c->rep_stride;
   a.d = c->d;
   a.rp = static_cast<int>(c->rp);
+  a.pitch = a.rp;
   a.nchunks = static_cast<int>((c->r + c->vw - 1) / c->vw);
   a.loss = loss ? loss->kind : 0;
   a.delta = static_cast<T>(loss ? loss->delta : 0.0);
@@ -595,11 +636,14 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   // slots than it hides latency, so it is opt-in (GCPB_PREFETCH=1).
   a.prefetch = 0;
   if (const char* ev = getenv("GCPB_PREFETCH")) a.prefetch = atoi(ev);
-  // Factor tables beyond ~half of L2 gather from HBM: use the staged kernel.
-  a.stage = (c->nelem * static_cast<int64_t>(c->tsize) > (int64_t{64} << 20)) ? 1 : 0;
+  // The cp.async-staged kernel (rows of the next tile staged in shared
+  // memory) is opt-in (GCPB_STAGE=1): since the plain kernel's lane groups
+  // and hot rows it is slower on C5 (6.68 vs 4.81 ms per launch, and 6.22 vs
+  // 3.85 ms on the interleaved table).
+  a.stage = 0;
   if (const char* ev = getenv("GCPB_STAGE")) a.stage = atoi(ev);
-  // Factor tables beyond L2: cold rows (unrestricted draws) and nonzero
-  // records evict_first, the nonzero picks' rows evict_last (C5: +3%).
+  // L2 hints for the staged kernel: cold rows (unrestricted draws) and
+  // nonzero records evict_first, the nonzero picks' rows evict_last.
   a.l2hint = a.stage ? 2 : 0;
   if (const char* ev = getenv("GCPB_L2HINT")) a.l2hint = atoi(ev);
   return a;
@@ -734,6 +778,25 @@ int hot_copies(gcpb_ctx* c, const FusedArgs<T>& a, int nrep) {
   return rh > nrep ? rh : 0;
 }
 
+// Allocates AG and, unless AG already mirrors A (ag_ok), rebuilds it from A.
+// Inside a graph capture the caller (run_steps_impl) has done this already.
+template <typename T>
+void ag_prepare(gcpb_ctx* c) {
+  if (!c->AG.p) {
+    const size_t bytes = static_cast<size_t>(2 * c->nelem) * c->tsize;
+    c->AG.alloc(bytes);
+    c->ag_ok = false;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(c->stream, &cs));
+  if (c->ag_ok || cs != cudaStreamCaptureStatusNone) return;
+  const int64_t nchunk = c->nelem / c->vw;
+  ag_sync_kernel<T><<<grid_for(nchunk, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+      c->A.as<T>(), c->AG.as<T>(), nchunk, static_cast<int>(c->rp));
+  CK(cudaGetLastError());
+  c->ag_ok = true;
+}
+
 template <typename T>
 void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   const int64_t tiles = finish_segments(a);
@@ -753,12 +816,30 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
       ev1 = pr.second;
     }
   }
-  if (a.scatter) {
+  c->il_pending = false;
+  if (a.scatter && fold && !record && c->il_enabled && c->nranks == 1) {
+    // interleaved table: the scatter goes to AG's gradient rows, Adam reads them
+    ag_prepare<T>(c);
+    a.A = c->AG.as<T>();
+    a.G = c->AG.as<T>() + c->rp;
+    a.pitch = static_cast<int>(2 * c->rp);
+    for (int k = 0; k < c->d; ++k) a.off[k] = 2 * c->off[k];
+    c->nrep = 1;
+    a.nrep = 1;
+    c->il_pending = true;
+    c->il_last = true;
+  } else if (a.scatter) {
+    a_current(c);
+    c->il_last = false;
     int64_t n = 0;
     for (int s = 0; s < a.nseg; ++s) n += std::max<int64_t>(0, a.seg[s].t_end - a.seg[s].t_begin);
     c->nrep = replicas_for(c, n);
     a.nrep = c->nrep;
     a.G = c->nrep > 1 ? c->Grep.as<T>() : c->Gr.as<T>();
+  } else {
+    a_current(c);
+  }
+  if (a.scatter) {
     if (!record) {
       a.rh = hot_copies<T>(c, a, c->nrep);
       if (a.rh > 0) {
@@ -1198,15 +1279,30 @@ void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0, int hot_rh
     }
   }
   const int grid = grid_for(c->nelem / c->vw, 256, c->num_sms, 8) + hot.n;
-  adam_kernel<T><<<grid, 256, 0, c->stream>>>(
-      c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
-      static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride, advance_rng,
-      hot);
+  if (c->il_pending) {  // gradient in AG's gradient rows; factors written to A and AG
+    ILTab<T> il;
+    il.ag = c->AG.as<T>();
+    il.rp = static_cast<int>(c->rp);
+    adam_kernel<T, true><<<grid, 256, 0, c->stream>>>(
+        c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem,
+        static_cast<int>(c->rp), static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps,
+        c->rep_stride, advance_rng, hot, il);
+    c->il_pending = false;
+    c->a_stale = true;
+  } else {
+    a_current(c);
+    adam_kernel<T><<<grid, 256, 0, c->stream>>>(
+        c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem,
+        static_cast<int>(c->rp), static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps,
+        c->rep_stride, advance_rng, hot);
+    c->ag_ok = false;  // A changed without AG
+  }
   CK(cudaGetLastError());
 }
 
 template <typename T>
 void estimate_launch(gcpb_ctx* c, const gcpb_loss* loss) {
+  a_current(c);
   ModelDesc<T> md;
   std::memset(&md, 0, sizeof(md));
   md.A = c->A.as<T>();
@@ -1368,8 +1464,22 @@ template <typename T>
 void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
                uint64_t iter, const uint64_t* iter_base, int zero_mode) {
   const bool multi = c->nranks > 1;
-  stoch_grad_impl<T>(c, sk, loss, seed, iter, true, false, zero_mode == ZERO_HOST_CHECK, false, -1,
-                     iter_base, /*fold=*/!multi, zero_mode);
+  try {
+    stoch_grad_impl<T>(c, sk, loss, seed, iter, true, false, zero_mode == ZERO_HOST_CHECK, false,
+                       -1, iter_base, /*fold=*/!multi, zero_mode);
+  } catch (...) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cs);
+    if (c->il_pending && cs == cudaStreamCaptureStatusNone) {
+      // AG's gradient rows may hold a partial scatter: keep its factor rows
+      // (A refreshed from them) and rebuild AG on the next interleaved step
+      c->il_pending = false;
+      a_current(c);
+      c->ag_ok = false;
+    }
+    c->il_pending = false;
+    throw;
+  }
   int fold = 0;
   if (multi) {
     if (!has_comm(c)) throw std::logic_error("sharded step without a communicator");
@@ -1445,6 +1555,8 @@ void small_launch_dm(const SmallArgs<T>& a, T* G, cudaStream_t stream) {
 template <typename T>
 void small_launch(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
                   int64_t n) {
+  a_current(c);
+  c->ag_ok = false;  // the cluster kernel writes A
   const FusedArgs<T> f = base_args<T>(c, loss, seed, 0);
   SmallArgs<T> a;
   std::memset(&a, 0, sizeof(a));
@@ -1520,6 +1632,11 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     return;
   }
   c->last_steps_path = 0;
+  const bool il = c->il_enabled && c->nranks == 1;
+  if (il)
+    ag_prepare<T>(c);  // not inside the capture
+  else
+    a_current(c);
   const std::string key = steps_key(c, sk, loss, seed, n);
   if (!c->graph_exec || key != c->graph_key) {
     if (c->graph_exec) {
@@ -1546,6 +1663,10 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
   }
   CK(cudaGraphLaunch(c->graph_exec, c->stream));
   c->grad_zero = true;
+  if (il) {  // a cached graph's interleaved Adam updates leave A stale on every replay
+    c->a_stale = true;
+    c->il_last = true;
+  }
 }
 
 // Synchronise and surface deferred device-side failures (graph-mode
@@ -1615,6 +1736,7 @@ void gradient_full_impl(gcpb_ctx* c, const gcpb_loss* loss) {
 
 template <typename T>
 void poisson_implicit_impl(gcpb_ctx* c, const gcpb_loss* loss) {
+  a_current(c);
   if (loss->kind != GCPB_LOSS_POISSON)
     throw std::invalid_argument(std::string("implicit gradient requires the poisson loss, got ") +
                                 loss_name(loss->kind));  // kernels.cpp:202-205
@@ -1889,6 +2011,9 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
       CK(cudaMemsetAsync(b->p, 0, bytes, c->stream));
     }
     c->grad_zero = true;
+    // Interleaved factor/gradient rows when the tables exceed L2 (GCPB_IL=0/1 forces)
+    c->il_enabled = bytes > (size_t{64} << 20);
+    if (const char* ev = getenv("GCPB_IL")) c->il_enabled = atoi(ev) != 0;
     // Privatized gradient replicas: the scatter of a small gradient (e.g. C2's
     // 51 KB) otherwise funnels every red.global into a few hundred L2 sectors,
     // where the L2 atomic units serialise per address.  Up to 32 replicas are
@@ -2502,6 +2627,13 @@ int gcpb_hot_rows(const gcpb_ctx* ctx, int* rows, int* copies) {
   return GCPB_OK;
 }
 
+int gcpb_interleaved(const gcpb_ctx* ctx, int* enabled, int* last) {
+  if (!ctx) return GCPB_ERR_USAGE;
+  if (enabled) *enabled = ctx->il_enabled ? 1 : 0;
+  if (last) *last = ctx->il_last ? 1 : 0;
+  return GCPB_OK;
+}
+
 int gcpb_synchronize(gcpb_ctx* ctx) {
   return guard(ctx, [&] { sync_and_check(ctx); });
 }
@@ -2854,6 +2986,7 @@ int gcpb_estimate(gcpb_ctx* ctx, const gcpb_loss* loss, double* out) {
 int gcpb_snapshot_save(gcpb_ctx* ctx) {
   return guard(ctx, [&] {
     const size_t bytes = ctx->nelem * ctx->tsize;
+    a_current(ctx);
     for (auto pr : {std::make_pair(&ctx->As, &ctx->A), std::make_pair(&ctx->Bs, &ctx->B),
                     std::make_pair(&ctx->Cs, &ctx->C)}) {
       pr.first->alloc(bytes);
@@ -2869,6 +3002,8 @@ int gcpb_snapshot_save(gcpb_ctx* ctx) {
 int gcpb_snapshot_restore(gcpb_ctx* ctx) {
   return guard(ctx, [&] {
     if (!ctx->have_snapshot) throw std::logic_error("no snapshot saved");
+    ctx->ag_ok = false;
+    ctx->a_stale = false;  // A is overwritten entirely
     const size_t bytes = ctx->nelem * ctx->tsize;
     for (auto pr : {std::make_pair(&ctx->A, &ctx->As), std::make_pair(&ctx->B, &ctx->Bs),
                     std::make_pair(&ctx->C, &ctx->Cs)})

@@ -501,15 +501,30 @@ __device__ __forceinline__ Vec<T> hot_rows_sum(T* __restrict__ Ghot, int slot, i
 // 16-byte chunk per array per iteration (rows are padded to 32 bytes, so a
 // chunk never straddles rows), two chunks in flight.  The last block advances
 // t (and the draw-stream base when advance_rng).
-template <typename T, bool EXTRA = false>
+// Interleaved factor/gradient table (AG, rows [A row | G row], pitch 2 rp):
+// element i0 of the contiguous layout (column col0 of its row) sits at
+// AG + 2 i0 - col0 (factor) and + rp (gradient).
+template <typename T>
+struct ILTab {
+  T* ag;  // null: no interleaved table
+  int rp;
+};
+
+template <typename T, bool EXTRA = false, bool IL = false>
 __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr,
                                            T* __restrict__ B, T* __restrict__ C, int64_t i0,
                                            int col0, int r, T* __restrict__ reps, int nrep,
                                            int64_t rep_stride, T c1, T c2, T lr, T b1, T b2,
                                            T ob1, T ob2, T eps, bool has_lb, T lb,
-                                           Vec<T> extra = Vec<T>{}) {
+                                           Vec<T> extra = Vec<T>{}, ILTab<T> il = ILTab<T>{}) {
   constexpr int VW = Vec<T>::W;
   Vec<T> a, g, b, c;
+  // IL: the factors live in AG (A is refreshed from it on demand)
+  T* const ila = IL ? il.ag + 2 * i0 - col0 : nullptr;  // this chunk's factor slot in AG
+  if (IL) {
+    Gr = ila + il.rp - i0;  // so that Gr + i0 is the chunk's gradient slot
+    A = ila - i0;           // and A + i0 its factor slot
+  }
   load_chunk(A + i0, a);
   load_chunk(B + i0, b);
   load_chunk(C + i0, c);
@@ -563,13 +578,17 @@ __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr
   store_chunk(C + i0, co);
 }
 
-template <typename T>
+// IL: factors and gradient are read from the interleaved table il.ag, the
+// gradient re-zeroed there and the updated factors written there only (the
+// host refreshes A from it when something else needs A).
+template <typename T, bool IL = false>
 __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restrict__ Gr,
                                                    T* __restrict__ B, T* __restrict__ C,
                                                    int64_t n, int rp, int r, DevState* st,
                                                    T* __restrict__ reps, int nrep,
                                                    int64_t rep_stride, int advance_rng,
-                                                   const HotAdam<T> hot) {
+                                                   const HotAdam<T> hot,
+                                                   const ILTab<T> il = ILTab<T>{}) {
   constexpr int VW = Vec<T>::W;
   __shared__ double s_c1, s_c2;
   if (threadIdx.x == 0) {
@@ -593,15 +612,15 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
     const int64_t row_off = hot.hot_off[slot];
     const Vec<T> hs = hot_rows_sum(hot.Ghot, slot, hot.rh, rp, reps, nrep, rep_stride, row_off);
     if (static_cast<int>(threadIdx.x) < rp / VW)  // gradient = copies + replicas (+ Gr)
-      adam_chunk<T, true>(A, Gr, B, C, row_off + threadIdx.x * VW,
-                          static_cast<int>(threadIdx.x) * VW, r, nullptr, 0, 0, c1, c2, lr, b1,
-                          b2, ob1, ob2, eps, has_lb, lb, hs);
+      adam_chunk<T, true, IL>(A, Gr, B, C, row_off + threadIdx.x * VW,
+                              static_cast<int>(threadIdx.x) * VW, r, nullptr, 0, 0, c1, c2, lr,
+                              b1, b2, ob1, ob2, eps, has_lb, lb, hs, il);
   } else if (nrep > 0) {  // small problems: replicas folded, simple loop
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nchunk; q += stride)
       if (hot.n == 0 || !hot_chunk(hot, static_cast<int64_t>(q) * VW, rp))
-        adam_chunk<T>(A, Gr, B, C, static_cast<int64_t>(q) * VW,
+        adam_chunk<T, false, IL>(A, Gr, B, C, static_cast<int64_t>(q) * VW,
                     static_cast<int>((q * VW) % static_cast<uint32_t>(rp)), r, reps, nrep,
-                    rep_stride, c1, c2, lr, b1, b2, ob1, ob2, eps, has_lb, lb);
+                    rep_stride, c1, c2, lr, b1, b2, ob1, ob2, eps, has_lb, lb, Vec<T>{}, il);
   } else {
     // Streaming path: U chunks per thread with all 4U loads issued before any
     // use, so enough bytes are in flight to cover HBM latency.
@@ -613,8 +632,14 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
         uint32_t q = q0 + u * stride;
         q = q < nchunk ? q : nchunk - 1;
         const int64_t i0 = static_cast<int64_t>(q) * VW;
-        load_chunk(A + i0, a[u]);
-        load_chunk_cg(Gr + i0, g[u]);
+        if (IL) {
+          const int64_t col = static_cast<int64_t>((q * VW) % static_cast<uint32_t>(rp));
+          load_chunk(il.ag + 2 * i0 - col, a[u]);
+          load_chunk_cg(il.ag + 2 * i0 - col + rp, g[u]);
+        } else {
+          load_chunk(A + i0, a[u]);
+          load_chunk_cg(Gr + i0, g[u]);
+        }
         load_chunk(B + i0, b[u]);
         load_chunk(C + i0, c[u]);
       }
@@ -639,8 +664,14 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
             ao.v[e] = av;
           }
         }
-        store_chunk(Gr + i0, Vec<T>{});
-        store_chunk(A + i0, ao);
+        if (IL) {
+          T* ila = il.ag + 2 * i0 - col0;
+          store_chunk(ila + rp, Vec<T>{});
+          store_chunk(ila, ao);
+        } else {
+          store_chunk(Gr + i0, Vec<T>{});
+          store_chunk(A + i0, ao);
+        }
         store_chunk(B + i0, bo);
         store_chunk(C + i0, co);
       }
@@ -655,6 +686,37 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
       if (advance_rng) st->rng_iter += 1;
       st->adam_done = 0;
     }
+  }
+}
+
+// AG <- [A row | 0]: (re)builds the interleaved factor/gradient table from
+// the contiguous factors (after any factor write other than the IL Adam).
+template <typename T>
+__global__ void ag_sync_kernel(const T* __restrict__ A, T* __restrict__ AG, int64_t nchunk,
+                               int rp) {
+  constexpr int VW = Vec<T>::W;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nchunk;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i0 = q * VW;
+    const int64_t col = i0 % rp;
+    Vec<T> a;
+    load_chunk(A + i0, a);
+    store_chunk(AG + 2 * i0 - col, a);
+    store_chunk(AG + 2 * i0 - col + rp, Vec<T>{});
+  }
+}
+
+// A <- AG's factor rows (A is stale after interleaved Adam updates).
+template <typename T>
+__global__ void ag_unsync_kernel(const T* __restrict__ AG, T* __restrict__ A, int64_t nchunk,
+                                 int rp) {
+  constexpr int VW = Vec<T>::W;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nchunk;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i0 = q * VW;
+    Vec<T> a;
+    load_chunk(AG + 2 * i0 - i0 % rp, a);
+    store_chunk(A + i0, a);
   }
 }
 

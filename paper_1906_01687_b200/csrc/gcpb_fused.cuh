@@ -272,7 +272,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
     for (int k = 0; k < DM; ++k) {
       if (EXACT || k < d) {
-        const int64_t ro = a.off[k] + static_cast<int64_t>(ik[k]) * a.rp;
+        const int64_t ro = a.off[k] + static_cast<int64_t>(ik[k]) * a.pitch;
         for (int b = 0; b < a.rp * static_cast<int>(sizeof(T)); b += 128) {
           prefetch_l2(reinterpret_cast<const char*>(a.A + ro) + b);
           prefetch_l2(reinterpret_cast<const char*>(a.G + ro) + b);
@@ -351,7 +351,7 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
     uint32_t roff[DM];
 #pragma unroll
     for (int k = 0; k < DM; ++k)
-      roff[k] = static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.rp);
+      roff[k] = static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.pitch);
     T row[DM][SL];
     T pre[DM][SL];
 #pragma unroll
@@ -614,7 +614,7 @@ __device__ __forceinline__ void stage_rows(const FusedArgs<T>& a, T* slot,
   if (valid) {
 #pragma unroll
     for (int k = 0; k < DM; ++k) {
-      const T* src = a.A + a.off[k] + static_cast<int64_t>(ik[k]) * a.rp;
+      const T* src = a.A + a.off[k] + static_cast<int64_t>(ik[k]) * a.pitch;
       if (pol)
         for (int c = 0; c < a.nchunks; ++c)
           cp_async16_hint(slot + k * a.rp + c * VW, src + c * VW, pol);
@@ -704,7 +704,7 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
         }
         T* gp = grad_row<T, HOT>(a, Gb,
                                  static_cast<uint32_t>(a.off[k]) +
-                                     ii[k] * static_cast<uint32_t>(a.rp),
+                                     ii[k] * static_cast<uint32_t>(a.pitch),
                                  hsv, k, rsel) +
                 cidx * VW;
         if (pol)

@@ -47,12 +47,14 @@ struct Seg {
 
 template <typename T>
 struct FusedArgs {
-  const T* A;  // factors, mode k at A + off[k], row i at + i * rp
+  const T* A;  // factors, mode k at A + off[k], row i at + i * pitch
   T* G;        // gradient (or nrep privatized replicas), same layout
   int nrep;          // gradient replicas: block b accumulates into replica b % nrep
   int64_t rep_stride;  // elements between replicas
   int d;
   int rp;      // padded row length (elements)
+  int pitch;   // elements between consecutive rows of A (and of G): rp, or 2 * rp
+               // when factor and gradient rows are interleaved ([A row | G row])
   int nchunks; // 16-byte chunks holding real columns: ceil(r / VW)
   int loss;
   T delta;

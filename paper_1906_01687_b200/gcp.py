@@ -499,6 +499,13 @@ class Engine:
         self._ck(lib.gcpb_hot_rows(self._h, C.byref(rows), C.byref(copies)))
         return rows.value, copies.value
 
+    @property
+    def interleaved(self) -> tuple:
+        """(interleaved factor/gradient table enabled, last scatter used it)."""
+        en, last = C.c_int(), C.c_int()
+        self._ck(lib.gcpb_interleaved(self._h, C.byref(en), C.byref(last)))
+        return bool(en.value), bool(last.value)
+
     def adam_reset(self) -> None:
         self._ck(lib.gcpb_adam_reset(self._h))
 

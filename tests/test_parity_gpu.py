@@ -476,7 +476,7 @@ def test_bit_and_byte_storage_agree(orc):
 @pytest.mark.parametrize("dims,r,strategy", [((60, 40, 50), 16, 2), ((30, 20, 25, 10), 8, 1),
                                              ((50, 40, 30), 20, 0)])
 def test_staged_kernel_parity(orc, monkeypatch, dims, r, strategy):
-    """The cp.async-staged kernel (used when factors exceed L2) forced on a
+    """The cp.async-staged kernel (opt-in, GCPB_STAGE=1) forced on a
     small problem: same gradient as the oracle."""
     monkeypatch.setenv("GCPB_STAGE", "1")
     g = G()
