@@ -204,8 +204,11 @@ ROOFLINE_NOTES = {
           "red.global.add.v4.f32 per launch), see DESIGN.md section 5",
     "c3": "factors (512 KB) L2-resident; bound by L2 reductions and the hash probes",
     "c4": "latency-bound: 2e5 samples per step (1.3 tiles per warp)",
-    "c5": "random 64-byte HBM access: measured bound for this pattern is 4.9e9 samples/s "
-          "(tools/randbw.cu, profiles/r01_randbw.md), i.e. frac 0.30 of streaming peak",
+    "c5": "random HBM row access (factors 531 MB): factor and gradient rows interleaved in one "
+          "128-byte line so a row gather and its reduction share a DRAM burst; ncu DRAM traffic "
+          "401 B/sample (B_alg 396) at 3.3 TB/s, long-scoreboard bound (profiles/r01_c5_il.md); "
+          "the random-access microbenchmark tops out at 6.0e9 samples/s for this mix "
+          "(tools/randbw.cu, profiles/r01_randbw.md)",
 }
 
 

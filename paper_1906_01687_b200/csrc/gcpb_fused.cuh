@@ -46,6 +46,11 @@
 #ifndef GCPB_MINB_HOT
 #define GCPB_MINB_HOT 3
 #endif
+// Same for the three-mode slim hot-row variants (C5: random HBM access, so
+// resident warps = loads in flight).
+#ifndef GCPB_MINB_HOT3
+#define GCPB_MINB_HOT3 3
+#endif
 
 namespace gcpb {
 
@@ -498,6 +503,7 @@ inline int pow2ceil(int v) {
 template <typename T, int DM, bool EXACT, bool REC>
 cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
                             int num_sms, bool* used_hot) {
+  constexpr int MHOT = DM == 3 ? GCPB_MINB_HOT3 : GCPB_MINB_HOT;
   const int nchunks = a.nchunks;
   int G = pow2ceil(nchunks);
   int vpl = 1;
@@ -531,8 +537,8 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
               if (a.rh > 0) {
                 *used_hot = true;
                 return nchunks == 5
-                           ? go(fused_grad_kernel<T, DM, EXACT, 5, 1, REC, GCPB_MINB_HOT, false, true>)
-                           : go(fused_grad_kernel<T, DM, EXACT, 6, 1, REC, GCPB_MINB_HOT, false, true>);
+                           ? go(fused_grad_kernel<T, DM, EXACT, 5, 1, REC, MHOT, false, true>)
+                           : go(fused_grad_kernel<T, DM, EXACT, 6, 1, REC, MHOT, false, true>);
               }
             }
             return nchunks == 5
@@ -544,12 +550,12 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
           if (a.rh > 0) {  // hot rows privatized (sparse, skewed modes)
             *used_hot = true;
             switch (G) {
-              case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, GCPB_MINB_HOT, false, true>);
-              case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, GCPB_MINB_HOT, false, true>);
-              case 4: return go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, GCPB_MINB_HOT, false, true>);
-              case 8: return go(fused_grad_kernel<T, DM, EXACT, 8, 1, REC, GCPB_MINB_HOT, false, true>);
-              case 16: return go(fused_grad_kernel<T, DM, EXACT, 16, 1, REC, GCPB_MINB_HOT, false, true>);
-              default: return go(fused_grad_kernel<T, DM, EXACT, 32, 1, REC, GCPB_MINB_HOT, false, true>);
+              case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, MHOT, false, true>);
+              case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, MHOT, false, true>);
+              case 4: return go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, MHOT, false, true>);
+              case 8: return go(fused_grad_kernel<T, DM, EXACT, 8, 1, REC, MHOT, false, true>);
+              case 16: return go(fused_grad_kernel<T, DM, EXACT, 16, 1, REC, MHOT, false, true>);
+              default: return go(fused_grad_kernel<T, DM, EXACT, 32, 1, REC, MHOT, false, true>);
             }
           }
         }
