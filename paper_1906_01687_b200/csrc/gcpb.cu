@@ -857,17 +857,15 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   if (a.scatter) c->hot_last = used_hot ? a.rh : 0;
   if (ev1) CK(cudaEventRecord(ev1, c->stream));
   if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
-    grad_reduce_kernel<T><<<grid_for(c->nelem, 256, c->num_sms, 4), 256, 0, c->stream>>>(
-        c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride);
-    CK(cudaGetLastError());
+    CK(launch_k(grad_reduce_kernel<T>, dim3(grid_for(c->nelem, 256, c->num_sms, 4)), dim3(256), 0,
+                c->stream, c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride));
   }
   c->hot_pending = 0;
   if (used_hot && fold) {  // the fused Adam folds the hot rows' copies itself
     c->hot_pending = a.rh;
   } else if (used_hot) {   // hot rows' copies into the gradient
-    hot_fold_kernel<T><<<c->hot_n, 256, 0, c->stream>>>(
-        c->Ghot.as<T>(), a.rh, static_cast<int>(c->rp), c->hot_off.as<int64_t>(), c->Gr.as<T>());
-    CK(cudaGetLastError());
+    CK(launch_k(hot_fold_kernel<T>, dim3(c->hot_n), dim3(256), 0, c->stream, c->Ghot.as<T>(), a.rh,
+                static_cast<int>(c->rp), c->hot_off.as<int64_t>(), c->Gr.as<T>()));
   }
 }
 
@@ -937,9 +935,9 @@ void fill_refstream(const gcpb_ctx* c, ZeroArgs& za, uint64_t key, int64_t p_ref
 
 void launch_zero_cand(const gcpb_ctx* c, int grid, const ZeroArgs& za) {
   switch (c->d) {
-    case 3: zero_cand_kernel<3><<<grid, kZcThreads, 0, c->stream>>>(za); break;
-    case 4: zero_cand_kernel<4><<<grid, kZcThreads, 0, c->stream>>>(za); break;
-    default: zero_cand_kernel<0><<<grid, kZcThreads, 0, c->stream>>>(za); break;
+    case 3: CK(launch_k(zero_cand_kernel<3>, dim3(grid), dim3(kZcThreads), 0, c->stream, za)); break;
+    case 4: CK(launch_k(zero_cand_kernel<4>, dim3(grid), dim3(kZcThreads), 0, c->stream, za)); break;
+    default: CK(launch_k(zero_cand_kernel<0>, dim3(grid), dim3(kZcThreads), 0, c->stream, za)); break;
   }
 }
 
@@ -973,13 +971,13 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   fill_refstream(c, za, seed, p_ref);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
   for (int b = 0; b < 3; ++b) {
-    zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, b == 0 ? 1 : 0);
+    CK(launch_k(zero_plan_kernel, dim3(1), dim3(1), 0, c->stream, st, b == 0 ? 1 : 0));
     launch_zero_cand(c, grid, za);
-    zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    CK(launch_k(zero_scatter_kernel, dim3(grid), dim3(kZcThreads), 0, c->stream, za));
   }
   CK(cudaGetLastError());
   if (mode == ZERO_CAPTURE) {
-    zero_check_kernel<<<1, 1, 0, c->stream>>>(st);
+    CK(launch_k(zero_check_kernel, dim3(1), dim3(1), 0, c->stream, st));
     CK(cudaGetLastError());
     return;
   }
@@ -988,9 +986,9 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
     c->pull_state();
     if (c->host_state.z_overflow) throw std::logic_error("zero sampler: status overflow");
     if (std::min(c->host_state.z_accepted, q) >= q) break;
-    zero_plan_kernel<<<1, 1, 0, c->stream>>>(st, 0);
+    CK(launch_k(zero_plan_kernel, dim3(1), dim3(1), 0, c->stream, st, 0));
     launch_zero_cand(c, grid, za);
-    zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+    CK(launch_k(zero_scatter_kernel, dim3(grid), dim3(kZcThreads), 0, c->stream, za));
     CK(cudaGetLastError());
   }
 }
@@ -1103,7 +1101,7 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
       const int grid =
           static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
       launch_zero_cand(c, grid, za);
-      zero_scatter_kernel<<<grid, kZcThreads, 0, c->stream>>>(za);
+      CK(launch_k(zero_scatter_kernel, dim3(grid), dim3(kZcThreads), 0, c->stream, za));
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(&mine, &st->z_accepted, 8, cudaMemcpyDeviceToHost, c->stream));
       c->sync();
@@ -1170,7 +1168,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     res.n = s;
     run_fused(c, a, record, fold);
     if (c->draw_stream == 1) {  // sample_uniform consumed s * d draws
-      ref_advance_kernel<<<1, 1, 0, c->stream>>>(c->dst(), static_cast<uint64_t>(s) * c->d, 0, c->d);
+      CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, c->dst(), static_cast<uint64_t>(s) * c->d, 0, c->d));
       CK(cudaGetLastError());
     }
     return res;
@@ -1227,13 +1225,13 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   run_fused(c, a, record, fold);
   if (c->draw_stream == 1) {  // p picks, then d draws per tested candidate / q draw
     if (strat && q > 0 && c->nranks > 1)
-      ref_advance_kernel<<<1, 1, 0, c->stream>>>(
-          c->dst(), static_cast<uint64_t>(p + res.stats.tested * c->d), 0, c->d);
+      CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, 
+          c->dst(), static_cast<uint64_t>(p + res.stats.tested * c->d), 0, c->d));
     else if (strat && q > 0)
-      ref_advance_kernel<<<1, 1, 0, c->stream>>>(c->dst(), static_cast<uint64_t>(p), 1, c->d);
+      CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, c->dst(), static_cast<uint64_t>(p), 1, c->d));
     else
-      ref_advance_kernel<<<1, 1, 0, c->stream>>>(c->dst(), static_cast<uint64_t>(p + q * c->d), 0,
-                                                 c->d);
+      CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, c->dst(), static_cast<uint64_t>(p + q * c->d), 0,
+                                                 c->d));
     CK(cudaGetLastError());
   }
   if (strat && q > 0 && zero_mode == ZERO_HOST_CHECK && c->nranks == 1) {
@@ -1283,18 +1281,18 @@ void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0, int hot_rh
     ILTab<T> il;
     il.ag = c->AG.as<T>();
     il.rp = static_cast<int>(c->rp);
-    adam_kernel<T, true><<<grid, 256, 0, c->stream>>>(
-        c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem,
-        static_cast<int>(c->rp), static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps,
-        c->rep_stride, advance_rng, hot, il);
+    CK(launch_k(adam_kernel<T, true>, dim3(grid), dim3(256), 0, c->stream, c->A.as<T>(),
+                c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
+                static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride,
+                advance_rng, hot, il));
     c->il_pending = false;
     c->a_stale = true;
   } else {
     a_current(c);
-    adam_kernel<T><<<grid, 256, 0, c->stream>>>(
-        c->A.as<T>(), c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem,
-        static_cast<int>(c->rp), static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps,
-        c->rep_stride, advance_rng, hot);
+    CK(launch_k(adam_kernel<T, false>, dim3(grid), dim3(256), 0, c->stream, c->A.as<T>(),
+                c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
+                static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride,
+                advance_rng, hot, ILTab<T>{}));
     c->ag_ok = false;  // A changed without AG
   }
   CK(cudaGetLastError());

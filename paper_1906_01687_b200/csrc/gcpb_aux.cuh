@@ -76,6 +76,7 @@ __host__ __device__ inline int64_t zero_batch_size_dev(double total, double zeta
 
 // Plans the next rejection batch from the device-resident shortfall.
 __global__ void zero_plan_kernel(DevState* st, int first) {
+  pdl_begin();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (first) {
     st->z_tested = 0;
@@ -203,12 +204,14 @@ __global__ void to_double_kernel(const T* __restrict__ in, double* out, int64_t 
 // RefStream: advance the counter by the draws one sampler call consumed:
 // fixed + (per_tested ? tested * d : 0)  (stratified: p + tested * d).
 __global__ void ref_advance_kernel(DevState* st, uint64_t fixed, int per_tested, int d) {
+  pdl_begin();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   st->ref_ctr += fixed + (per_tested ? static_cast<uint64_t>(st->z_tested) * d : 0ull);
 }
 
 // Graph mode: counts steps whose device-planned batches did not yield q zeros.
 __global__ void zero_check_kernel(DevState* st) {
+  pdl_begin();
   if (threadIdx.x == 0 && blockIdx.x == 0 && st->z_accepted < st->z_q) st->z_incomplete += 1;
 }
 
@@ -257,6 +260,7 @@ __device__ __forceinline__ bool bloom_maybe(const uint32_t* __restrict__ bloom, 
 // so the per-mode loops unroll over constant-bank parameters.
 template <int DM>
 __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a) {
+  pdl_begin();
   const int d = DM > 0 ? DM : a.d;
   __shared__ int s_warp_sum[kZcThreads / 32];
   __shared__ int s_warp_valid[kZcThreads / 32];
@@ -343,6 +347,7 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
 }
 
 __global__ void __launch_bounds__(kZcThreads) zero_scatter_kernel(const ZeroArgs a) {
+  pdl_begin();
   __shared__ unsigned long long s_part[kZcThreads / 32];
   DevState* st = a.st;
   const int64_t nchunks = st->z_nchunks;
@@ -589,6 +594,7 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
                                                    int64_t rep_stride, int advance_rng,
                                                    const HotAdam<T> hot,
                                                    const ILTab<T> il = ILTab<T>{}) {
+  pdl_begin();
   constexpr int VW = Vec<T>::W;
   __shared__ double s_c1, s_c2;
   if (threadIdx.x == 0) {
@@ -724,6 +730,7 @@ __global__ void ag_unsync_kernel(const T* __restrict__ AG, T* __restrict__ A, in
 template <typename T>
 __global__ void grad_reduce_kernel(T* __restrict__ G, T* __restrict__ reps, int64_t n,
                                    int nrep, int64_t stride) {
+  pdl_begin();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     T s = static_cast<T>(0);
@@ -767,6 +774,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int rh, int rp,
                                                        const int64_t* __restrict__ hot_off,
                                                        T* __restrict__ G) {
+  pdl_begin();
   constexpr int VW = Vec<T>::W;
   const Vec<T> acc =
       hot_rows_sum<T>(Ghot, static_cast<int>(blockIdx.x), rh, rp, nullptr, 0, 0, 0);

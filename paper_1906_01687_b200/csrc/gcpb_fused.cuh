@@ -454,6 +454,7 @@ template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bo
           bool HOT = false>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
                                                                int64_t total_tiles) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -525,8 +526,8 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
     const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    kern<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(a, total_tiles);
-    return cudaGetLastError();
+    return launch_k(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream, a,
+                    total_tiles);
   };
   if (vpl == 1) {
     if constexpr (!REC && EXACT) {
@@ -725,6 +726,7 @@ __device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegR
 template <typename T, int DM, int G, bool HOT = false>
 __global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T> a,
                                                               int64_t total_tiles) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -789,8 +791,8 @@ bool launch_staged(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stre
     const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    kern<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(a, total_tiles);
-    *err = cudaGetLastError();
+    *err = launch_k(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), smem, stream, a,
+                    total_tiles);
   };
   if (a.rh > 0) {
     *used_hot = true;
