@@ -207,7 +207,9 @@ int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
  * copied in before the step and the updated factors copied out to model_out
  * after it (either may be NULL).  One call, one synchronisation; page-locked
  * buffers (cudaHostAlloc / cudaHostRegister) are DMA'd in place, pageable
- * ones through the context's pinned staging block. */
+ * ones through the context's pinned staging block.  Small problems (those
+ * gcpb_run_steps runs as one cluster kernel) on page-locked in/out buffers
+ * take one launch that reads and writes the host model directly. */
 int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter, const gcpb_adam* adam, const double* model_in,
                    double* model_out);
@@ -219,8 +221,11 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
  * next synchronising call. */
 int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter0, int64_t n, const gcpb_adam* adam);
-/* Which engine ran the last gcpb_run_steps: 0 = CUDA graph of fused steps,
- * 1 = the small-problem cluster kernel (all n iterations in one launch,
+/* Which engine ran the last gcpb_run_steps (or small-problem gcpb_step_host):
+ * 0 = CUDA graph of fused steps,
+ * 1 = the small-problem cluster kernel (all n iterations in one launch;
+ * gcpb_step_host on page-locked buffers reads and writes the host model
+ * from that kernel directly,
  * chosen when uniform draws, one rank, Philox, the model fits in shared
  * memory and s*d*r <= 16384; GCPB_NO_SMALL=1 disables it). */
 int gcpb_steps_path(const gcpb_ctx* ctx);

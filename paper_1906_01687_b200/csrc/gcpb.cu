@@ -389,6 +389,16 @@ void mode_rows(const gcpb_ctx* c, int mode, int* k0, int* k1, int64_t* rows) {
 
 // Page-locked (cudaHostAlloc / cudaHostRegister) host memory can be the DMA
 // source or target itself, skipping the staging copy.
+// Device address of page-locked host memory (null when p is not mapped).
+const void* host_device_alias(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -1533,8 +1543,10 @@ bool small_eligible(const gcpb_ctx* c, const gcpb_sampler* sk) {
 template <typename T, int DM>
 void small_launch_dm(const SmallArgs<T>& a, T* G, cudaStream_t stream) {
   const size_t smem = 3 * static_cast<size_t>(a.nelem) * sizeof(T);
-  CK(cudaFuncSetAttribute(small_steps_kernel<T, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(kSmallModelMax)));
+  static const cudaError_t attr_set = cudaFuncSetAttribute(  // once per instantiation
+      small_steps_kernel<T, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      static_cast<int>(kSmallModelMax));
+  CK(attr_set);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kSmallCluster, 1, 1);
   cfg.blockDim = dim3(kSmallThreads, 1, 1);
@@ -1552,7 +1564,8 @@ void small_launch_dm(const SmallArgs<T>& a, T* G, cudaStream_t stream) {
 
 template <typename T>
 void small_launch(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint64_t seed,
-                  int64_t n) {
+                  int64_t n, const double* host_in = nullptr, double* host_out = nullptr,
+                  const uint64_t* iter = nullptr) {
   a_current(c);
   c->ag_ok = false;  // the cluster kernel writes A
   const FusedArgs<T> f = base_args<T>(c, loss, seed, 0);
@@ -1585,6 +1598,10 @@ void small_launch(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, ui
   a.tag = TAG_GRAD_UNIFORM;
   a.n_steps = n;
   a.st = c->dst();
+  a.host_in = host_in;
+  a.host_out = host_out;
+  a.iter_given = iter ? 1 : 0;
+  a.iter = iter ? *iter : 0;
   c->small_g.alloc(3 * static_cast<size_t>(c->nelem) * sizeof(T));
   if (!c->small_g_zero) {
     CK(cudaMemsetAsync(c->small_g.p, 0, 3 * static_cast<size_t>(c->nelem) * sizeof(T), c->stream));
@@ -2546,6 +2563,27 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
                    double* model_out) {
   return guard(ctx, [&] {
     check_step_args(ctx, sampler, loss);
+    // Small problems on page-locked buffers: one cluster launch reads the
+    // model from host memory, runs the iteration and writes it back (no
+    // copies or pack kernels: C1's step is launch/latency-bound).
+    if (model_in && model_out) {
+      const void* din = host_device_alias(model_in);
+      void* dout = din ? const_cast<void*>(host_device_alias(model_out)) : nullptr;
+      const bool small = ctx->dtype == GCPB_F32 ? small_eligible<float>(ctx, sampler)
+                                                : small_eligible<double>(ctx, sampler);
+      if (din && dout && small) {
+        set_adam_params(ctx, adam);
+        if (ctx->dtype == GCPB_F32)
+          small_launch<float>(ctx, sampler, loss, seed, 1, static_cast<const double*>(din),
+                              static_cast<double*>(dout), &iter);
+        else
+          small_launch<double>(ctx, sampler, loss, seed, 1, static_cast<const double*>(din),
+                               static_cast<double*>(dout), &iter);
+        ctx->last_steps_path = 1;
+        CK(cudaStreamSynchronize(ctx->stream));
+        return;
+      }
+    }
     // pinned buffers are transferred in place: the call synchronises on the
     // download before returning (without model_out, on the stream)
     if (model_in) upload(ctx, ctx->A, -1, model_in, is_pinned(model_in));

@@ -51,6 +51,12 @@
 #ifndef GCPB_MINB_HOT3
 #define GCPB_MINB_HOT3 3
 #endif
+// Four-mode hot-row variant with 8-lane groups (C3, r = 32 fp32; L2-reduction
+// bound): 4 blocks/SM at 64 registers, measured 202 -> 199 us on C3 (the
+// 5/6-lane C4 variant is faster at 3).
+#ifndef GCPB_MINB_HOT8
+#define GCPB_MINB_HOT8 4
+#endif
 
 namespace gcpb {
 
@@ -505,6 +511,7 @@ template <typename T, int DM, bool EXACT, bool REC>
 cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
                             int num_sms, bool* used_hot) {
   constexpr int MHOT = DM == 3 ? GCPB_MINB_HOT3 : GCPB_MINB_HOT;
+  constexpr int MHOT8 = DM == 4 ? GCPB_MINB_HOT8 : MHOT;
   const int nchunks = a.nchunks;
   int G = pow2ceil(nchunks);
   int vpl = 1;
@@ -554,7 +561,7 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
               case 1: return go(fused_grad_kernel<T, DM, EXACT, 1, 1, REC, MHOT, false, true>);
               case 2: return go(fused_grad_kernel<T, DM, EXACT, 2, 1, REC, MHOT, false, true>);
               case 4: return go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, MHOT, false, true>);
-              case 8: return go(fused_grad_kernel<T, DM, EXACT, 8, 1, REC, MHOT, false, true>);
+              case 8: return go(fused_grad_kernel<T, DM, EXACT, 8, 1, REC, MHOT8, false, true>);
               case 16: return go(fused_grad_kernel<T, DM, EXACT, 16, 1, REC, MHOT, false, true>);
               default: return go(fused_grad_kernel<T, DM, EXACT, 32, 1, REC, MHOT, false, true>);
             }

@@ -45,6 +45,14 @@ struct SmallArgs {
   uint32_t tag;
   int64_t n_steps;
   DevState* st;
+  // Host-model step (gcpb_step_host on page-locked buffers): the model is
+  // read from / written to host memory directly (unpadded fp64 rows, mapped
+  // into the device address space) instead of separate copies and pack
+  // kernels; the iteration is given (iter_given) rather than device-resident.
+  const double* host_in;
+  double* host_out;
+  int iter_given;
+  uint64_t iter;
 };
 
 template <typename T, int DM>
@@ -125,13 +133,31 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_steps_kernel(const Sma
   // still spread over every SM of the cluster
   const int64_t tid = static_cast<int64_t>(threadIdx.x) * ncta + cta;
   const int64_t nth = static_cast<int64_t>(ncta) * blockDim.x;
+  if (a.host_in) {
+    // padded element e <- host row e / rp, column e % rp; four host reads in
+    // flight per thread (each is a round trip over the host link)
+    for (int64_t e0 = threadIdx.x; e0 < a.nelem; e0 += 4 * static_cast<int64_t>(blockDim.x)) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x);
+        const int64_t row = e / a.rp, col = e - row * a.rp;
+        v[u] = (e < a.nelem && col < a.r) ? a.host_in[row * a.r + col] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * static_cast<int64_t>(blockDim.x);
+        if (e < a.nelem) sA[e] = static_cast<T>(v[u]);
+      }
+    }
+  }
   for (int64_t e = threadIdx.x; e < a.nelem; e += blockDim.x) {
-    sA[e] = a.A[e];
+    if (!a.host_in) sA[e] = a.A[e];
     sB[e] = a.B[e];
     sC[e] = a.C[e];
   }
   const DevState* st = a.st;
-  const uint64_t iter0 = st->rng_iter;
+  const uint64_t iter0 = a.iter_given ? a.iter : st->rng_iter;
   const int64_t t0 = st->t;
   const T lr = static_cast<T>(st->lr);
   const double beta1 = st->beta1, beta2 = st->beta2;
@@ -246,9 +272,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_steps_kernel(const Sma
       a.B[e] = sB[e];
       a.C[e] = sC[e];
     }
+    if (a.host_out)
+      for (int64_t q = threadIdx.x; q < nreal; q += blockDim.x) {
+        const int64_t row = q / a.r;
+        a.host_out[q] = static_cast<double>(sA[row * a.rp + (q - row * a.r)]);
+      }
     if (threadIdx.x == 0) {
       a.st->t = t0 + a.n_steps;
-      a.st->rng_iter = iter0 + static_cast<uint64_t>(a.n_steps);
+      if (!a.iter_given) a.st->rng_iter = iter0 + static_cast<uint64_t>(a.n_steps);
     }
   }
 }

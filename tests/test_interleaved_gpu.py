@@ -148,3 +148,36 @@ def test_interleaved_step_host(monkeypatch):
         outs.append(out)
         e.close()
     assert O.rel_error(outs[1], outs[0]) <= 2e-5
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_small_step_host_zero_copy_matches_stepping(dtype):
+    """Small problems: gcpb_step_host on page-locked buffers runs one cluster
+    launch that reads and writes the host model directly; it must equal the
+    device-resident stepping path (same draws, summation order aside)."""
+    import torch
+    g = G()
+    rs = np.random.default_rng(17)
+    dims, r = (30, 25, 20), 5
+    dense = rs.normal(size=int(np.prod(dims)))
+    F = [rs.normal(size=(n, r)) for n in dims]
+    sk, lf = g.SamplerKind.uniform(300), g.LossFunction.gaussian()
+    a, b = (g.Engine(dims, r, dtype=dtype) for _ in range(2))
+    for e in (a, b):
+        e.set_dense(dense, "f64")
+        e.set_factors(F)
+    n = sum(dims) * r
+    pin_in = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    pin_out = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    pin_in[:] = np.concatenate([f.ravel() for f in F])
+    for it in range(6):
+        a.step_host(sk, lf, 4, 100 + it, 1e-2, pin_in, pin_out)
+        pin_in[:] = pin_out
+        b.step(sk, lf, 4, 100 + it, 1e-2)
+    assert a.steps_path == "small"
+    want = np.concatenate([f.ravel() for f in b.factors()])
+    tol = 1e-10 if dtype == "f64" else 1e-5
+    assert O.rel_error(pin_out, want) <= tol
+    # the device copy of the model follows too (a later device-side call sees it)
+    assert O.rel_error(np.concatenate([f.ravel() for f in a.factors()]), want) <= tol
+    assert a.iterations == b.iterations == 6

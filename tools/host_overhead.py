@@ -1,5 +1,6 @@
 """Per-call host overhead of the C-ABI on a C1-sized problem."""
 import os, sys, time
+import torch  # before the engine: torch needs its bundled NCCL symbols
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1906_01687_b200.gcp as g
@@ -31,3 +32,13 @@ t("set_factors", lambda: e.set_factors(F))
 t("factors()", lambda: e.factors())
 t("step_host in/out", lambda: e.step_host(sk, lf, 1, 5, 1e-3, flat, out))
 t("step_host no io", lambda: e.step_host(sk, lf, 1, 5, 1e-3, None, None))
+
+# page-locked model buffers: the small-problem zero-copy step_host path
+pin_in = torch.empty(flat.size, dtype=torch.float64, pin_memory=True).numpy()
+pin_out = torch.empty(flat.size, dtype=torch.float64, pin_memory=True).numpy()
+pin_in[:] = flat
+t("step_host pinned in/out", lambda: e.step_host(sk, lf, 1, 5, 1e-3, pin_in, pin_out))
+t("run_steps(1)", lambda: (e.run_steps(sk, lf, 1, 5, 1, 1e-3), e.synchronize()))
+t("torch.cuda.synchronize", lambda: torch.cuda.synchronize())
+import paper_1906_01687_b200.gcp as gg  # noqa: E402
+t("python arg structs only", lambda: (sk.c(), lf.c(), gg.Engine._adam(1e-3)))
