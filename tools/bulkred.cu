@@ -19,13 +19,14 @@ constexpr int ROWS = 800, RF = 16, REPS = 32;
 // MODE 0: 4 lanes x red.global.add.v4.f32 per row (the engine today)
 // MODE 1: every lane stages one whole row in shared memory, one bulk reduce per lane
 // MODE 2: 4 lanes stage a row (one 16-byte chunk each), lane 0 of 4 issues the bulk reduce
-// MODE 3: 4 lanes x 4 scalar red.shared.add.f32 into a per-block shared gradient, flushed at the end
+// MODE 3: 4 lanes x 4 scalar atomicAdd (shared) into a per-block shared copy of
+//         the whole gradient (51 KB, dynamic smem), flushed with red.global at the end
 template <int MODE>
 __global__ void __launch_bounds__(256) kern(float* G, int64_t n, uint32_t seed) {
   __shared__ __align__(128) float stage[MODE == 3 ? 1 : 2][MODE == 3 ? 1 : 256][RF];
-  __shared__ float sg[MODE == 3 ? ROWS * RF / 2 : 1];
+  extern __shared__ float sg[];
   if (MODE == 3) {
-    for (int e = threadIdx.x; e < ROWS * RF / 2; e += blockDim.x) sg[e] = 0.f;
+    for (int e = threadIdx.x; e < ROWS * RF; e += blockDim.x) sg[e] = 0.f;
     __syncthreads();
   }
   const int lane4 = threadIdx.x & 3;
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(256) kern(float* G, int64_t n, uint32_t seed) 
                    : "memory");
     } else if (MODE == 3) {
       const uint32_t row = mix32(seed ^ static_cast<uint32_t>(i >> 2)) % ROWS;
-      float* p = sg + (row % (ROWS / 2)) * RF + lane4 * 4;
+      float* p = sg + row * RF + lane4 * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e) atomicAdd(p + ((e + lane4) & 3), y);
     } else if (MODE == 1) {
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(256) kern(float* G, int64_t n, uint32_t seed) 
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (MODE == 3) {
     __syncthreads();
-    for (int e = threadIdx.x; e < ROWS * RF / 2; e += blockDim.x) atomicAdd(Gb + e, sg[e]);
+    for (int e = threadIdx.x; e < ROWS * RF; e += blockDim.x) atomicAdd(Gb + e, sg[e]);
   }
 }
 
@@ -91,12 +92,14 @@ template <int MODE>
 void run(float* G, int64_t rows_total, int blocks_per_sm) {
   const int64_t n = MODE == 1 ? rows_total : rows_total * 4;  // threads-items
   const int grid = 148 * blocks_per_sm;
-  kern<MODE><<<grid, 256>>>(G, n, 1);
+  const size_t smem = MODE == 3 ? ROWS * RF * sizeof(float) : 0;
+  cudaFuncSetAttribute(kern<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  kern<MODE><<<grid, 256, smem>>>(G, n, 1);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  for (int it = 0; it < 5; ++it) kern<MODE><<<grid, 256>>>(G, n, 7 + it);
+  for (int it = 0; it < 5; ++it) kern<MODE><<<grid, 256, smem>>>(G, n, 7 + it);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0.f;
@@ -112,6 +115,10 @@ int main() {
   cudaMemset(G, 0, sizeof(float) * ROWS * RF * REPS);
   const int64_t rows_total = 64'000'000;  // C2: 1.6e7 samples x 4 modes
   for (int bps : {2, 4}) {
+    if (bps > 0) {
+      run<3>(G, rows_total, bps);
+      continue;
+    }
     run<0>(G, rows_total, bps);
     run<1>(G, rows_total, bps);
     run<2>(G, rows_total, bps);
