@@ -194,6 +194,8 @@ struct gcpb_ctx {
   bool il_enabled = false;
   bool ag_ok = false;
   bool il_pending = false;
+  bool il_gpack = false;  // sharded step: gradient packed from AG into Gr, factors in AG
+  bool in_step = false;   // inside step_impl (the interleaved table is used only there)
   bool il_last = false;  // the last fused scatter used AG (gcpb_interleaved)
   bool a_stale = false;
   DBuf Grep;            // privatized gradient replicas (L2-resident), zero at rest
@@ -827,7 +829,11 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     }
   }
   c->il_pending = false;
-  if (a.scatter && fold && !record && c->il_enabled && c->nranks == 1) {
+  c->il_gpack = false;
+  // interleaved table: iterations only (folded single-rank steps, or sharded
+  // steps whose gradient is packed back for the all-reduce)
+  const bool il = a.scatter && !record && c->il_enabled && c->in_step && (fold || c->nranks > 1);
+  if (il) {
     // interleaved table: the scatter goes to AG's gradient rows, Adam reads them
     ag_prepare<T>(c);
     a.A = c->AG.as<T>();
@@ -836,7 +842,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     for (int k = 0; k < c->d; ++k) a.off[k] = 2 * c->off[k];
     c->nrep = 1;
     a.nrep = 1;
-    c->il_pending = true;
+    c->il_pending = fold;
     c->il_last = true;
   } else if (a.scatter) {
     a_current(c);
@@ -866,6 +872,12 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot));
   if (a.scatter) c->hot_last = used_hot ? a.rh : 0;
   if (ev1) CK(cudaEventRecord(ev1, c->stream));
+  if (il && !fold) {  // the all-reduce needs the gradient contiguous
+    const int64_t nchunk = c->nelem / c->vw;
+    CK(launch_k(ag_pack_kernel<T>, dim3(grid_for(nchunk, 256, c->num_sms, 8)), dim3(256), 0,
+                c->stream, c->AG.as<T>(), c->Gr.as<T>(), nchunk, static_cast<int>(c->rp)));
+    c->il_gpack = true;
+  }
   if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
     CK(launch_k(grad_reduce_kernel<T>, dim3(grid_for(c->nelem, 256, c->num_sms, 4)), dim3(256), 0,
                 c->stream, c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride));
@@ -1287,15 +1299,17 @@ void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0, int hot_rh
     }
   }
   const int grid = grid_for(c->nelem / c->vw, 256, c->num_sms, 8) + hot.n;
-  if (c->il_pending) {  // gradient in AG's gradient rows; factors written to A and AG
+  if (c->il_pending || c->il_gpack) {  // factors (and unless packed, the gradient) in AG
     ILTab<T> il;
     il.ag = c->AG.as<T>();
     il.rp = static_cast<int>(c->rp);
+    il.gcontig = c->il_gpack ? 1 : 0;
     CK(launch_k(adam_kernel<T, true>, dim3(grid), dim3(256), 0, c->stream, c->A.as<T>(),
                 c->Gr.as<T>(), c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp),
                 static_cast<int>(c->r), c->dst(), c->Grep.as<T>(), fold_reps, c->rep_stride,
                 advance_rng, hot, il));
     c->il_pending = false;
+    c->il_gpack = false;
     c->a_stale = true;
   } else {
     a_current(c);
@@ -1473,31 +1487,38 @@ void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint6
                uint64_t iter, const uint64_t* iter_base, int zero_mode) {
   const bool multi = c->nranks > 1;
   try {
+    c->in_step = true;
     stoch_grad_impl<T>(c, sk, loss, seed, iter, true, false, zero_mode == ZERO_HOST_CHECK, false,
                        -1, iter_base, /*fold=*/!multi, zero_mode);
+    c->in_step = false;
+    int fold = 0;
+    if (multi) {
+      if (!has_comm(c)) throw std::logic_error("sharded step without a communicator");
+      if (!c->comm && zero_mode == ZERO_CAPTURE)
+        throw std::invalid_argument("graph-replayed multi-rank steps need an NCCL communicator");
+      comm_allreduce_grad<T>(c);
+    } else if (c->nrep > 1) {
+      fold = c->nrep;
+    }
+    adam_launch<T>(c, fold, iter_base ? 1 : 0, c->hot_pending);
   } catch (...) {
+    c->in_step = false;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(c->stream, &cs);
-    if (c->il_pending && cs == cudaStreamCaptureStatusNone) {
-      // AG's gradient rows may hold a partial scatter: keep its factor rows
-      // (A refreshed from them) and rebuild AG on the next interleaved step
+    if ((c->il_pending || c->il_gpack) && cs == cudaStreamCaptureStatusNone) {
+      // AG's gradient rows (or Gr) may hold a partial gradient: keep AG's
+      // factor rows (A refreshed from them), rebuild AG on the next
+      // interleaved step, re-zero Gr on the next use
       c->il_pending = false;
+      c->il_gpack = false;
       a_current(c);
       c->ag_ok = false;
+      c->grad_zero = false;
     }
     c->il_pending = false;
+    c->il_gpack = false;
     throw;
   }
-  int fold = 0;
-  if (multi) {
-    if (!has_comm(c)) throw std::logic_error("sharded step without a communicator");
-    if (!c->comm && zero_mode == ZERO_CAPTURE)
-      throw std::invalid_argument("graph-replayed multi-rank steps need an NCCL communicator");
-    comm_allreduce_grad<T>(c);
-  } else if (c->nrep > 1) {
-    fold = c->nrep;
-  }
-  adam_launch<T>(c, fold, iter_base ? 1 : 0, c->hot_pending);
   c->hot_pending = 0;
   c->grad_zero = true;
 }
@@ -1647,7 +1668,7 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     return;
   }
   c->last_steps_path = 0;
-  const bool il = c->il_enabled && c->nranks == 1;
+  const bool il = c->il_enabled;
   if (il)
     ag_prepare<T>(c);  // not inside the capture
   else

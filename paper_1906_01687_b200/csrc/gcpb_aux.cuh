@@ -513,6 +513,7 @@ template <typename T>
 struct ILTab {
   T* ag;  // null: no interleaved table
   int rp;
+  int gcontig;  // 1: the gradient was packed into the contiguous Gr (sharded steps)
 };
 
 template <typename T, bool EXTRA = false, bool IL = false>
@@ -527,8 +528,8 @@ __device__ __forceinline__ void adam_chunk(T* __restrict__ A, T* __restrict__ Gr
   // IL: the factors live in AG (A is refreshed from it on demand)
   T* const ila = IL ? il.ag + 2 * i0 - col0 : nullptr;  // this chunk's factor slot in AG
   if (IL) {
-    Gr = ila + il.rp - i0;  // so that Gr + i0 is the chunk's gradient slot
-    A = ila - i0;           // and A + i0 its factor slot
+    if (!il.gcontig) Gr = ila + il.rp - i0;  // so that Gr + i0 is the chunk's gradient slot
+    A = ila - i0;                            // and A + i0 its factor slot
   }
   load_chunk(A + i0, a);
   load_chunk(B + i0, b);
@@ -641,7 +642,7 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
         if (IL) {
           const int64_t col = static_cast<int64_t>((q * VW) % static_cast<uint32_t>(rp));
           load_chunk(il.ag + 2 * i0 - col, a[u]);
-          load_chunk_cg(il.ag + 2 * i0 - col + rp, g[u]);
+          load_chunk_cg(il.gcontig ? Gr + i0 : il.ag + 2 * i0 - col + rp, g[u]);
         } else {
           load_chunk(A + i0, a[u]);
           load_chunk_cg(Gr + i0, g[u]);
@@ -672,7 +673,7 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
         }
         if (IL) {
           T* ila = il.ag + 2 * i0 - col0;
-          store_chunk(ila + rp, Vec<T>{});
+          store_chunk(il.gcontig ? Gr + i0 : ila + rp, Vec<T>{});
           store_chunk(ila, ao);
         } else {
           store_chunk(Gr + i0, Vec<T>{});
@@ -709,6 +710,23 @@ __global__ void ag_sync_kernel(const T* __restrict__ A, T* __restrict__ AG, int6
     load_chunk(A + i0, a);
     store_chunk(AG + 2 * i0 - col, a);
     store_chunk(AG + 2 * i0 - col + rp, Vec<T>{});
+  }
+}
+
+// Gr <- AG's gradient rows, which are re-zeroed (sharded steps: the
+// all-reduce needs the gradient contiguous).
+template <typename T>
+__global__ void ag_pack_kernel(T* __restrict__ AG, T* __restrict__ Gr, int64_t nchunk, int rp) {
+  pdl_begin();
+  constexpr int VW = Vec<T>::W;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nchunk;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i0 = q * VW;
+    T* g = AG + 2 * i0 - i0 % rp + rp;
+    Vec<T> v;
+    load_chunk_cg(g, v);
+    store_chunk(g, Vec<T>{});
+    store_chunk(Gr + i0, v);
   }
 }
 

@@ -181,3 +181,65 @@ def test_small_step_host_zero_copy_matches_stepping(dtype):
     # the device copy of the model follows too (a later device-side call sees it)
     assert O.rel_error(np.concatenate([f.ravel() for f in a.factors()]), want) <= tol
     assert a.iterations == b.iterations == 6
+
+
+def test_interleaved_sharded_steps_match_single_rank(monkeypatch):
+    """Sharded steps on the interleaved table (host-callback communicator, two
+    contexts on one GPU): the scatter goes to AG, is packed into the
+    contiguous gradient for the all-reduce, and Adam updates AG's factor rows;
+    the replicas must equal a single-rank run on the plain layout."""
+    import threading
+    monkeypatch.setenv("GCPB_HOT_T", "4")
+    g = G()
+    rs = np.random.default_rng(29)
+    dims, r = (40, 30, 20, 10), 8
+    coords, vals = _zipf_coords(rs, dims, 2000)
+    F = [rs.uniform(0.1, 1.0, (n, r)) for n in dims]
+    sk, lf = g.SamplerKind.semi_stratified(6000, 6000), g.LossFunction.poisson()
+    single = _engine(g, monkeypatch, False, dims, r, "f64", coords, vals, F)
+    for it in range(4):
+        single.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+    want = _flat(single)
+    monkeypatch.setenv("GCPB_IL", "1")
+    n = 2
+    barrier, slots = threading.Barrier(n), [None] * n
+
+    def allgather(rank, v):
+        slots[rank] = v
+        barrier.wait()
+        out = list(slots)
+        barrier.wait()
+        return out
+
+    def allreduce(rank, arr):
+        slots[rank] = arr.copy()
+        barrier.wait()
+        total = np.sum(slots, axis=0)
+        barrier.wait()
+        arr[:] = total
+
+    out, err = [None] * n, []
+
+    def worker(rank):
+        try:
+            e = g.Engine(dims, r, "f64")
+            e.set_sparse(coords, vals)
+            e.set_factors(F)
+            e.comm_init_host(rank, n, lambda v: allgather(rank, v), lambda a: allreduce(rank, a))
+            for it in range(4):
+                e.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+            out[rank] = (_flat(e), e.interleaved, e.hot_rows[1])
+        except Exception as ex:  # pragma: no cover - surfaced below
+            err.append(ex)
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    for flat, il, copies in out:
+        assert il == (True, True)
+        assert copies >= 2
+        assert O.rel_error(flat, want) <= 1e-12
