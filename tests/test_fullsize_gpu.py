@@ -118,5 +118,19 @@ def test_c5_fullsize_semistratified_draws_and_replay():
     e.mttkrp_samples(out["idx"], out["y"])
     replay = e.grad_flat()
     assert O.rel_error(fused, replay) <= 1e-5
+    # the iteration on the interleaved factor/gradient table (C5's factors
+    # exceed L2) equals the plain gradient + plain Adam on the same draws
+    assert e.interleaved[0]
+    full = g.SamplerKind.semi_stratified(w.p, w.q)
+    lb = w.lower_bound
+    e.snapshot_save()
+    e.step(full, loss, 3005, 14, 1e-3, lower_bound=lb)
+    assert e.interleaved[1]
+    f_il = np.concatenate([f.ravel() for f in e.factors()])
+    e.snapshot_restore()
+    e.stoch_grad(full, loss, 3005, 14)
+    e.adam_step(1e-3, lower_bound=lb)
+    f_plain = np.concatenate([f.ravel() for f in e.factors()])
+    assert O.rel_error(f_il, f_plain) <= 1e-5
     del e
     gc.collect()
