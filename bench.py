@@ -410,6 +410,17 @@ def run_ours(args, w):
                                             "scattered factor rows)",
                 "units_per_launch": w.samples_per_step, "peak_source": peak_src,
                 "note": ROOFLINE_NOTES.get(w.name, "")}
+    if w.name in ("c2", "c3"):
+        # L2-resident factors: the binding ceiling is the L2 vector-reduction
+        # rate, measured by tools/bulkred.cu (profiles/r01_bulkred.md: 6.4e7
+        # 64-byte rows = 2.56e8 red.global.add.v4 in 0.794 ms)
+        F = 4 if w.dtype == "f32" else 8
+        reds = w.samples_per_step * w.d * ((w.rank * F + 15) // 16)
+        red_rate = reds / (fused_ms / 1e3)
+        roofline["binding"] = {"limit": "L2 vector reductions (red.global.add.v4.f32)",
+                               "achieved": float("%.4g" % red_rate), "peak": 3.22e11,
+                               "unit": "reductions/s", "frac": round(red_rate / 3.22e11, 3),
+                               "source": "tools/bulkred.cu, profiles/r01_bulkred.md"}
 
     # e2e through the C-ABI with host buffers: every step copies the model in
     # from pinned host memory, runs the iteration, and copies the updated
