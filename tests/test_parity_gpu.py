@@ -397,6 +397,39 @@ def test_stratified_small_q_needs_several_batches(orc):
         assert (st.tested, st.accepted, st.rejected) == want["stats"]
 
 
+def test_stratified_graph_batches_match_stepping():
+    """Graph-replayed steps plan rejection batches 2 and 3 on the device (the
+    previous batch's last scatter block) on a reduced grid: on a dense-ish
+    tensor where the first batch often falls short they must give the same
+    iterations as host-checked stepping; a problem three batches cannot
+    satisfy is reported at the next synchronisation."""
+    g = G()
+    rs = np.random.default_rng(8)
+    dims, r = (5, 4, 3), 3
+    lin = np.nonzero(rs.random(60) < 0.7)[0]
+    coords = np.stack(np.unravel_index(lin, dims, order="F"), 1)
+    F = [rs.uniform(0.1, 1.0, (n, r)) for n in dims]
+    sk, lf = g.SamplerKind.stratified(3, 4, 1.05), g.LossFunction.bernoulli_odds()
+    ok = 0
+    for seed in range(12):
+        a, b = (g.Engine(dims, r, dtype="f64") for _ in range(2))
+        for e in (a, b):
+            e.set_sparse(coords, np.ones(len(lin)))
+            e.set_factors(F)
+        try:
+            a.run_steps(sk, lf, seed, 0, 3, 1e-2, lower_bound=0.0)
+            a.synchronize()
+        except RuntimeError as ex:  # more than three batches needed by some step
+            assert "fewer than q zeros" in str(ex)
+            continue
+        for it in range(3):
+            b.step(sk, lf, seed, it, 1e-2, lower_bound=0.0)
+        for x, y in zip(a.factors(), b.factors()):
+            assert O.rel_error(x, y) <= 1e-12
+        ok += 1
+    assert ok >= 6
+
+
 def test_seed_and_iteration_determinism():
     g = G()
     rs = np.random.default_rng(99)
