@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
                                                    T* __restrict__ reps, int nrep,
                                                    int64_t rep_stride, int advance_rng,
                                                    const HotAdam<T> hot,
-                                                   const ILTab<T> il = ILTab<T>{}) {
+                                                   const ILTab<T> il = ILTab<T>{}, int lp = 1) {
   pdl_begin();
   constexpr int VW = Vec<T>::W;
   __shared__ double s_c1, s_c2;
@@ -622,12 +622,50 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
       adam_chunk<T, true, IL>(A, Gr, B, C, row_off + threadIdx.x * VW,
                               static_cast<int>(threadIdx.x) * VW, r, nullptr, 0, 0, c1, c2, lr,
                               b1, b2, ob1, ob2, eps, has_lb, lb, hs, il);
-  } else if (nrep > 0) {  // small problems: replicas folded, simple loop
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nchunk; q += stride)
-      if (hot.n == 0 || !hot_chunk(hot, static_cast<int64_t>(q) * VW, rp))
-        adam_chunk<T, false, IL>(A, Gr, B, C, static_cast<int64_t>(q) * VW,
-                    static_cast<int>((q * VW) % static_cast<uint32_t>(rp)), r, reps, nrep,
-                    rep_stride, c1, c2, lr, b1, b2, ob1, ob2, eps, has_lb, lb, Vec<T>{}, il);
+  } else if (nrep > 0) {
+    // Small problems: the replicas are folded here.  lp lanes share a chunk,
+    // each summing (and re-zeroing) replicas j, j + lp, ... with up to four
+    // loads in flight, so the fold is one or two L2 round trips instead of
+    // nrep / 4 (C2: 32 replicas); a fixed xor-shuffle tree combines them and
+    // lane 0 applies the update.
+    const uint32_t total = nchunk * static_cast<uint32_t>(lp);
+    for (uint32_t t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; t0 < total; t0 += stride) {
+      const uint32_t t = t0 + (threadIdx.x & 31u);
+      const bool in = t < total;
+      const uint32_t q = t / static_cast<uint32_t>(lp);
+      const int j = static_cast<int>(t % static_cast<uint32_t>(lp));
+      const int64_t i0 = static_cast<int64_t>(in ? q : 0u) * VW;
+      Vec<T> g;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) g.v[e] = static_cast<T>(0);
+      for (int rr = j; in && rr < nrep; rr += 4 * lp) {
+        Vec<T> x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (rr + u * lp < nrep) {
+            load_chunk_cg(reps + (rr + u * lp) * rep_stride + i0, x[u]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VW; ++e) x[u].v[e] = static_cast<T>(0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (rr + u * lp < nrep) {
+#pragma unroll
+            for (int e = 0; e < VW; ++e) g.v[e] += x[u].v[e];
+            store_chunk(reps + (rr + u * lp) * rep_stride + i0, Vec<T>{});
+          }
+        }
+      }
+      for (int o = lp / 2; o > 0; o >>= 1) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) g.v[e] += __shfl_xor_sync(0xffffffffu, g.v[e], o);
+      }
+      if (in && j == 0 && (hot.n == 0 || !hot_chunk(hot, i0, rp)))
+        adam_chunk<T, true, IL>(A, Gr, B, C, i0, static_cast<int>(i0 % rp), r, nullptr, 0, 0, c1,
+                                c2, lr, b1, b2, ob1, ob2, eps, has_lb, lb, g, il);
+    }
   } else {
     // Streaming path: U chunks per thread with all 4U loads issued before any
     // use, so enough bytes are in flight to cover HBM latency.
