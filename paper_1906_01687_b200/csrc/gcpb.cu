@@ -672,9 +672,12 @@ int64_t finish_segments(FusedArgs<T>& a) {
   return tiles;
 }
 
+constexpr int kHotRows = 32;  // hot rows per mode
+
 // Replicas worth using for a scatter of n samples: contention scales with the
-// updates per 16-byte gradient chunk; one replica per ~4 updates per chunk,
-// capped by what is allocated (GCPB_REPLICAS forces the count).
+// updates per 16-byte gradient chunk; one replica per ~4 updates per chunk on
+// average, or per ~128 updates of a row of the shortest mode, capped by what
+// is allocated (GCPB_REPLICAS forces the count).
 int replicas_for(const gcpb_ctx* c, int64_t n) {
   if (c->nrep_cap < 2) return 1;
   static const int forced = [] {
@@ -683,13 +686,19 @@ int replicas_for(const gcpb_ctx* c, int64_t n) {
   }();
   if (forced > 0) return std::min(forced, c->nrep_cap);
   const int64_t chunks = std::max<int64_t>(1, c->nelem / c->vw);
-  const int64_t want = n / (4 * chunks);
+  int64_t want = n / (4 * chunks);
+  // short modes concentrate the reductions: a mode with n_k rows sees about
+  // n / n_k per row; keep that under ~128 per replica (C4's 183-row mode:
+  // R 2 -> 8, step 34.8 -> 32.6 us)
+  // (modes of at most kHotRows rows are covered by hot-row copies on sparse data)
+  for (int k = 0; k < c->d; ++k)
+    if (c->tensor_kind != 2 || c->dims[k] > kHotRows)
+      want = std::max<int64_t>(want, n / (128 * std::max<int64_t>(1, c->dims[k])));
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, c->nrep_cap)));
 }
 
 // Hot-row selection: per mode, up to kHotRows rows holding at
 // least 1/1024 of the nonzeros each, from a device histogram of the records.
-constexpr int kHotRows = 32;
 constexpr int kHotCopiesMax = 256;
 
 void ensure_hot(gcpb_ctx* c) {
