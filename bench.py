@@ -402,6 +402,8 @@ def run_ours(args, w):
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
                 "frac": round(achieved / peak_gbs, 4), "traffic": traffic,
+                # also against the north star's nominal 8.0 TB/s
+                "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
                 "kernel": kernel_name,
                 "kernel_ms": round(fused_ms, 4),
                 "kernel_share_of_step": round(fused_ms / ms_per_step, 3),
