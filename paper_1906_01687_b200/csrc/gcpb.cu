@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -54,6 +55,12 @@ void nck(ncclResult_t r, const char* what) {
 }
 
 // Simple owning device buffer.
+// Bumped whenever device scratch is (re)allocated or freed: part of the key
+// of the cached step graph (gcpb_run_steps), which holds raw buffer
+// addresses -- a buffer regrown by a plain call in between must not be
+// replayed through a stale graph.
+std::atomic<uint64_t> g_dbuf_gen{0};
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -62,7 +69,10 @@ struct DBuf {
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      g_dbuf_gen.fetch_add(1, std::memory_order_relaxed);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -71,6 +81,7 @@ struct DBuf {
     reset();
     if (n == 0) n = 16;
     ck(cudaMalloc(&p, n), "cudaMalloc");
+    g_dbuf_gen.fetch_add(1, std::memory_order_relaxed);
     bytes = n;
   }
   template <typename T>
@@ -1554,7 +1565,8 @@ std::string steps_key(const gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss
                 static_cast<unsigned long long>(seed), static_cast<long long>(n),
                 static_cast<long long>(c->tensor_version), c->rank, c->nranks,
                 c->hash_ready ? 1 : 0);
-  return std::string(buf) + (c->draw_stream ? "|ref" : "|philox");
+  return std::string(buf) + (c->draw_stream ? "|ref" : "|philox") + "|g" +
+         std::to_string(g_dbuf_gen.load(std::memory_order_relaxed));
 }
 
 // Small problems (model L2-resident, few samples, uniform draws, one rank,

@@ -81,6 +81,32 @@ def test_run_steps_graph_equals_stepping(kind):
         assert O.rel_error(x, y) <= 1e-10
 
 
+def test_run_steps_graph_recaptured_after_scratch_regrows():
+    """A plain step with a larger zero budget regrows the zero-sampler scratch
+    (the old buffer is freed); replaying the cached step graph afterwards must
+    not touch the freed buffer: the graph key carries the scratch generation,
+    so the graph is re-captured and the run equals plain stepping."""
+    g = G()
+    rs = np.random.default_rng(3)
+    dims, r = (40, 30, 20), 8
+    coords, vals = _sparse(rs, dims, 0.02)
+    F = [rs.uniform(0.1, 1, (n, r)) for n in dims]
+    a, b = g.Engine(dims, r, "f64"), g.Engine(dims, r, "f64")
+    for e in (a, b):
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+    lf = g.LossFunction.bernoulli_odds()
+    small, big = g.SamplerKind.stratified(500, 2000), g.SamplerKind.stratified(500, 20000)
+    a.run_steps(small, lf, 6, 0, 3, 1e-2, lower_bound=0.0)
+    a.step(big, lf, 6, 3, 1e-2, lower_bound=0.0)
+    a.run_steps(small, lf, 6, 4, 3, 1e-2, lower_bound=0.0)
+    for it in range(7):
+        b.step(big if it == 3 else small, lf, 6, it, 1e-2, lower_bound=0.0)
+    for x, y in zip(a.factors(), b.factors()):
+        assert O.rel_error(x, y) <= 1e-10
+    assert a.iterations == b.iterations == 7
+
+
 def _expected_init(orc, seed, dims, r, data_norm):
     """Reference init (kruskal.cpp:33-45, 85-93) via the restated RngStream."""
     import ctypes as C
