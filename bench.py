@@ -212,11 +212,14 @@ ROOFLINE_NOTES = {
 }
 
 
-def launches_per_step(w, hot, world):
+def launches_per_step(w, hot, world, interleaved=False):
     # fused kernel + adam (which folds the hot-row copies; sharded steps fold
     # them before the all-reduce instead); the stratified zero sampler adds
-    # 3 x (plan + candidate test + scatter) + a shortfall check
-    return 2 + (1 if hot and world > 1 else 0) + (10 if w.sampler == "stratified" else 0)
+    # 3 x (plan + candidate test + scatter) + a shortfall check; on the
+    # interleaved table the unrestricted draws are put in mode-0 row order
+    # first (count, scan init, scan, scatter)
+    return (2 + (1 if hot and world > 1 else 0) + (10 if w.sampler == "stratified" else 0)
+            + (4 if interleaved and w.sampler == "semi-stratified" else 0))
 
 
 # ---------------------------------------------------------------------------
@@ -483,7 +486,7 @@ def run_ours(args, w):
                             "fused sample+eval+MTTKRP kernel + (all-reduce) + fused Adam; K steps "
                             "replayed as one CUDA graph")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w, hot_copies > 0, world) * K, "clocks": clk,
+        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w, hot_copies > 0, world, e.interleaved[0]) * K, "clocks": clk,
         "impl": "ours",
     }
     if rank == 0:

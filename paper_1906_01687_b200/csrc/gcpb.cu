@@ -90,6 +90,13 @@ struct DBuf {
   }
 };
 
+// Scratch of one ordered sample list (order_build).
+struct OrderBufs {
+  DBuf out, cnt, tmp;
+  int64_t out_cap = 0, bins_cap = 0;
+  size_t tmp_bytes = 0;
+};
+
 const char* loss_name(int kind) {
   switch (kind) {
     case GCPB_LOSS_GAUSSIAN: return "gaussian";
@@ -270,6 +277,8 @@ struct gcpb_ctx {
 
   // stratified zero sampler
   DBuf zero_list, zstatus, ztbits;
+  // sampled segments in memory order (large tables): q draws, nonzero picks
+  OrderBufs qorder, porder;
   int64_t zero_cap = 0, zstatus_cap = 0, z_nchunks_first = 0;
 
   // estimator
@@ -1166,6 +1175,147 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
   return kept_local;
 }
 
+// ---- sampled segments walked in memory order (tables beyond L2) -----------
+// For factor tables beyond L2 (the interleaved table), sampled segments can
+// be walked in an order with locality instead of ordinal order:
+// * the q unrestricted draws of semi-stratified sampling (samplers.hpp:
+//   211-216): ordinals t sorted by the block of their mode-0 row (the row
+//   recomputed exactly as phase_a draws it), walked as a SEG_ZERO_LIST
+//   segment of the same tag;
+// * the nonzero picks (samplers.hpp:149-151,195-199): the drawn nonzero
+//   ordinals e themselves, sorted by block, read by phase_a instead of being
+//   drawn (FusedArgs::pick_list) -- the COO is in linear-key order, so the
+//   sweep visits the last mode's rows in order and the record gathers run
+//   forward through the table (opt-in, GCPB_SORTP=1: measured slower, the
+//   sorted picks pile reductions onto the same last-mode rows).
+// A counting sort (count, scan, scatter); same draws, same weights, only the
+// gradient's summation order changes.
+struct SortSpec {
+  uint64_t seed, iter;
+  const uint64_t* iter_base;
+  uint32_t tag;
+  int kind;  // 0: q draws by mode-0 row (value t); 1: picks by nonzero ordinal (value e)
+  int64_t b0, n;
+  uint64_t range;  // n_0 (kind 0) or eta (kind 1)
+  uint32_t thr;    // Lemire threshold of range (32-bit draws)
+  int shift;
+};
+
+__device__ __forceinline__ void sort_item(const SortSpec& sp, uint64_t it, uint64_t t,
+                                          uint32_t* bin, uint64_t* val) {
+  uint64_t key;
+  if (sp.range <= (1ull << 32)) {  // phase_a: group 0, word 0, attempt 0 first
+    const U4 b = philox_block(sp.seed, sp.tag, 0u, 0u, it, t);
+    const uint64_t prod = static_cast<uint64_t>(b.x) * sp.range;
+    key = (static_cast<uint32_t>(prod) >= sp.thr)
+              ? (prod >> 32)
+              : bounded32_from(sp.seed, sp.tag, it, t, 0, sp.range, sp.thr, 1u);
+  } else {
+    key = bounded64(sp.seed, sp.tag, it, t, 0, sp.range);
+  }
+  *bin = static_cast<uint32_t>(key >> sp.shift);
+  *val = sp.kind == 0 ? t : key;
+}
+
+__global__ void __launch_bounds__(256) order_count_kernel(SortSpec sp, uint32_t* cnt) {
+  const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t bin;
+    uint64_t v;
+    sort_item(sp, it, static_cast<uint64_t>(sp.b0 + i), &bin, &v);
+    atomicAdd(cnt + bin, 1u);
+  }
+}
+
+__global__ void __launch_bounds__(256) order_scatter_kernel(SortSpec sp, uint32_t* cursor,
+                                                            uint64_t* out) {
+  const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t bin;
+    uint64_t v;
+    sort_item(sp, it, static_cast<uint64_t>(sp.b0 + i), &bin, &v);
+    out[atomicAdd(cursor + bin, 1u)] = v;
+  }
+}
+
+bool order_picks() {
+  const char* e = getenv("GCPB_SORTP");
+  return e != nullptr && atoi(e) != 0;
+}
+
+bool order_wanted(const gcpb_ctx* c) {
+  const char* e = getenv("GCPB_SORTQ");
+  return e ? atoi(e) != 0 : c->il_enabled;
+}
+
+// Writes the ordered list for sp into ob.out; false when it cannot (scratch
+// too small inside a graph capture): the caller walks ordinal order instead.
+bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
+  if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
+  const int64_t nbins = static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1;
+  if (nbins >= (int64_t{1} << 31)) return false;
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<uint32_t*>(nullptr),
+                                   static_cast<uint32_t*>(nullptr), static_cast<int>(nbins),
+                                   c->stream));
+  if (sp.n > ob.out_cap || nbins > ob.bins_cap || tmp > ob.tmp_bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return false;
+    if (sp.n > ob.out_cap) {
+      ob.out.alloc(static_cast<size_t>(sp.n) * sizeof(uint64_t));
+      ob.out_cap = sp.n;
+    }
+    if (nbins > ob.bins_cap) {
+      ob.cnt.alloc(static_cast<size_t>(2 * nbins) * sizeof(uint32_t));
+      ob.bins_cap = nbins;
+    }
+    if (tmp > ob.tmp_bytes) {
+      ob.tmp.alloc(tmp);
+      ob.tmp_bytes = tmp;
+    }
+  }
+  uint32_t* cnt = ob.cnt.as<uint32_t>();
+  uint32_t* cur = cnt + nbins;
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((sp.n + 255) / 256, static_cast<int64_t>(c->num_sms) * 8)));
+  CK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nbins) * sizeof(uint32_t), c->stream));
+  order_count_kernel<<<grid, 256, 0, c->stream>>>(sp, cnt);
+  CK(cudaGetLastError());
+  size_t tb = ob.tmp_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(ob.tmp.p, tb, cnt, cur, static_cast<int>(nbins), c->stream));
+  order_scatter_kernel<<<grid, 256, 0, c->stream>>>(sp, cur, ob.out.as<uint64_t>());
+  CK(cudaGetLastError());
+  return true;
+}
+
+template <typename T>
+SortSpec order_spec(const FusedArgs<T>& a, uint32_t tag, int kind, int64_t b0, int64_t b1) {
+  SortSpec sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.seed = a.seed;
+  sp.iter = a.iter;
+  sp.iter_base = a.iter_base;
+  sp.tag = tag;
+  sp.kind = kind;
+  sp.b0 = b0;
+  sp.n = b1 - b0;
+  if (kind == 0) {
+    sp.range = a.dims[0];
+    sp.thr = a.thr[0];
+    sp.shift = 6;  // 64 mode-0 rows per bin
+  } else {
+    sp.range = a.eta;
+    sp.thr = a.thr_eta;
+    int sh = 0;
+    while ((a.eta >> sh) > (1ull << 21)) ++sh;  // <= 2M bins (records of one bin: a few KB)
+    sp.shift = sh;
+  }
+  return sp;
+}
+
 struct SampleResult {
   int64_t n = 0;
   gcpb_stats stats{0, 0, 0};
@@ -1247,10 +1397,21 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     a.zero_list = c->zero_list.as<uint64_t>();
   }
   a.nseg = 0;
+  const bool ordered = scatter && !record && est_kind < 0 && c->draw_stream == 0 &&
+                       order_wanted(c);
   if (p > 0) {
     gcpb_shard_range(p, c->rank, c->nranks, &b0, &b1);
-    a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p,
-                               (!strat && est_kind < 0) ? 1 : 0, 0);
+    // (walking the picks in COO order -- FusedArgs::pick_list -- measured
+    // slower on C5: fused 2.84 -> 3.11 ms plus 0.5 ms of ordering; opt-in
+    // GCPB_SORTP=1)
+    const int pflag = (!strat && est_kind < 0) ? 1 : 0;
+    if (ordered && order_picks() && a.eta > 0 &&
+        order_build(c, c->porder, order_spec(a, tag_p, 1, b0, b1))) {
+      a.pick_list = c->porder.out.as<uint64_t>();  // the drawn ordinals, in COO order
+      a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, 0, b1 - b0, eta_over_p, pflag, 0);
+    } else {
+      a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p, pflag, 0);
+    }
   }
   if (q > 0) {
     const double zeta_d = static_cast<double>(zeta128);
@@ -1259,8 +1420,14 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
                                  zeta_d / static_cast<double>(q), 0, p, p);
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
-      a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1,
-                                 c->total_d / static_cast<double>(q), 0, p, p);
+      const double wq = c->total_d / static_cast<double>(q);
+      if (ordered &&
+          order_build(c, c->qorder, order_spec(a, TAG_GRAD_SEMI_Q, 0, b0, b1))) {
+        a.zero_list = c->qorder.out.as<uint64_t>();  // the same draws, in mode-0 row order
+        a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
+      } else {
+        a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1, wq, 0, p, p);
+      }
     }
   }
   res.n = p + q;

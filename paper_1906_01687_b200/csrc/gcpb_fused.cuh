@@ -174,7 +174,9 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
     }
   } else if (kind == SEG_PICK) {
     uint64_t e;
-    if (a.refstream) {
+    if (a.pick_list) {  // drawn beforehand, in nonzero order (order_build)
+      e = a.pick_list[t];
+    } else if (a.refstream) {
       e = refstream_below(a.ref_key, *a.ref_ctr + static_cast<uint64_t>(sg.ref_off + t) + 1, a.eta,
                           a.thr64_eta, a.ref_flag);
     } else if (a.eta <= (1ull << 32)) {

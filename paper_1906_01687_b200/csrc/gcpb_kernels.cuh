@@ -128,6 +128,7 @@ struct FusedArgs {
   int nseg;
   Seg seg[3];
   const uint64_t* zero_list;
+  const uint64_t* pick_list;  // optional: SEG_PICK reads its drawn ordinals e from here
   // given samples
   const int64_t* g_idx;
   const double* g_x;

@@ -243,3 +243,40 @@ def test_interleaved_sharded_steps_match_single_rank(monkeypatch):
         assert il == (True, True)
         assert copies >= 2
         assert O.rel_error(flat, want) <= 1e-12
+
+
+@pytest.mark.parametrize("order", [("1", "0"), ("1", "1"), ("0", "1")])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_ordered_segments_match_ordinal_order(monkeypatch, order, dtype):
+    """Tables beyond L2 walk the semi-stratified unrestricted draws in mode-0
+    row order (GCPB_SORTQ, default on with the interleaved table) and, opt-in,
+    the nonzero picks in COO order (GCPB_SORTP): the same draws and weights
+    in another order, so gradient and iterations equal the ordinal-order walk
+    up to summation order."""
+    monkeypatch.setenv("GCPB_HOT_T", "4")
+    g = G()
+    rs = np.random.default_rng(5)
+    dims, r = (300, 40, 50), 8
+    coords, vals = _zipf_coords(rs, dims, 3000)
+    F = [rs.uniform(0.1, 1.0, (n, r)) for n in dims]
+    sk, lf = g.SamplerKind.semi_stratified(7000, 9000), g.LossFunction.poisson()
+    tol = 1e-10 if dtype == "f64" else 2e-5
+
+    def run(sq, sp):
+        monkeypatch.setenv("GCPB_SORTQ", sq)
+        monkeypatch.setenv("GCPB_SORTP", sp)
+        e = _engine(g, monkeypatch, True, dims, r, dtype, coords, vals, F)
+        e.stoch_grad(sk, lf, 3, 0)
+        grad = e.grad_flat().copy()
+        e.adam_step(1e-2, lower_bound=0.0)
+        for it in range(1, 4):
+            e.step(sk, lf, 3, it, 1e-2, lower_bound=0.0)
+        e.run_steps(sk, lf, 3, 4, 3, 1e-2, lower_bound=0.0)
+        out = _flat(e)
+        e.close()
+        return grad, out
+
+    g0, m0 = run("0", "0")
+    g1, m1 = run(*order)
+    assert O.rel_error(g1, g0) <= tol
+    assert O.rel_error(m1, m0) <= tol
