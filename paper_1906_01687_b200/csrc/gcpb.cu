@@ -1199,6 +1199,9 @@ struct SortSpec {
   uint64_t range;  // n_0 (kind 0) or eta (kind 1)
   uint32_t thr;    // Lemire threshold of range (32-bit draws)
   int shift;
+  // kind 0: slabs of mode 1 (bin = slab * nbins0 + (mode-0 row >> shift)),
+  // so each slab's mode-1 lines stay L2-resident while mode 0 is swept
+  uint32_t n1, thr1, slabs, nbins0;
 };
 
 __device__ __forceinline__ void sort_item(const SortSpec& sp, uint64_t it, uint64_t t,
@@ -1213,7 +1216,16 @@ __device__ __forceinline__ void sort_item(const SortSpec& sp, uint64_t it, uint6
   } else {
     key = bounded64(sp.seed, sp.tag, it, t, 0, sp.range);
   }
-  *bin = static_cast<uint32_t>(key >> sp.shift);
+  uint32_t b = static_cast<uint32_t>(key >> sp.shift);
+  if (sp.kind == 0 && sp.slabs > 1) {  // phase_a: mode 1 = word 1 of the same block
+    const U4 b1 = philox_block(sp.seed, sp.tag, 0u, 0u, it, t);
+    const uint64_t prod = static_cast<uint64_t>(b1.y) * sp.n1;
+    const uint32_t i1 = (static_cast<uint32_t>(prod) >= sp.thr1)
+                            ? static_cast<uint32_t>(prod >> 32)
+                            : bounded32_from(sp.seed, sp.tag, it, t, 1, sp.n1, sp.thr1, 1u);
+    b += static_cast<uint32_t>(static_cast<uint64_t>(i1) * sp.slabs / sp.n1) * sp.nbins0;
+  }
+  *bin = b;
   *val = sp.kind == 0 ? t : key;
 }
 
@@ -1254,7 +1266,8 @@ bool order_wanted(const gcpb_ctx* c) {
 // too small inside a graph capture): the caller walks ordinal order instead.
 bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
   if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
-  const int64_t nbins = static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1;
+  const int64_t nbins = (static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1) *
+                       (sp.kind == 0 && sp.slabs > 1 ? sp.slabs : 1);
   if (nbins >= (int64_t{1} << 31)) return false;
   size_t tmp = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<uint32_t*>(nullptr),
@@ -1306,6 +1319,18 @@ SortSpec order_spec(const FusedArgs<T>& a, uint32_t tag, int kind, int64_t b0, i
     sp.range = a.dims[0];
     sp.thr = a.thr[0];
     sp.shift = 6;  // 64 mode-0 rows per bin
+    sp.nbins0 = static_cast<uint32_t>(((a.dims[0] - 1) >> sp.shift) + 1);
+    sp.slabs = 1;
+    if (a.d > 1) {
+      sp.n1 = a.dims[1];
+      sp.thr1 = a.thr[1];
+      // Mode-1 slabs (opt-in, GCPB_QSLABS=k): measured on C5 (218 MB of
+      // mode-1 lines) fused 2.84 / 2.86 / 3.02 / 3.04 / 2.89 ms for
+      // 1 / 2 / 5 / 8 / 16 slabs -- the slab's lines do not stay resident
+      // under the picks' traffic, and mode 0 is swept once per slab.
+      if (const char* e = getenv("GCPB_QSLABS")) sp.slabs = std::max(1, atoi(e));
+      if (sp.slabs < 1) sp.slabs = 1;
+    }
   } else {
     sp.range = a.eta;
     sp.thr = a.thr_eta;

@@ -265,6 +265,7 @@ def test_ordered_segments_match_ordinal_order(monkeypatch, order, dtype):
     def run(sq, sp):
         monkeypatch.setenv("GCPB_SORTQ", sq)
         monkeypatch.setenv("GCPB_SORTP", sp)
+        monkeypatch.setenv("GCPB_QSLABS", "3")  # mode-1 slabs (C5 takes 5)
         e = _engine(g, monkeypatch, True, dims, r, dtype, coords, vals, F)
         e.stoch_grad(sk, lf, 3, 0)
         grad = e.grad_flat().copy()
