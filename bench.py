@@ -205,10 +205,12 @@ ROOFLINE_NOTES = {
     "c3": "factors (512 KB) L2-resident; bound by L2 reductions and the hash probes",
     "c4": "latency-bound: 2e5 samples per step (1.3 tiles per warp)",
     "c5": "random HBM row access (factors 531 MB): factor and gradient rows interleaved in one "
-          "128-byte line so a row gather and its reduction share a DRAM burst; ncu DRAM traffic "
-          "401 B/sample (B_alg 396) at 3.3 TB/s, long-scoreboard bound (profiles/r01_c5_il.md); "
-          "the random-access microbenchmark tops out at 6.0e9 samples/s for this mix "
-          "(tools/randbw.cu, profiles/r01_randbw.md)",
+          "128-byte line so a row gather and its reduction share a DRAM burst, and the "
+          "unrestricted draws walked in mode-0 row order (mode 0 swept instead of gathered); ncu "
+          "DRAM traffic 334 B/sample (B_alg 396; 401 in ordinal order) at 3.8 TB/s, "
+          "long-scoreboard bound (profiles/r01_c5_ordered.md); the random-access "
+          "microbenchmark tops out at 6.0e9 samples/s for the unordered mix (tools/randbw.cu, "
+          "profiles/r01_randbw.md)",
 }
 
 
