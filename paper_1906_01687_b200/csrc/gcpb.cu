@@ -1319,6 +1319,7 @@ SortSpec order_spec(const FusedArgs<T>& a, uint32_t tag, int kind, int64_t b0, i
     sp.range = a.dims[0];
     sp.thr = a.thr[0];
     sp.shift = 6;  // 64 mode-0 rows per bin
+    if (const char* e = getenv("GCPB_QSHIFT")) sp.shift = std::max(0, std::min(20, atoi(e)));
     sp.nbins0 = static_cast<uint32_t>(((a.dims[0] - 1) >> sp.shift) + 1);
     sp.slabs = 1;
     if (a.d > 1) {
