@@ -1264,32 +1264,42 @@ bool order_wanted(const gcpb_ctx* c) {
 
 // Writes the ordered list for sp into ob.out; false when it cannot (scratch
 // too small inside a graph capture): the caller walks ordinal order instead.
-bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
-  if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
-  const int64_t nbins = (static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1) *
-                       (sp.kind == 0 && sp.slabs > 1 ? sp.slabs : 1);
-  if (nbins >= (int64_t{1} << 31)) return false;
+// Sizes ob for n items in nbins bins; false inside a graph capture when it
+// would have to allocate.
+bool order_reserve(gcpb_ctx* c, OrderBufs& ob, int64_t n, int64_t nbins) {
   size_t tmp = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<uint32_t*>(nullptr),
                                    static_cast<uint32_t*>(nullptr), static_cast<int>(nbins),
                                    c->stream));
-  if (sp.n > ob.out_cap || nbins > ob.bins_cap || tmp > ob.tmp_bytes) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(c->stream, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return false;
-    if (sp.n > ob.out_cap) {
-      ob.out.alloc(static_cast<size_t>(sp.n) * sizeof(uint64_t));
-      ob.out_cap = sp.n;
-    }
-    if (nbins > ob.bins_cap) {
-      ob.cnt.alloc(static_cast<size_t>(2 * nbins) * sizeof(uint32_t));
-      ob.bins_cap = nbins;
-    }
-    if (tmp > ob.tmp_bytes) {
-      ob.tmp.alloc(tmp);
-      ob.tmp_bytes = tmp;
-    }
+  if (n <= ob.out_cap && nbins <= ob.bins_cap && tmp <= ob.tmp_bytes) return true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return false;
+  if (n > ob.out_cap) {
+    ob.out.alloc(static_cast<size_t>(n) * sizeof(uint64_t));
+    ob.out_cap = n;
   }
+  if (nbins > ob.bins_cap) {
+    ob.cnt.alloc(static_cast<size_t>(2 * nbins) * sizeof(uint32_t));
+    ob.bins_cap = nbins;
+  }
+  if (tmp > ob.tmp_bytes) {
+    ob.tmp.alloc(tmp);
+    ob.tmp_bytes = tmp;
+  }
+  return true;
+}
+
+int64_t order_bins(const SortSpec& sp) {
+  return (static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1) *
+         (sp.kind == 0 && sp.slabs > 1 ? sp.slabs : 1);
+}
+
+bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
+  if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
+  const int64_t nbins = order_bins(sp);
+  if (nbins >= (int64_t{1} << 31)) return false;
+  if (!order_reserve(c, ob, sp.n, nbins)) return false;
   uint32_t* cnt = ob.cnt.as<uint32_t>();
   uint32_t* cur = cnt + nbins;
   const int grid = static_cast<int>(std::max<int64_t>(
@@ -1879,6 +1889,14 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     ensure_hash(c);
   }
   if (c->tensor_kind == 2) ensure_hot(c);  // host work: not inside the capture
+  if (sk->strategy == GCPB_SEMI_STRATIFIED && sk->zero_samples > 0 && c->draw_stream == 0 &&
+      order_wanted(c)) {  // ordering scratch for the unrestricted draws, before the capture
+    int64_t b0 = 0, b1 = 0;
+    gcpb_shard_range(sk->zero_samples, c->rank, c->nranks, &b0, &b1);
+    FusedArgs<T> fa = base_args<T>(c, nullptr, seed, iter0);
+    const SortSpec sp = order_spec(fa, TAG_GRAD_SEMI_Q, 0, b0, b1);
+    if (sp.n > 0) order_reserve(c, c->qorder, sp.n, order_bins(sp));
+  }
   set_rng_iter(c, iter0);
   if (small_eligible<T>(c, sk)) {
     small_launch<T>(c, sk, loss, seed, n);
