@@ -1348,6 +1348,7 @@ SortSpec order_spec(const FusedArgs<T>& a, uint32_t tag, int kind, int64_t b0, i
     int sh = 0;
     while ((a.eta >> sh) > (1ull << 21)) ++sh;  // <= 2M bins (records of one bin: a few KB)
     sp.shift = sh;
+    if (const char* e = getenv("GCPB_PSHIFT")) sp.shift = std::max(0, std::min(40, atoi(e)));
   }
   return sp;
 }
