@@ -279,6 +279,12 @@ struct gcpb_ctx {
   DBuf zero_list, zstatus, ztbits;
   // sampled segments in memory order (large tables): q draws, nonzero picks
   OrderBufs qorder, porder;
+  // overlapped ordering inside step graphs (GCPB_ORD_OVERLAP): step k+1's
+  // list is built on a side stream while step k's Adam runs
+  OrderBufs qpre[2];
+  cudaStream_t ord_side = nullptr;
+  cudaEvent_t ord_fork = nullptr, ord_done[2] = {nullptr, nullptr};
+  int64_t ord_step = -1, ord_n = 0;
   int64_t zero_cap = 0, zstatus_cap = 0, z_nchunks_first = 0;
 
   // estimator
@@ -315,6 +321,10 @@ struct gcpb_ctx {
     }
     if (xfer_done) cudaEventDestroy(xfer_done);
     if (comm) ncclCommDestroy(comm);
+    if (ord_fork) cudaEventDestroy(ord_fork);
+    for (auto& e : ord_done)
+      if (e) cudaEventDestroy(e);
+    if (ord_side) cudaStreamDestroy(ord_side);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -1257,6 +1267,11 @@ bool order_picks() {
   return e != nullptr && atoi(e) != 0;
 }
 
+bool ord_overlap_wanted() {
+  const char* e = getenv("GCPB_ORD_OVERLAP");
+  return e != nullptr && atoi(e) != 0;
+}
+
 bool order_wanted(const gcpb_ctx* c) {
   const char* e = getenv("GCPB_SORTQ");
   return e ? atoi(e) != 0 : c->il_enabled;
@@ -1295,7 +1310,8 @@ int64_t order_bins(const SortSpec& sp) {
          (sp.kind == 0 && sp.slabs > 1 ? sp.slabs : 1);
 }
 
-bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
+bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp, cudaStream_t stream = nullptr) {
+  if (!stream) stream = c->stream;
   if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
   const int64_t nbins = order_bins(sp);
   if (nbins >= (int64_t{1} << 31)) return false;
@@ -1304,12 +1320,12 @@ bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
   uint32_t* cur = cnt + nbins;
   const int grid = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>((sp.n + 255) / 256, static_cast<int64_t>(c->num_sms) * 8)));
-  CK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nbins) * sizeof(uint32_t), c->stream));
-  order_count_kernel<<<grid, 256, 0, c->stream>>>(sp, cnt);
+  CK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nbins) * sizeof(uint32_t), stream));
+  order_count_kernel<<<grid, 256, 0, stream>>>(sp, cnt);
   CK(cudaGetLastError());
   size_t tb = ob.tmp_bytes;
-  CK(cub::DeviceScan::ExclusiveSum(ob.tmp.p, tb, cnt, cur, static_cast<int>(nbins), c->stream));
-  order_scatter_kernel<<<grid, 256, 0, c->stream>>>(sp, cur, ob.out.as<uint64_t>());
+  CK(cub::DeviceScan::ExclusiveSum(ob.tmp.p, tb, cnt, cur, static_cast<int>(nbins), stream));
+  order_scatter_kernel<<<grid, 256, 0, stream>>>(sp, cur, ob.out.as<uint64_t>());
   CK(cudaGetLastError());
   return true;
 }
@@ -1436,6 +1452,8 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   a.nseg = 0;
   const bool ordered = scatter && !record && est_kind < 0 && c->draw_stream == 0 &&
                        order_wanted(c);
+  bool ord_next = false;
+  int64_t ord_b0 = 0, ord_b1 = 0;
   if (p > 0) {
     gcpb_shard_range(p, c->rank, c->nranks, &b0, &b1);
     // (walking the picks in COO order -- FusedArgs::pick_list -- measured
@@ -1458,7 +1476,18 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       const double wq = c->total_d / static_cast<double>(q);
-      if (ordered &&
+      if (ordered && c->ord_step >= 0) {
+        // overlapped: this step's list was built on the side stream (step 0:
+        // by run_steps_impl on the main stream); join it before the fused
+        // kernel, and fork the next step's list right after it
+        const int64_t k = c->ord_step;
+        if (k > 0) CK(cudaStreamWaitEvent(c->stream, c->ord_done[k & 1], 0));
+        a.zero_list = c->qpre[k & 1].out.as<uint64_t>();
+        a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
+        ord_next = k + 1 < c->ord_n;
+        ord_b0 = b0;
+        ord_b1 = b1;
+      } else if (ordered &&
           order_build(c, c->qorder, order_spec(a, TAG_GRAD_SEMI_Q, 0, b0, b1))) {
         a.zero_list = c->qorder.out.as<uint64_t>();  // the same draws, in mode-0 row order
         a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
@@ -1469,6 +1498,17 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   }
   res.n = p + q;
   run_fused(c, a, record, fold);
+  if (ord_next) {  // next step's list on the side stream, under this step's Adam
+    const int64_t k1 = c->ord_step + 1;
+    SortSpec sp = order_spec(a, TAG_GRAD_SEMI_Q, 0, ord_b0, ord_b1);
+    sp.iter = static_cast<uint64_t>(k1);
+    sp.iter_base = &c->dst()->graph_base;
+    CK(cudaEventRecord(c->ord_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->ord_side, c->ord_fork, 0));
+    if (!order_build(c, c->qpre[k1 & 1], sp, c->ord_side))
+      throw std::logic_error("overlapped ordering: scratch not reserved");
+    CK(cudaEventRecord(c->ord_done[k1 & 1], c->ord_side));
+  }
   if (c->draw_stream == 1) {  // p picks, then d draws per tested candidate / q draw
     if (strat && q > 0 && c->nranks > 1)
       CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, 
@@ -1527,7 +1567,10 @@ void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0, int hot_rh
   // are the long pole and the wider grid measured slower (C3 11.5 -> 22 us)
   int lp = 1;
   while (hot.n == 0 && lp < 8 && 4 * lp < fold_reps) lp <<= 1;
-  const int grid = grid_for(c->nelem / c->vw * lp, 256, c->num_sms, 8) + hot.n;
+  // (2 blocks per SM stream as fast; under the overlapped ordering they leave
+  // the side stream's kernels room)
+  const int grid = grid_for(c->nelem / c->vw * lp, 256, c->num_sms, c->ord_step >= 0 ? 2 : 8) +
+                   hot.n;
   if (c->il_pending || c->il_gpack) {  // factors (and unless packed, the gradient) in AG
     ILTab<T> il;
     il.ag = c->AG.as<T>();
@@ -1890,6 +1933,9 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     ensure_hash(c);
   }
   if (c->tensor_kind == 2) ensure_hot(c);  // host work: not inside the capture
+  bool overlap = false;
+  SortSpec ov_spec;
+  std::memset(&ov_spec, 0, sizeof(ov_spec));
   if (sk->strategy == GCPB_SEMI_STRATIFIED && sk->zero_samples > 0 && c->draw_stream == 0 &&
       order_wanted(c)) {  // ordering scratch for the unrestricted draws, before the capture
     int64_t b0 = 0, b1 = 0;
@@ -1897,6 +1943,18 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     FusedArgs<T> fa = base_args<T>(c, nullptr, seed, iter0);
     const SortSpec sp = order_spec(fa, TAG_GRAD_SEMI_Q, 0, b0, b1);
     if (sp.n > 0) order_reserve(c, c->qorder, sp.n, order_bins(sp));
+    if (sp.n > 0 && ord_overlap_wanted() && c->nranks == 1 && c->il_enabled) {
+      overlap = order_reserve(c, c->qpre[0], sp.n, order_bins(sp)) &&
+                order_reserve(c, c->qpre[1], sp.n, order_bins(sp));
+      if (overlap && !c->ord_side) {
+        CK(cudaStreamCreateWithFlags(&c->ord_side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ord_fork, cudaEventDisableTiming));
+        for (auto& e : c->ord_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      ov_spec = sp;
+      ov_spec.iter = 0;
+      ov_spec.iter_base = &c->dst()->graph_base;
+    }
   }
   set_rng_iter(c, iter0);
   if (small_eligible<T>(c, sk)) {
@@ -1911,7 +1969,7 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     ag_prepare<T>(c);  // not inside the capture
   else
     a_current(c);
-  const std::string key = steps_key(c, sk, loss, seed, n);
+  const std::string key = steps_key(c, sk, loss, seed, n) + (overlap ? "|ov" : "");
   if (!c->graph_exec || key != c->graph_key) {
     if (c->graph_exec) {
       cudaGraphExecDestroy(c->graph_exec);
@@ -1920,9 +1978,20 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      for (int64_t k = 0; k < n; ++k)
+      if (overlap) {  // step 0's list on the main stream, from the replay's base
+        graph_base_kernel<<<1, 1, 0, c->stream>>>(c->dst());
+        CK(cudaGetLastError());
+        if (!order_build(c, c->qpre[0], ov_spec))
+          throw std::logic_error("overlapped ordering: scratch not reserved");
+        c->ord_n = n;
+      }
+      for (int64_t k = 0; k < n; ++k) {
+        if (overlap) c->ord_step = k;
         step_impl<T>(c, sk, loss, seed, 0, &c->dst()->rng_iter, ZERO_CAPTURE);
+      }
+      c->ord_step = -1;
     } catch (...) {
+      c->ord_step = -1;
       cudaStreamEndCapture(c->stream, &g);
       if (g) cudaGraphDestroy(g);
       throw;

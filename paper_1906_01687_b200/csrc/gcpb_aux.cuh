@@ -31,7 +31,10 @@ struct DevState {
   uint64_t ref_ctr;      // RefStream counter (draws consumed so far)
   uint32_t ref_flag;     // RefStream: a draw hit the rejection region
   uint32_t ref_pad;
+  uint64_t graph_base;   // rng_iter at the start of a step-graph replay (ordering overlap)
 };
+
+__global__ void graph_base_kernel(DevState* st) { st->graph_base = st->rng_iter; }
 
 constexpr int kZcThreads = 256;
 constexpr int kZcItems = 8;
