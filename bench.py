@@ -9,13 +9,16 @@ One "step" = one iteration of the reference's epoch loop body
 sample -> model eval -> loss derivative -> d-mode MTTKRP kernel, the NCCL
 all-reduce of the gradient when N > 1, and the fused Adam update.  The K timed
 steps are replayed as one CUDA graph (gcpb_run_steps).  Default workload:
-BASELINE.json configs[1] (C2: dense 200^4 binary, bernoulli-odds, r=16,
-uniform s=1.6e7 per GPU).  Multi-GPU is weak scaling (s per GPU fixed, sample
-ordinals sharded, factors replicated).
+the largest single-GPU config, BASELINE.json configs[4] (C5: sparse
+4.8e6x1.7e6x1.8e6 with 1.7e9 nonzeros, gaussian, r=16, semi-stratified
+p=q=1.6e7 per GPU -- the only config whose factor table lives in HBM).
+Multi-GPU is weak scaling (s per GPU fixed, sample ordinals and nonzeros
+sharded, factors replicated); `--gpus N` outside torchrun re-launches itself
+under torch.distributed.run with N ranks.
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
 CPU implementation (oracle/_ref = /root/reference compiled unmodified) on the
-host cores on a bounded sample of the same workload.
+host cores, every step at the config's full sample count.
 """
 from __future__ import annotations
 
@@ -197,6 +200,11 @@ def sampler_of(w, G, nranks=1):
     return G.SamplerKind.semi_stratified(w.p * nranks, w.q * nranks)
 
 
+# What bounds each config's fused kernel: C5's factor table
+# (531 MB) lives in HBM; C2/C3's factors are L2-resident and the binding limit
+# is the L2 vector-reduction rate; C1/C4 are latency-bound.
+BOUND = {"c1": "latency", "c2": "l2_red", "c3": "l2_red", "c4": "latency", "c5": "hbm"}
+
 ROOFLINE_NOTES = {
     "c1": "latency-bound (300 samples/step); one cluster launch runs all K iterations",
     "c2": "factor rows are L1/L2-resident (51 KB), so B_alg/s exceeds HBM peak; the binding "
@@ -214,20 +222,28 @@ ROOFLINE_NOTES = {
 }
 
 
-def launches_per_step(w, hot, world, interleaved=False):
-    # fused kernel + adam (which folds the hot-row copies; sharded steps fold
-    # them before the all-reduce instead); the stratified zero sampler adds
-    # 3 x (plan + candidate test + scatter) + a shortfall check; on the
-    # interleaved table the unrestricted draws are put in mode-0 row order
-    # first (count, scan init, scan, scatter)
-    return (2 + (1 if hot and world > 1 else 0) + (10 if w.sampler == "stratified" else 0)
-            + (4 if interleaved and w.sampler == "semi-stratified" else 0))
-
-
 # ---------------------------------------------------------------------------
 # CPU reference timing (oracle/_ref = the unmodified reference compiled here)
 # ---------------------------------------------------------------------------
-def reference_cpu(w, steps, warmup, n_sample, log):
+def c5_cpu_samples(w, rs, n_pick, n_draw):
+    """C5 draws for the reference's CPU path: p nonzero picks with the data's
+    generating distribution (per-mode Zipf(1.05) coordinates, values
+    log(1+Poisson(3)), Poisson >= 1) and q unrestricted uniform indices."""
+    from paper_1906_01687_b200 import workloads as WL
+    idx_p = np.stack([WL.zipf_indices(rs, n, 1.05, n_pick) for n in w.dims], 1).astype(np.int64)
+    x_p = np.log1p(np.maximum(1, rs.poisson(3.0, n_pick))).astype(np.float64)
+    idx_q = np.stack([rs.integers(0, n, n_draw) for n in w.dims], 1).astype(np.int64)
+    return idx_p, x_p, idx_q
+
+
+def reference_cpu(w, steps, warmup, log):
+    """The reference's own CPU step (oracle/_ref) per BASELINE.md §2: `warmup`
+    untimed steps, then the median over `steps` of draw_gradient_samples (or,
+    for C2/C5 whose tensors it cannot hold, its per-sample entry + deriv +
+    weight + append loop on pre-drawn indices) and mttkrp_sampled_all with all
+    host threads; samples/s = s / (t_sample + t_mttkrp); adam_step timed once
+    (the last step) and reported beside it.  Every step is the config's full
+    sample count."""
     import ctypes as C
     import oracle as O
     from paper_1906_01687_b200 import workloads as WL
@@ -239,45 +255,47 @@ def reference_cpu(w, steps, warmup, n_sample, log):
     rs = np.random.default_rng(4242)
     dims = np.array(w.dims, dtype=np.int64)
     has_lb = 1 if w.lower_bound is not None else 0
-    times = []
+    times, adam_s = [], None
     tm = np.zeros(3)
     h = C.c_void_p()
-    if w.name in ("c2", "c5"):
-        # The reference cannot hold these tensors (DenseTensor cap 1e8,
-        # tensor.hpp:54; C5's 1.7e9-entry COO needs >> host RAM,
-        # tensor.cpp:18-23): time its per-sample entry + deriv + weight +
-        # append loop (samplers.hpp:87-93) on builder-supplied (index, x), then
-        # mttkrp_sampled_all(threads) and adam_step.
-        if w.name == "c2":
-            T = WL.c2_true_factors(1002)
-            idx = np.stack([rs.integers(0, n, n_sample) for n in w.dims], 1).astype(np.int64)
-            m = np.ones((n_sample, T[0].shape[1]))
-            for k in range(4):
-                m *= T[k][idx[:, k]]
-            m = m.sum(1)
-            x = (rs.random(n_sample) < m / (1.0 + m)).astype(np.float64)
-            F = WL.init_factors(w.dims, w.rank, 2002, data_norm=np.sqrt(0.1 * 1.6e9))
-            weight = float(np.prod(dims.astype(np.float64))) / n_sample
-            what = "uniform samples of C2 (x from the C2 generator model)"
-        else:
-            idx = np.stack([WL.zipf_indices(rs, n, 1.05, n_sample) for n in w.dims],
-                           1).astype(np.int64)
-            x = np.log1p(np.maximum(1, rs.poisson(3.0, n_sample))).astype(np.float64)
-            F = WL.init_factors(w.dims, w.rank, 2005, data_norm=None, lo=0.0, hi=0.1)
-            weight = 1.7e9 / (n_sample / 2)
-            what = "C5-distributed samples (COO lookup cost excluded)"
-        ref._ck(ref.lib.ref_bench_model_new(len(dims), O._i64(dims), w.rank,
-                                            O._f64(O.Oracle.flat(F)), C.byref(h)))
-        for it in range(warmup + steps):
-            ref._ck(ref.lib.ref_bench_step_given(h, lk, 0.0, n_sample, O._i64(idx), O._f64(x),
-                                                 weight, threads, 1e-3, has_lb, 0.0, O._f64(tm)))
-            if it >= warmup:
-                times.append(tm.copy())
-        ref.lib.ref_bench_model_free(h)
-        per_step = n_sample
-        sample = f"{n_sample} pre-drawn {what} per step"
+    total = float(np.prod(dims.astype(np.float64)))
+    t_setup = time.perf_counter()
+    if w.name == "c2":
+        # DenseTensor cap 1e8 (tensor.hpp:54): the sample_uniform loop body
+        # (samplers.hpp:87-93) on pre-drawn indices with x from the C2 model
+        n = w.s
+        T = WL.c2_true_factors(1002)
+        idx = np.stack([rs.integers(0, k, n) for k in w.dims], 1).astype(np.int64)
+        m = np.ones((n, T[0].shape[1]))
+        for k in range(4):
+            m *= T[k][idx[:, k]]
+        x = (rs.random(n) < m.sum(1) / (1.0 + m.sum(1))).astype(np.float64)
+        del m
+        F = WL.init_factors(w.dims, w.rank, 2002, data_norm=np.sqrt(0.1 * 1.6e9))
+        per_step = n
+        what = (f"{n} pre-drawn uniform samples of C2 per step (x from the C2 generator model; "
+                "the reference's DenseTensor cannot hold 1.6e9 entries)")
+
+        def one(do_adam):
+            ref._ck(ref.lib.ref_bench_step_given(h, lk, 0.0, n, O._i64(idx), O._f64(x), total / n,
+                                                 threads, 1e-3, has_lb, 0.0, do_adam, O._f64(tm)))
+    elif w.name == "c5":
+        # the COO needs >> host RAM (tensor.cpp:18-23): the
+        # sample_semi_stratified loop body (samplers.hpp:199-216) on pre-drawn
+        # picks and unrestricted indices, COO lookup excluded
+        idx_p, x_p, idx_q = c5_cpu_samples(w, rs, w.p, w.q)
+        F = WL.init_factors(w.dims, w.rank, 2005, data_norm=None, lo=0.0, hi=0.1)
+        per_step = w.p + w.q
+        what = (f"{w.p} pre-drawn nonzero picks (Zipf(1.05) coordinates, log(1+Poisson(3)) "
+                f"values) + {w.q} unrestricted uniform draws per step; the COO lookup is excluded "
+                "(the reference cannot hold C5's 1.7e9-entry COO)")
+
+        def one(do_adam):
+            ref._ck(ref.lib.ref_bench_step_semi_given(
+                h, lk, 0.0, w.p, O._i64(idx_p), O._f64(x_p), w.q, O._i64(idx_q), w.nnz, total,
+                threads, 1e-3, has_lb, 0.0, do_adam, O._f64(tm)))
     else:
-        # Reference samplers on reference containers (C1, C3, C4).
+        # the reference's own samplers + RngStream on reference containers
         if w.name == "c1":
             rt = ref.dense(w.dims, c1_tensor())
         else:
@@ -285,25 +303,54 @@ def reference_cpu(w, steps, warmup, n_sample, log):
             coords = np.stack(np.unravel_index(keys.astype(np.int64), w.dims, order="F"), 1)
             rt = ref.sparse(w.dims, coords, vals.astype(np.float64))
         F = WL.init_factors(w.dims, w.rank, 2000 + int(w.name[1]), data_norm=rt.norm())
-        ref._ck(ref.lib.ref_bench_model_new(len(dims), O._i64(dims), w.rank,
-                                            O._f64(O.Oracle.flat(F)), C.byref(h)))
         strat = {"uniform": 0, "stratified": 1, "semi-stratified": 2}[w.sampler]
         nsm = C.c_int64()
-        for it in range(warmup + steps):
+        per_step = w.samples_per_step
+        what = (f"the full {w.name.upper()} step ({per_step} samples) with the reference's own "
+                f"{w.sampler} sampler and RngStream")
+        seq = [0]
+
+        def one(do_adam):
+            seq[0] += 1
             ref._ck(ref.lib.ref_bench_step_sampler(h, rt.h, lk, 0.0, strat, w.s, w.p, w.q, w.rho,
-                                                   77 + it, threads, 1e-3, has_lb, 0.0,
-                                                   O._f64(tm), C.byref(nsm)))
-            if it >= warmup:
-                times.append(tm.copy())
-        ref.lib.ref_bench_model_free(h)
-        per_step = int(nsm.value)
-        sample = (f"the full {w.name.upper()} step ({per_step} samples) with the reference's own "
-                  f"{w.sampler} sampler and RngStream")
-    t = np.mean(times, axis=0)
-    sample += (f"; draw_gradient_samples {t[0]*1e3:.1f} ms, mttkrp_sampled_all({threads} threads) "
-               f"{t[1]*1e3:.1f} ms, adam_step {t[2]*1e3:.1f} ms; mean of {len(times)} steps")
-    return {"value": per_step / float(t.sum()), "unit": UNIT, "cores": threads,
-            "kind": "reference", "sample": sample, "step_s": float(t.sum())}
+                                                   77 + seq[0], threads, 1e-3, has_lb, 0.0,
+                                                   do_adam, O._f64(tm), C.byref(nsm)))
+    ref._ck(ref.lib.ref_bench_model_new(len(dims), O._i64(dims), w.rank,
+                                        O._f64(O.Oracle.flat(F)), C.byref(h)))
+    log(f"[bench] reference data ready in {time.perf_counter() - t_setup:.1f}s")
+    for it in range(warmup + steps):
+        last = it == warmup + steps - 1
+        one(1 if last else 0)
+        if it >= warmup:
+            times.append(tm[:2].copy())
+        if last:
+            adam_s = float(tm[2])
+    ref.lib.ref_bench_model_free(h)
+    t = np.median(np.array(times), axis=0)
+    step_s = float(t.sum())
+    sample = (f"{what}; medians over {len(times)} steps after {warmup} warm-up: "
+              f"draw_gradient_samples {t[0]*1e3:.1f} ms + mttkrp_sampled_all({threads} threads) "
+              f"{t[1]*1e3:.1f} ms; adam_step {adam_s*1e3:.1f} ms (timed once, not in the metric: "
+              "BASELINE.md §2 samples/s = s/(t_sample+t_mttkrp))")
+    return {"value": per_step / step_s, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": sample, "step_s": step_s}
+
+
+# CPU-leg sizes inside our arm (rank 0, N=1): the config's full sample count
+# per step, about 10-30 s of host work in total.
+CPU_LEG = {"c1": (3, 20), "c2": (1, 5), "c3": (1, 5), "c4": (3, 20), "c5": (0, 1)}
+
+
+def config_of(w, world):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    return {"workload": f"{w.name.upper()}: {w.description}",
+            "samples_per_gpu_step": w.samples_per_step,
+            "global_batch": w.samples_per_step * world,
+            "rank": w.rank, "dims": list(w.dims), "loss": w.loss, "sampler": w.sampler,
+            "parallelism": (f"dp{world}: sample ordinals sharded, factors replicated, NCCL "
+                            f"all-reduce of the gradient") if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (tensor in HBM); factor rows L1/L2-resident by "
+                  "design (they are the model)"}
 
 
 # ---------------------------------------------------------------------------
@@ -316,6 +363,11 @@ def run_ours(args, w):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} needs {world} GPUs, "
+                         f"found {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -365,6 +417,7 @@ def run_ours(args, w):
     if dist:
         dist.barrier()
     clk = clocks.stop()
+    launches = e.run_steps_launches()
     total_ms = start.elapsed_time(end)
     if dist:
         t = torch.tensor([total_ms], device=f"cuda:{local}")
@@ -372,7 +425,6 @@ def run_ours(args, w):
         total_ms = float(t[0])
     ms_per_step = total_ms / K
     steps_path = e.steps_path
-    hot_copies = e.hot_rows[1] if w.kind == "sparse" else 0
     samples_per_step = w.samples_per_step * world
     value = samples_per_step / (ms_per_step / 1e3)
 
@@ -405,7 +457,8 @@ def run_ours(args, w):
     prof = ROOT / "profiles" / f"ncu_traffic_{w.name}.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
+    bound = BOUND.get(w.name, "hbm")
+    roofline = {"bound": bound, "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
                 "frac": round(achieved / peak_gbs, 4), "traffic": traffic,
                 # also against the north star's nominal 8.0 TB/s
                 "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
@@ -417,7 +470,11 @@ def run_ours(args, w):
                                             "scattered factor rows)",
                 "units_per_launch": w.samples_per_step, "peak_source": peak_src,
                 "note": ROOFLINE_NOTES.get(w.name, "")}
-    if w.name in ("c2", "c3"):
+    if traffic:
+        # DRAM-counter cross-check: the ncu capture's bytes over this run's
+        # launch time (ncu times are cold and serialised; the bytes are not)
+        roofline["traffic_frac"] = round(traffic / (fused_ms / 1e3) / 1e9 / peak_gbs, 4)
+    if bound == "l2_red":
         # L2-resident factors: the binding ceiling is the L2 vector-reduction
         # rate, measured by tools/bulkred.cu (profiles/r01_bulkred.md: 6.4e7
         # 64-byte rows = 2.56e8 red.global.add.v4 in 0.794 ms)
@@ -427,7 +484,7 @@ def run_ours(args, w):
         roofline["binding"] = {"limit": "L2 vector reductions (red.global.add.v4.f32)",
                                "achieved": float("%.4g" % red_rate), "peak": 3.22e11,
                                "unit": "reductions/s", "frac": round(red_rate / 3.22e11, 3),
-                               "source": "tools/bulkred.cu, profiles/r01_bulkred.md"}
+                               "source": "tools/bulkred.cu microbenchmark, profiles/r01_bulkred.md"}
 
     # e2e through the C-ABI with host buffers: every step copies the model in
     # from pinned host memory, runs the iteration, and copies the updated
@@ -461,11 +518,13 @@ def run_ours(args, w):
                "what": "per step through the C-ABI with pinned host buffers: gcpb_step_host = "
                        "model H2D + sample/eval/MTTKRP (+ all-reduce) + Adam + model D2H, one "
                        "call and one synchronisation per step, wall clock"}
+    e.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = reference_cpu(w, steps=2, warmup=1, n_sample=args.cpu_samples, log=log)
+            cw, cs = CPU_LEG.get(w.name, (1, 3))
+            cpu = reference_cpu(w, steps=cs, warmup=cw, log=log)
         except Exception as ex:  # reported, not fatal
             log(f"[bench] cpu baseline failed: {ex}")
     if cpu:
@@ -476,19 +535,15 @@ def run_ours(args, w):
         "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": w.dtype,
         "data": f"synthetic ({w.description}); seeded generator, no dataset",
-        "config": {"workload": f"{w.name.upper()}: {w.description}",
-                   "samples_per_gpu_step": w.samples_per_step, "global_batch": samples_per_step,
-                   "rank": w.rank, "dims": list(w.dims), "loss": w.loss, "sampler": w.sampler,
-                   "parallelism": (f"dp{world}: sample ordinals sharded, factors replicated, NCCL "
-                                   f"all-reduce of the gradient") if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (tensor in HBM); factor rows L1/L2-resident by "
-                         "design (they are the model)",
-                   "step": ("small-problem cluster kernel: K iterations (sample+eval+MTTKRP, "
-                            "cluster barrier, Adam) in one launch" if steps_path == "small" else
-                            "fused sample+eval+MTTKRP kernel + (all-reduce) + fused Adam; K steps "
-                            "replayed as one CUDA graph")},
+        "config": config_of(w, world),
+        "step": ("small-problem cluster kernel: K iterations (sample+eval+MTTKRP, cluster "
+                 "barrier, Adam) in one launch" if steps_path == "small" else
+                 "fused sample+eval+MTTKRP kernel + (all-reduce) + fused Adam; K steps "
+                 "replayed as one CUDA graph"),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 1 if steps_path == "small" else launches_per_step(w, hot_copies > 0, world, e.interleaved[0]) * K, "clocks": clk,
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / K,
+        "clocks": clk,
         "impl": "ours",
     }
     if rank == 0:
@@ -504,8 +559,8 @@ def run_reference(args, w):
     if rank != 0:
         return
     t0 = time.perf_counter()
-    cpu = reference_cpu(w, steps=args.steps, warmup=args.warmup, n_sample=args.cpu_samples,
-                        log=lambda m: print(m, file=sys.stderr))
+    cpu = reference_cpu(w, steps=args.steps, warmup=args.warmup,
+                        log=lambda m: print(m, file=sys.stderr, flush=True))
     if cpu is None:
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libgcpref.so (reference compiled from /root/reference) "
@@ -516,8 +571,9 @@ def run_reference(args, w):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["step_s"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic ({w.description})",
-        "config": {"workload": f"{w.name.upper()}: {w.description}", "rank": w.rank,
-                   "dims": list(w.dims), "loss": w.loss, "sampler": w.sampler},
+        "config": config_of(w, world),
+        "step": ("the reference's own CPU step (oracle/_ref): sampling + mttkrp_sampled_all "
+                 "with all host threads, fp64"),
         "impl": "reference",
         "cpu_baseline": {"value": cpu["value"], "unit": UNIT, "cores": cpu["cores"],
                          "kind": "reference", "sample": cpu["sample"]},
@@ -528,15 +584,27 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+def _relaunch_under_torchrun(args):
+    """`--gpus N` without a torchrun environment: re-execute under
+    torch.distributed.run with one process per GPU (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--samples", type=int, default=None, help="override s (uniform) per GPU")
-    ap.add_argument("--cpu-samples", type=int, default=1_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -544,6 +612,10 @@ def main():
         args.warmup = 3
     from paper_1906_01687_b200 import workloads as WL
     w = WL.get(args.config, s=args.samples)
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args, w)
     else:

@@ -122,7 +122,8 @@ void* gcpb_get_stream(gcpb_ctx* ctx);
 int gcpb_set_sparse(gcpb_ctx* ctx, int64_t nnz, const int64_t* coords, const double* values);
 /* Device-resident ingest for generated data: keys_sorted (strictly
  * increasing linear keys, device pointer) and values (device pointer of
- * value_dtype GCPB_F32/GCPB_F64); copied into the context. */
+ * value_dtype GCPB_F32/GCPB_F64); copied into the context after all work
+ * already queued on the device (any stream) has completed. */
 int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_sorted,
                            const void* d_values, int value_dtype);
 int64_t gcpb_nnz(const gcpb_ctx* ctx);
@@ -130,7 +131,8 @@ int64_t gcpb_nnz(const gcpb_ctx* ctx);
 int gcpb_get_sparse(gcpb_ctx* ctx, int64_t* coords_out, double* values_out);
 /* DenseTensor values (include/gcp/tensor.hpp:52-81), first-mode-fastest. */
 int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage);
-/* Device-resident dense ingest from a device pointer in `storage` layout. */
+/* Device-resident dense ingest from a device pointer in `storage` layout
+ * (read after all work already queued on the device has completed). */
 int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage);
 /* Synthetic dense binary tensor generated in HBM (BASELINE configs[1]):
  * x(i) ~ Bernoulli(m_i / (1 + m_i)) with m the rank-true_rank model given by
@@ -229,6 +231,10 @@ int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
  * chosen when uniform draws, one rank, Philox, the model fits in shared
  * memory and s*d*r <= 16384; GCPB_NO_SMALL=1 disables it). */
 int gcpb_steps_path(const gcpb_ctx* ctx);
+/* Kernels launched by the last gcpb_run_steps call: the kernel nodes of the
+ * replayed step graph (every kernel is this library's own), or 1 for the
+ * one-launch small-problem path. */
+int gcpb_run_steps_launches(const gcpb_ctx* ctx, int64_t* kernels);
 /* Hot rows of the sparse tensor: *rows = rows selected over
  * all modes (the most frequent rows of each mode among the nonzeros, up to 32
  * per mode), *copies = privatized copies per hot row used by the last fused

@@ -365,11 +365,14 @@ class Reference:
         L.ref_bench_model_free.argtypes = [vp]
         L.ref_bench_step_given.argtypes = [vp, C.c_int, C.c_double, C.c_int64, i64p, f64p,
                                            C.c_double, C.c_int, C.c_double, C.c_int, C.c_double,
-                                           f64p]
+                                           C.c_int, f64p]
+        L.ref_bench_step_semi_given.argtypes = [vp, C.c_int, C.c_double, C.c_int64, i64p, f64p,
+                                                C.c_int64, i64p, C.c_int64, C.c_double, C.c_int,
+                                                C.c_double, C.c_int, C.c_double, C.c_int, f64p]
         L.ref_bench_step_sampler.argtypes = [vp, vp, C.c_int, C.c_double, C.c_int, C.c_int64,
                                              C.c_int64, C.c_int64, C.c_double, C.c_uint64,
-                                             C.c_int, C.c_double, C.c_int, C.c_double, f64p,
-                                             i64p]
+                                             C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
+                                             f64p, i64p]
 
     def _ck(self, rc):
         if rc != 0:

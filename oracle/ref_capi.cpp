@@ -658,9 +658,60 @@ int ref_bench_model_new(int d, const std::int64_t* dims, std::int64_t r, const d
 }
 void ref_bench_model_free(void* h) { delete static_cast<BenchModel*>(h); }
 
+// The reference step's tail: mttkrp_sampled_all(threads) and, when do_adam,
+// adam_step (times[1], times[2]; times[2] = 0 when skipped).
+static void bench_tail(BenchModel& b, const gcp::GradientSamples& gs, int threads,
+                       double learning_rate, int has_lb, double lb, int do_adam, double* times) {
+  const auto t1 = std::chrono::steady_clock::now();
+  const gcp::GradientSet g = gcp::mttkrp_sampled_all(gs, b.model, threads);
+  const auto t2 = std::chrono::steady_clock::now();
+  times[1] = secs(t1, t2);
+  times[2] = 0.0;
+  if (!do_adam) return;
+  gcp::FitConfig cfg;
+  if (has_lb) cfg.lower_bound = lb;
+  b.state.learning_rate = learning_rate;
+  gcp::adam_step(b.model, b.state, g, cfg);
+  times[2] = secs(t2, std::chrono::steady_clock::now());
+}
+
+// Semi-stratified step on builder-supplied draws (C5, whose COO the reference
+// cannot hold): the loop body of sample_semi_stratified (samplers.hpp:199-216)
+// on p pre-drawn nonzero picks (index, value) and q pre-drawn unrestricted
+// indices (x = 0: the COO lookup of value_at is excluded), then the tail.
+int ref_bench_step_semi_given(void* bm, int loss_kind, double delta, std::int64_t p,
+                              const std::int64_t* idx_p, const double* x_p, std::int64_t q,
+                              const std::int64_t* idx_q, std::int64_t eta, double total,
+                              int threads, double learning_rate, int has_lb, double lb,
+                              int do_adam, double* times /*3*/) {
+  return guard([&] {
+    BenchModel& b = *static_cast<BenchModel*>(bm);
+    const gcp::LossFunction loss = make_loss(loss_kind, delta);
+    const int d = b.model.ndims();
+    const auto t0 = std::chrono::steady_clock::now();
+    gcp::GradientSamples gs(b.model.shape());
+    gs.reserve(p + q);
+    const double eta_over_p = p > 0 ? static_cast<double>(eta) / static_cast<double>(p) : 0.0;
+    for (std::int64_t t = 0; t < p; ++t) {
+      const std::span<const std::int64_t> span(idx_p + t * d, static_cast<std::size_t>(d));
+      const double m = b.model.entry(span);
+      gs.append(span, eta_over_p * (loss.deriv(x_p[t], m) - loss.deriv(0.0, m)));
+    }
+    const double weight = total / static_cast<double>(q > 0 ? q : 1);
+    for (std::int64_t t = 0; t < q; ++t) {
+      const std::span<const std::int64_t> span(idx_q + t * d, static_cast<std::size_t>(d));
+      const double m = b.model.entry(span);
+      gs.append(span, weight * loss.deriv(0.0, m));
+    }
+    times[0] = secs(t0, std::chrono::steady_clock::now());
+    bench_tail(b, gs, threads, learning_rate, has_lb, lb, do_adam, times);
+  });
+}
+
 int ref_bench_step_given(void* bm, int loss_kind, double delta, std::int64_t n,
                          const std::int64_t* idx, const double* x, double weight, int threads,
-                         double learning_rate, int has_lb, double lb, double* times /*3*/) {
+                         double learning_rate, int has_lb, double lb, int do_adam,
+                         double* times /*3*/) {
   return guard([&] {
     BenchModel& b = *static_cast<BenchModel*>(bm);
     const gcp::LossFunction loss = make_loss(loss_kind, delta);
@@ -673,17 +724,8 @@ int ref_bench_step_given(void* bm, int loss_kind, double delta, std::int64_t n,
       const double m = b.model.entry(span);
       gs.append(span, weight * loss.deriv(x[e], m));
     }
-    const auto t1 = std::chrono::steady_clock::now();
-    const gcp::GradientSet g = gcp::mttkrp_sampled_all(gs, b.model, threads);
-    const auto t2 = std::chrono::steady_clock::now();
-    gcp::FitConfig cfg;
-    if (has_lb) cfg.lower_bound = lb;
-    b.state.learning_rate = learning_rate;
-    gcp::adam_step(b.model, b.state, g, cfg);
-    const auto t3 = std::chrono::steady_clock::now();
-    times[0] = secs(t0, t1);
-    times[1] = secs(t1, t2);
-    times[2] = secs(t2, t3);
+    times[0] = secs(t0, std::chrono::steady_clock::now());
+    bench_tail(b, gs, threads, learning_rate, has_lb, lb, do_adam, times);
   });
 }
 
@@ -691,7 +733,7 @@ int ref_bench_step_given(void* bm, int loss_kind, double delta, std::int64_t n,
 int ref_bench_step_sampler(void* bm, void* tensor, int loss_kind, double delta, int strategy,
                            std::int64_t s, std::int64_t p, std::int64_t q, double rho,
                            std::uint64_t seed, int threads, double learning_rate, int has_lb,
-                           double lb, double* times /*3*/, std::int64_t* n_samples) {
+                           double lb, int do_adam, double* times /*3*/, std::int64_t* n_samples) {
   return guard([&] {
     BenchModel& b = *static_cast<BenchModel*>(bm);
     const TensorH* t = static_cast<TensorH*>(tensor);
@@ -700,17 +742,8 @@ int ref_bench_step_sampler(void* bm, void* tensor, int loss_kind, double delta, 
     const auto t0 = std::chrono::steady_clock::now();
     const gcp::GradientSamples gs = gcp::draw_gradient_samples(
         t->view(), b.model, loss, make_kind(strategy, s, p, q, rho), rng);
-    const auto t1 = std::chrono::steady_clock::now();
-    const gcp::GradientSet g = gcp::mttkrp_sampled_all(gs, b.model, threads);
-    const auto t2 = std::chrono::steady_clock::now();
-    gcp::FitConfig cfg;
-    if (has_lb) cfg.lower_bound = lb;
-    b.state.learning_rate = learning_rate;
-    gcp::adam_step(b.model, b.state, g, cfg);
-    const auto t3 = std::chrono::steady_clock::now();
-    times[0] = secs(t0, t1);
-    times[1] = secs(t1, t2);
-    times[2] = secs(t2, t3);
+    times[0] = secs(t0, std::chrono::steady_clock::now());
+    bench_tail(b, gs, threads, learning_rate, has_lb, lb, do_adam, times);
     *n_samples = gs.size();
   });
 }

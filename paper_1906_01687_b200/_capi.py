@@ -127,6 +127,7 @@ SIGNATURES = [
                                  C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(gcpb_adam)]),
     ("gcpb_synchronize", C.c_int, [ctx_p]),
     ("gcpb_steps_path", C.c_int, [ctx_p]),
+    ("gcpb_run_steps_launches", C.c_int, [ctx_p, C.POINTER(C.c_int64)]),
     ("gcpb_hot_rows", C.c_int, [ctx_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("gcpb_interleaved", C.c_int, [ctx_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("gcpb_gradient_full", C.c_int, [ctx_p, C.POINTER(gcpb_loss)]),

@@ -86,7 +86,9 @@ def build_engine(force: bool = False, verbose: bool = True) -> Path:
 def build_oracles(verbose: bool = True) -> None:
     targets = ["liboracle"]
     if REFERENCE.exists():
-        targets.append("ref")
+        # the reference itself, its acceptance gate, and the reference-side
+        # binding of the engine (integration/gcp_b200.hpp) compiled against it
+        targets += ["ref", "binding"]
     r = subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "-j8", *targets],
                        capture_output=True, text=True)
     if r.returncode != 0:

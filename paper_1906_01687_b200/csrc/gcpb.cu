@@ -92,9 +92,8 @@ struct DBuf {
 
 // Scratch of one ordered sample list (order_build).
 struct OrderBufs {
-  DBuf out, cnt, tmp;
+  DBuf out, cnt;
   int64_t out_cap = 0, bins_cap = 0;
-  size_t tmp_bytes = 0;
 };
 
 const char* loss_name(int kind) {
@@ -174,6 +173,35 @@ size_t dense_bytes(int storage, uint64_t n) {
   throw std::invalid_argument("unknown dense storage");
 }
 
+// Measured-choice switches, read from the environment once
+// per context at gcpb_create so that every later call -- and every cached
+// step graph -- sees the same values.  None changes results beyond the
+// gradient's summation order.
+struct Tuning {
+  int il = -1;          // GCPB_IL: interleaved [A | G] table (-1: by size)
+  int sortq = -1;       // GCPB_SORTQ: unrestricted draws in mode-0 order (-1: with IL)
+  int qshift = 6;       // GCPB_QSHIFT: log2 mode-0 rows per ordering bin
+  double hot_t = 256.0; // GCPB_HOT_T: reductions per address before a row is privatized
+  int replicas = 0;     // GCPB_REPLICAS: forced gradient replica count (0: by load)
+  bool no_small = false;  // GCPB_NO_SMALL: no one-launch small-problem path
+  bool no_bloom = false;  // GCPB_NO_BLOOM: zero sampler without the Bloom prefilter
+  int pb = 1;             // GCPB_PB: passes per batch of the slim fused kernels
+  int l2line = 0;         // GCPB_L2LINE: interleaved-table row loads fetch 128-byte lines
+  int adam = 1;           // GCPB_ADAM: streaming Adam variant for tables in HBM (0 = off)
+  void read_env() {
+    if (const char* e = getenv("GCPB_ADAM")) adam = atoi(e);
+    if (const char* e = getenv("GCPB_L2LINE")) l2line = atoi(e) != 0;
+    if (const char* e = getenv("GCPB_PB")) pb = std::max(1, atoi(e));
+    if (const char* e = getenv("GCPB_IL")) il = atoi(e) != 0;
+    if (const char* e = getenv("GCPB_SORTQ")) sortq = atoi(e) != 0;
+    if (const char* e = getenv("GCPB_QSHIFT")) qshift = std::max(0, std::min(20, atoi(e)));
+    if (const char* e = getenv("GCPB_HOT_T")) hot_t = atof(e);
+    if (const char* e = getenv("GCPB_REPLICAS")) replicas = std::max(1, atoi(e));
+    no_small = getenv("GCPB_NO_SMALL") != nullptr;
+    no_bloom = getenv("GCPB_NO_BLOOM") != nullptr;
+  }
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -182,6 +210,7 @@ size_t dense_bytes(int storage, uint64_t n) {
 struct gcpb_ctx {
   int device = 0;
   int dtype = GCPB_F32;
+  Tuning tune;  // environment switches, read once at gcpb_create
   size_t tsize = 4;
   int d = 0;
   int64_t dims[kMaxModes] = {};
@@ -277,14 +306,8 @@ struct gcpb_ctx {
 
   // stratified zero sampler
   DBuf zero_list, zstatus, ztbits;
-  // sampled segments in memory order (large tables): q draws, nonzero picks
-  OrderBufs qorder, porder;
-  // overlapped ordering inside step graphs (GCPB_ORD_OVERLAP): step k+1's
-  // list is built on a side stream while step k's Adam runs
-  OrderBufs qpre[2];
-  cudaStream_t ord_side = nullptr;
-  cudaEvent_t ord_fork = nullptr, ord_done[2] = {nullptr, nullptr};
-  int64_t ord_step = -1, ord_n = 0;
+  // semi-stratified unrestricted draws in mode-0 row order (large tables)
+  OrderBufs qorder;
   int64_t zero_cap = 0, zstatus_cap = 0, z_nchunks_first = 0;
 
   // estimator
@@ -302,6 +325,7 @@ struct gcpb_ctx {
   DBuf small_g;               // triple-buffered gradient of the small-problem kernel
   bool small_g_zero = false;
   int last_steps_path = 0;    // 0: CUDA graph of fused steps, 1: small-problem cluster kernel
+  int64_t graph_kernels = 0;  // kernel nodes of the cached step graph
   DBuf xfer_dev;
   cudaEvent_t xfer_done = nullptr;
 
@@ -321,10 +345,6 @@ struct gcpb_ctx {
     }
     if (xfer_done) cudaEventDestroy(xfer_done);
     if (comm) ncclCommDestroy(comm);
-    if (ord_fork) cudaEventDestroy(ord_fork);
-    for (auto& e : ord_done)
-      if (e) cudaEventDestroy(e);
-    if (ord_side) cudaStreamDestroy(ord_side);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -673,21 +693,7 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     }
   }
   a.scatter = 1;
-  // Factor + gradient tables beyond ~half of L2: prefetch rows a tile ahead.
-  // Measured on C5: the L2 prefetch of the next tile's rows costs more issue
-  // slots than it hides latency, so it is opt-in (GCPB_PREFETCH=1).
-  a.prefetch = 0;
-  if (const char* ev = getenv("GCPB_PREFETCH")) a.prefetch = atoi(ev);
-  // The cp.async-staged kernel (rows of the next tile staged in shared
-  // memory) is opt-in (GCPB_STAGE=1): since the plain kernel's lane groups
-  // and hot rows it is slower on C5 (6.68 vs 4.81 ms per launch, and 6.22 vs
-  // 3.85 ms on the interleaved table).
-  a.stage = 0;
-  if (const char* ev = getenv("GCPB_STAGE")) a.stage = atoi(ev);
-  // L2 hints for the staged kernel: cold rows (unrestricted draws) and
-  // nonzero records evict_first, the nonzero picks' rows evict_last.
-  a.l2hint = a.stage ? 2 : 0;
-  if (const char* ev = getenv("GCPB_L2HINT")) a.l2hint = atoi(ev);
+  a.pb = c->tune.pb;
   return a;
 }
 
@@ -710,11 +716,7 @@ constexpr int kHotRows = 32;  // hot rows per mode
 // is allocated (GCPB_REPLICAS forces the count).
 int replicas_for(const gcpb_ctx* c, int64_t n) {
   if (c->nrep_cap < 2) return 1;
-  static const int forced = [] {
-    const char* e = getenv("GCPB_REPLICAS");
-    return e ? atoi(e) : 0;
-  }();
-  if (forced > 0) return std::min(forced, c->nrep_cap);
+  if (c->tune.replicas > 0) return std::min(c->tune.replicas, c->nrep_cap);
   const int64_t chunks = std::max<int64_t>(1, c->nelem / c->vw);
   int64_t want = n / (4 * chunks);
   // short modes concentrate the reductions: a mode with n_k rows sees about
@@ -804,8 +806,7 @@ void ensure_hot(gcpb_ctx* c) {
 // reductions per address (GCPB_HOT_T), when that beats the block replicas.
 template <typename T>
 int hot_copies(gcpb_ctx* c, const FusedArgs<T>& a, int nrep) {
-  const char* te = getenv("GCPB_HOT_T");
-  const double target = te ? atof(te) : 256.0;
+  const double target = c->tune.hot_t;
   if (target <= 0.0 || c->tensor_kind != 2 || c->d > 4 || c->rp / c->vw > 64) return 0;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cs);
@@ -878,6 +879,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     a.A = c->AG.as<T>();
     a.G = c->AG.as<T>() + c->rp;
     a.pitch = static_cast<int>(2 * c->rp);
+    a.l2line = c->tune.l2line;
     for (int k = 0; k < c->d; ++k) a.off[k] = 2 * c->off[k];
     c->nrep = 1;
     a.nrep = 1;
@@ -1023,7 +1025,7 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   za.tag = tag;
   za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
   za.hmask = c->hmask;
-  za.bloom = c->nnz > 0 && getenv("GCPB_NO_BLOOM") == nullptr ? c->bloom.as<uint32_t>() : nullptr;
+  za.bloom = c->nnz > 0 && !c->tune.no_bloom ? c->bloom.as<uint32_t>() : nullptr;
   za.bmask = c->bmask;
   za.st = st;
   za.status = c->zstatus.as<unsigned long long>();
@@ -1131,7 +1133,7 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
   za.tag = tag;
   za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
   za.hmask = c->hmask;
-  za.bloom = c->nnz > 0 && getenv("GCPB_NO_BLOOM") == nullptr ? c->bloom.as<uint32_t>() : nullptr;
+  za.bloom = c->nnz > 0 && !c->tune.no_bloom ? c->bloom.as<uint32_t>() : nullptr;
   za.bmask = c->bmask;
   za.st = st;
   fill_refstream(c, za, seed, p_ref);
@@ -1185,37 +1187,24 @@ int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t 
   return kept_local;
 }
 
-// ---- sampled segments walked in memory order (tables beyond L2) -----------
-// For factor tables beyond L2 (the interleaved table), sampled segments can
-// be walked in an order with locality instead of ordinal order:
-// * the q unrestricted draws of semi-stratified sampling (samplers.hpp:
-//   211-216): ordinals t sorted by the block of their mode-0 row (the row
-//   recomputed exactly as phase_a draws it), walked as a SEG_ZERO_LIST
-//   segment of the same tag;
-// * the nonzero picks (samplers.hpp:149-151,195-199): the drawn nonzero
-//   ordinals e themselves, sorted by block, read by phase_a instead of being
-//   drawn (FusedArgs::pick_list) -- the COO is in linear-key order, so the
-//   sweep visits the last mode's rows in order and the record gathers run
-//   forward through the table (opt-in, GCPB_SORTP=1: measured slower, the
-//   sorted picks pile reductions onto the same last-mode rows).
-// A counting sort (count, scan, scatter); same draws, same weights, only the
-// gradient's summation order changes.
+// ---- unrestricted draws walked in memory order (tables beyond L2) ----------
+// For factor tables beyond L2 (the interleaved table) the q unrestricted
+// draws of semi-stratified sampling (samplers.hpp:211-216) are walked in the
+// order of their mode-0 row block instead of ordinal order: ordinals t
+// counting-sorted by (mode-0 row >> shift), the row recomputed exactly as
+// phase_a draws it, then walked as a SEG_ZERO_LIST segment of the same tag.
+// Same draws, same weights; only the gradient's summation order changes.
 struct SortSpec {
   uint64_t seed, iter;
   const uint64_t* iter_base;
   uint32_t tag;
-  int kind;  // 0: q draws by mode-0 row (value t); 1: picks by nonzero ordinal (value e)
   int64_t b0, n;
-  uint64_t range;  // n_0 (kind 0) or eta (kind 1)
+  uint64_t range;  // n_0
   uint32_t thr;    // Lemire threshold of range (32-bit draws)
   int shift;
-  // kind 0: slabs of mode 1 (bin = slab * nbins0 + (mode-0 row >> shift)),
-  // so each slab's mode-1 lines stay L2-resident while mode 0 is swept
-  uint32_t n1, thr1, slabs, nbins0;
 };
 
-__device__ __forceinline__ void sort_item(const SortSpec& sp, uint64_t it, uint64_t t,
-                                          uint32_t* bin, uint64_t* val) {
+__device__ __forceinline__ uint32_t sort_bin(const SortSpec& sp, uint64_t it, uint64_t t) {
   uint64_t key;
   if (sp.range <= (1ull << 32)) {  // phase_a: group 0, word 0, attempt 0 first
     const U4 b = philox_block(sp.seed, sp.tag, 0u, 0u, it, t);
@@ -1226,27 +1215,14 @@ __device__ __forceinline__ void sort_item(const SortSpec& sp, uint64_t it, uint6
   } else {
     key = bounded64(sp.seed, sp.tag, it, t, 0, sp.range);
   }
-  uint32_t b = static_cast<uint32_t>(key >> sp.shift);
-  if (sp.kind == 0 && sp.slabs > 1) {  // phase_a: mode 1 = word 1 of the same block
-    const U4 b1 = philox_block(sp.seed, sp.tag, 0u, 0u, it, t);
-    const uint64_t prod = static_cast<uint64_t>(b1.y) * sp.n1;
-    const uint32_t i1 = (static_cast<uint32_t>(prod) >= sp.thr1)
-                            ? static_cast<uint32_t>(prod >> 32)
-                            : bounded32_from(sp.seed, sp.tag, it, t, 1, sp.n1, sp.thr1, 1u);
-    b += static_cast<uint32_t>(static_cast<uint64_t>(i1) * sp.slabs / sp.n1) * sp.nbins0;
-  }
-  *bin = b;
-  *val = sp.kind == 0 ? t : key;
+  return static_cast<uint32_t>(key >> sp.shift);
 }
 
 __global__ void __launch_bounds__(256) order_count_kernel(SortSpec sp, uint32_t* cnt) {
   const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    uint32_t bin;
-    uint64_t v;
-    sort_item(sp, it, static_cast<uint64_t>(sp.b0 + i), &bin, &v);
-    atomicAdd(cnt + bin, 1u);
+    atomicAdd(cnt + sort_bin(sp, it, static_cast<uint64_t>(sp.b0 + i)), 1u);
   }
 }
 
@@ -1255,26 +1231,63 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(SortSpec sp, uint32_
   const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    uint32_t bin;
-    uint64_t v;
-    sort_item(sp, it, static_cast<uint64_t>(sp.b0 + i), &bin, &v);
-    out[atomicAdd(cursor + bin, 1u)] = v;
+    const uint64_t t = static_cast<uint64_t>(sp.b0 + i);
+    out[atomicAdd(cursor + sort_bin(sp, it, t), 1u)] = t;
   }
 }
 
-bool order_picks() {
-  const char* e = getenv("GCPB_SORTP");
-  return e != nullptr && atoi(e) != 0;
-}
-
-bool ord_overlap_wanted() {
-  const char* e = getenv("GCPB_ORD_OVERLAP");
-  return e != nullptr && atoi(e) != 0;
+// Exclusive scan of the bin counts into the cursors: one block walks the bins
+// in tiles of 16 per thread (the counts are L2-resident, <= a few 100k bins).
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 16;
+__global__ void __launch_bounds__(kScanThreads) order_scan_kernel(const uint32_t* __restrict__ cnt,
+                                                                  uint32_t* __restrict__ cur,
+                                                                  int64_t n) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < n; base += int64_t{kScanThreads} * kScanPer) {
+    const int64_t b = base + static_cast<int64_t>(threadIdx.x) * kScanPer;
+    uint32_t v[kScanPer];
+    uint32_t tot = 0;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      v[j] = b + j < n ? cnt[b + j] : 0u;
+      tot += v[j];
+    }
+    uint32_t inc = tot;  // inclusive warp scan of the per-thread totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += u;
+      }
+      wsum[lane] = w - wsum[lane];  // exclusive warp offsets
+      if (lane == 31) carry_s = w;
+    }
+    __syncthreads();
+    uint32_t run = carry + wsum[wid] + inc - tot;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      if (b + j < n) cur[b + j] = run;
+      run += v[j];
+    }
+    carry += carry_s;
+    __syncthreads();  // wsum / carry_s reused by the next tile
+  }
 }
 
 bool order_wanted(const gcpb_ctx* c) {
-  const char* e = getenv("GCPB_SORTQ");
-  return e ? atoi(e) != 0 : c->il_enabled;
+  return c->tune.sortq >= 0 ? c->tune.sortq != 0 : c->il_enabled;
 }
 
 // Writes the ordered list for sp into ob.out; false when it cannot (scratch
@@ -1282,11 +1295,7 @@ bool order_wanted(const gcpb_ctx* c) {
 // Sizes ob for n items in nbins bins; false inside a graph capture when it
 // would have to allocate.
 bool order_reserve(gcpb_ctx* c, OrderBufs& ob, int64_t n, int64_t nbins) {
-  size_t tmp = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, static_cast<uint32_t*>(nullptr),
-                                   static_cast<uint32_t*>(nullptr), static_cast<int>(nbins),
-                                   c->stream));
-  if (n <= ob.out_cap && nbins <= ob.bins_cap && tmp <= ob.tmp_bytes) return true;
+  if (n <= ob.out_cap && nbins <= ob.bins_cap) return true;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cs);
   if (cs != cudaStreamCaptureStatusNone) return false;
@@ -1298,20 +1307,15 @@ bool order_reserve(gcpb_ctx* c, OrderBufs& ob, int64_t n, int64_t nbins) {
     ob.cnt.alloc(static_cast<size_t>(2 * nbins) * sizeof(uint32_t));
     ob.bins_cap = nbins;
   }
-  if (tmp > ob.tmp_bytes) {
-    ob.tmp.alloc(tmp);
-    ob.tmp_bytes = tmp;
-  }
   return true;
 }
 
 int64_t order_bins(const SortSpec& sp) {
-  return (static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1) *
-         (sp.kind == 0 && sp.slabs > 1 ? sp.slabs : 1);
+  return static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1;
 }
 
-bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp, cudaStream_t stream = nullptr) {
-  if (!stream) stream = c->stream;
+bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
+  cudaStream_t stream = c->stream;
   if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
   const int64_t nbins = order_bins(sp);
   if (nbins >= (int64_t{1} << 31)) return false;
@@ -1323,49 +1327,26 @@ bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp, cudaStream_t st
   CK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nbins) * sizeof(uint32_t), stream));
   order_count_kernel<<<grid, 256, 0, stream>>>(sp, cnt);
   CK(cudaGetLastError());
-  size_t tb = ob.tmp_bytes;
-  CK(cub::DeviceScan::ExclusiveSum(ob.tmp.p, tb, cnt, cur, static_cast<int>(nbins), stream));
+  order_scan_kernel<<<1, kScanThreads, 0, stream>>>(cnt, cur, nbins);
+  CK(cudaGetLastError());
   order_scatter_kernel<<<grid, 256, 0, stream>>>(sp, cur, ob.out.as<uint64_t>());
   CK(cudaGetLastError());
   return true;
 }
 
 template <typename T>
-SortSpec order_spec(const FusedArgs<T>& a, uint32_t tag, int kind, int64_t b0, int64_t b1) {
+SortSpec order_spec(const gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int64_t b0, int64_t b1) {
   SortSpec sp;
   std::memset(&sp, 0, sizeof(sp));
   sp.seed = a.seed;
   sp.iter = a.iter;
   sp.iter_base = a.iter_base;
   sp.tag = tag;
-  sp.kind = kind;
   sp.b0 = b0;
   sp.n = b1 - b0;
-  if (kind == 0) {
-    sp.range = a.dims[0];
-    sp.thr = a.thr[0];
-    sp.shift = 6;  // 64 mode-0 rows per bin
-    if (const char* e = getenv("GCPB_QSHIFT")) sp.shift = std::max(0, std::min(20, atoi(e)));
-    sp.nbins0 = static_cast<uint32_t>(((a.dims[0] - 1) >> sp.shift) + 1);
-    sp.slabs = 1;
-    if (a.d > 1) {
-      sp.n1 = a.dims[1];
-      sp.thr1 = a.thr[1];
-      // Mode-1 slabs (opt-in, GCPB_QSLABS=k): measured on C5 (218 MB of
-      // mode-1 lines) fused 2.84 / 2.86 / 3.02 / 3.04 / 2.89 ms for
-      // 1 / 2 / 5 / 8 / 16 slabs -- the slab's lines do not stay resident
-      // under the picks' traffic, and mode 0 is swept once per slab.
-      if (const char* e = getenv("GCPB_QSLABS")) sp.slabs = std::max(1, atoi(e));
-      if (sp.slabs < 1) sp.slabs = 1;
-    }
-  } else {
-    sp.range = a.eta;
-    sp.thr = a.thr_eta;
-    int sh = 0;
-    while ((a.eta >> sh) > (1ull << 21)) ++sh;  // <= 2M bins (records of one bin: a few KB)
-    sp.shift = sh;
-    if (const char* e = getenv("GCPB_PSHIFT")) sp.shift = std::max(0, std::min(40, atoi(e)));
-  }
+  sp.range = a.dims[0];
+  sp.thr = a.thr[0];
+  sp.shift = c->tune.qshift;  // 64 mode-0 rows per bin by default
   return sp;
 }
 
@@ -1452,21 +1433,12 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   a.nseg = 0;
   const bool ordered = scatter && !record && est_kind < 0 && c->draw_stream == 0 &&
                        order_wanted(c);
-  bool ord_next = false;
-  int64_t ord_b0 = 0, ord_b1 = 0;
   if (p > 0) {
     gcpb_shard_range(p, c->rank, c->nranks, &b0, &b1);
-    // (walking the picks in COO order -- FusedArgs::pick_list -- measured
-    // slower on C5: fused 2.84 -> 3.11 ms plus 0.5 ms of ordering; opt-in
-    // GCPB_SORTP=1)
+    // (walking the picks in COO order measured slower on C5 at every bin
+    // width: fused 2.84 -> 3.11 ms plus 0.5 ms of ordering)
     const int pflag = (!strat && est_kind < 0) ? 1 : 0;
-    if (ordered && order_picks() && a.eta > 0 &&
-        order_build(c, c->porder, order_spec(a, tag_p, 1, b0, b1))) {
-      a.pick_list = c->porder.out.as<uint64_t>();  // the drawn ordinals, in COO order
-      a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, 0, b1 - b0, eta_over_p, pflag, 0);
-    } else {
-      a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p, pflag, 0);
-    }
+    a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p, pflag, 0);
   }
   if (q > 0) {
     const double zeta_d = static_cast<double>(zeta128);
@@ -1476,19 +1448,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       const double wq = c->total_d / static_cast<double>(q);
-      if (ordered && c->ord_step >= 0) {
-        // overlapped: this step's list was built on the side stream (step 0:
-        // by run_steps_impl on the main stream); join it before the fused
-        // kernel, and fork the next step's list right after it
-        const int64_t k = c->ord_step;
-        if (k > 0) CK(cudaStreamWaitEvent(c->stream, c->ord_done[k & 1], 0));
-        a.zero_list = c->qpre[k & 1].out.as<uint64_t>();
-        a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
-        ord_next = k + 1 < c->ord_n;
-        ord_b0 = b0;
-        ord_b1 = b1;
-      } else if (ordered &&
-          order_build(c, c->qorder, order_spec(a, TAG_GRAD_SEMI_Q, 0, b0, b1))) {
+      if (ordered && order_build(c, c->qorder, order_spec(c, a, TAG_GRAD_SEMI_Q, b0, b1))) {
         a.zero_list = c->qorder.out.as<uint64_t>();  // the same draws, in mode-0 row order
         a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
       } else {
@@ -1498,17 +1458,6 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   }
   res.n = p + q;
   run_fused(c, a, record, fold);
-  if (ord_next) {  // next step's list on the side stream, under this step's Adam
-    const int64_t k1 = c->ord_step + 1;
-    SortSpec sp = order_spec(a, TAG_GRAD_SEMI_Q, 0, ord_b0, ord_b1);
-    sp.iter = static_cast<uint64_t>(k1);
-    sp.iter_base = &c->dst()->graph_base;
-    CK(cudaEventRecord(c->ord_fork, c->stream));
-    CK(cudaStreamWaitEvent(c->ord_side, c->ord_fork, 0));
-    if (!order_build(c, c->qpre[k1 & 1], sp, c->ord_side))
-      throw std::logic_error("overlapped ordering: scratch not reserved");
-    CK(cudaEventRecord(c->ord_done[k1 & 1], c->ord_side));
-  }
   if (c->draw_stream == 1) {  // p picks, then d draws per tested candidate / q draw
     if (strat && q > 0 && c->nranks > 1)
       CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, 
@@ -1567,11 +1516,57 @@ void adam_launch(gcpb_ctx* c, int fold_reps = 0, int advance_rng = 0, int hot_rh
   // are the long pole and the wider grid measured slower (C3 11.5 -> 22 us)
   int lp = 1;
   while (hot.n == 0 && lp < 8 && 4 * lp < fold_reps) lp <<= 1;
-  // (2 blocks per SM stream as fast; under the overlapped ordering they leave
-  // the side stream's kernels room)
-  const int grid = grid_for(c->nelem / c->vw * lp, 256, c->num_sms, c->ord_step >= 0 ? 2 : 8) +
-                   hot.n;
-  if (c->il_pending || c->il_gpack) {  // factors (and unless packed, the gradient) in AG
+  const int64_t cpr = c->rp / c->vw;  // chunks per row
+  int cpr_shift = 0;
+  while ((int64_t{1} << cpr_shift) < cpr) ++cpr_shift;
+  const bool il_now = c->il_pending || c->il_gpack;
+  if (fold_reps == 0 && c->tune.adam > 0 && (int64_t{1} << cpr_shift) == cpr &&
+      c->nelem >= (int64_t{1} << 20)) {
+    // streaming Adam for tables in HBM (adam_stream_kernel)
+    ILTab<T> il{};
+    if (il_now) {
+      il.ag = c->AG.as<T>();
+      il.rp = static_cast<int>(c->rp);
+      il.gcontig = c->il_gpack ? 1 : 0;
+    } else {
+      a_current(c);
+    }
+    const bool nopad = c->r == c->rp;
+    const int v = c->tune.adam;
+    const int per_sm = v == 2 ? 4 : 2;
+    const int grid = grid_for(c->nelem / c->vw, 256, c->num_sms, per_sm) + hot.n;
+    auto go = [&](auto kern) {
+      CK(launch_k(kern, dim3(grid), dim3(256), 0, c->stream, c->A.as<T>(), c->Gr.as<T>(),
+                  c->B.as<T>(), c->C.as<T>(), c->nelem, static_cast<int>(c->rp), cpr_shift,
+                  static_cast<int>(c->r), c->dst(), advance_rng, hot, il));
+    };
+    constexpr bool F32 = sizeof(T) == 4;
+#define GCPB_ADAM_GO(ILV)                                                                      \
+    if (v == 3 || !F32) {                                                                      \
+      nopad ? go(adam_stream_kernel<T, ILV, false, true, 4, 2>)                                \
+            : go(adam_stream_kernel<T, ILV, false, false, 4, 2>);                              \
+    } else if (v == 2) {                                                                       \
+      nopad ? go(adam_stream_kernel<T, ILV, F32, true, 2, 4>)                                  \
+            : go(adam_stream_kernel<T, ILV, F32, false, 2, 4>);                                \
+    } else {                                                                                   \
+      nopad ? go(adam_stream_kernel<T, ILV, F32, true, 4, 2>)                                  \
+            : go(adam_stream_kernel<T, ILV, F32, false, 4, 2>);                                \
+    }
+    if (il_now) {
+      GCPB_ADAM_GO(true)
+      c->il_pending = false;
+      c->il_gpack = false;
+      c->a_stale = true;
+    } else {
+      GCPB_ADAM_GO(false)
+      c->ag_ok = false;
+    }
+#undef GCPB_ADAM_GO
+    CK(cudaGetLastError());
+    return;
+  }
+  const int grid = grid_for(c->nelem / c->vw * lp, 256, c->num_sms, 8) + hot.n;
+  if (il_now) {  // factors (and unless packed, the gradient) in AG
     ILTab<T> il;
     il.ag = c->AG.as<T>();
     il.rp = static_cast<int>(c->rp);
@@ -1823,8 +1818,7 @@ constexpr size_t kSmallModelMax = 200 * 1024;  // A, B, C replicas in shared mem
 
 template <typename T>
 bool small_eligible(const gcpb_ctx* c, const gcpb_sampler* sk) {
-  static const bool disabled = std::getenv("GCPB_NO_SMALL") != nullptr;
-  if (disabled || c->nranks != 1 || c->draw_stream != 0 || c->timing) return false;
+  if (c->tune.no_small || c->nranks != 1 || c->draw_stream != 0 || c->timing) return false;
   // red.global issue costs ~1.3 cycles per lane on the issuing SM: keep the
   // per-iteration scatter of the 8 cluster SMs well under a microsecond
   if (sk->strategy != GCPB_UNIFORM || sk->num_samples * c->d * c->r > 16384) return false;
@@ -1933,28 +1927,13 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     ensure_hash(c);
   }
   if (c->tensor_kind == 2) ensure_hot(c);  // host work: not inside the capture
-  bool overlap = false;
-  SortSpec ov_spec;
-  std::memset(&ov_spec, 0, sizeof(ov_spec));
   if (sk->strategy == GCPB_SEMI_STRATIFIED && sk->zero_samples > 0 && c->draw_stream == 0 &&
       order_wanted(c)) {  // ordering scratch for the unrestricted draws, before the capture
     int64_t b0 = 0, b1 = 0;
     gcpb_shard_range(sk->zero_samples, c->rank, c->nranks, &b0, &b1);
     FusedArgs<T> fa = base_args<T>(c, nullptr, seed, iter0);
-    const SortSpec sp = order_spec(fa, TAG_GRAD_SEMI_Q, 0, b0, b1);
+    const SortSpec sp = order_spec(c, fa, TAG_GRAD_SEMI_Q, b0, b1);
     if (sp.n > 0) order_reserve(c, c->qorder, sp.n, order_bins(sp));
-    if (sp.n > 0 && ord_overlap_wanted() && c->nranks == 1 && c->il_enabled) {
-      overlap = order_reserve(c, c->qpre[0], sp.n, order_bins(sp)) &&
-                order_reserve(c, c->qpre[1], sp.n, order_bins(sp));
-      if (overlap && !c->ord_side) {
-        CK(cudaStreamCreateWithFlags(&c->ord_side, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&c->ord_fork, cudaEventDisableTiming));
-        for (auto& e : c->ord_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      }
-      ov_spec = sp;
-      ov_spec.iter = 0;
-      ov_spec.iter_base = &c->dst()->graph_base;
-    }
   }
   set_rng_iter(c, iter0);
   if (small_eligible<T>(c, sk)) {
@@ -1969,7 +1948,7 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     ag_prepare<T>(c);  // not inside the capture
   else
     a_current(c);
-  const std::string key = steps_key(c, sk, loss, seed, n) + (overlap ? "|ov" : "");
+  const std::string key = steps_key(c, sk, loss, seed, n);
   if (!c->graph_exec || key != c->graph_key) {
     if (c->graph_exec) {
       cudaGraphExecDestroy(c->graph_exec);
@@ -1978,25 +1957,24 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      if (overlap) {  // step 0's list on the main stream, from the replay's base
-        graph_base_kernel<<<1, 1, 0, c->stream>>>(c->dst());
-        CK(cudaGetLastError());
-        if (!order_build(c, c->qpre[0], ov_spec))
-          throw std::logic_error("overlapped ordering: scratch not reserved");
-        c->ord_n = n;
-      }
-      for (int64_t k = 0; k < n; ++k) {
-        if (overlap) c->ord_step = k;
+      for (int64_t k = 0; k < n; ++k)
         step_impl<T>(c, sk, loss, seed, 0, &c->dst()->rng_iter, ZERO_CAPTURE);
-      }
-      c->ord_step = -1;
     } catch (...) {
-      c->ord_step = -1;
       cudaStreamEndCapture(c->stream, &g);
       if (g) cudaGraphDestroy(g);
       throw;
     }
     CK(cudaStreamEndCapture(c->stream, &g));
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    c->graph_kernels = 0;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      CK(cudaGraphNodeGetType(nd, &ty));
+      if (ty == cudaGraphNodeTypeKernel) ++c->graph_kernels;
+    }
     cudaGraphExec_t ex = nullptr;
     const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
@@ -2354,9 +2332,9 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
       CK(cudaMemsetAsync(b->p, 0, bytes, c->stream));
     }
     c->grad_zero = true;
+    c->tune.read_env();
     // Interleaved factor/gradient rows when the tables exceed L2 (GCPB_IL=0/1 forces)
-    c->il_enabled = bytes > (size_t{64} << 20);
-    if (const char* ev = getenv("GCPB_IL")) c->il_enabled = atoi(ev) != 0;
+    c->il_enabled = c->tune.il >= 0 ? c->tune.il != 0 : bytes > (size_t{64} << 20);
     // Privatized gradient replicas: the scatter of a small gradient (e.g. C2's
     // 51 KB) otherwise funnels every red.global into a few hundred L2 sectors,
     // where the L2 atomic units serialise per address.  Up to 32 replicas are
@@ -2366,7 +2344,7 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
       const int64_t rs = (c->nelem + 63) / 64 * 64;
       int64_t cap = static_cast<int64_t>(16) * 1024 * 1024 / std::max<int64_t>(1, rs * c->tsize);
       cap = std::min<int64_t>(cap, 32);
-      if (const char* ev = getenv("GCPB_REPLICAS")) cap = std::max(1, atoi(ev));
+      if (c->tune.replicas > 0) cap = c->tune.replicas;
       if (cap >= 2) {
         c->nrep_cap = static_cast<int>(cap);
         c->rep_stride = rs;
@@ -2374,7 +2352,6 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
         CK(cudaMemsetAsync(c->Grep.p, 0, static_cast<size_t>(rs) * cap * c->tsize, c->stream));
       }
     }
-    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);  // random gathers: 32-byte sectors
     c->dstate.alloc(sizeof(DevState));
     CK(cudaMallocHost(reinterpret_cast<void**>(&c->pinned_params), 16 * sizeof(double)));
     std::memset(&c->host_state, 0, sizeof(DevState));
@@ -2419,6 +2396,9 @@ int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_so
     if (!ctx->total_fits) throw std::invalid_argument("sparse tensor: N >= 2^64 unsupported (u64 keys)");
     if (value_dtype != GCPB_F32 && value_dtype != GCPB_F64)
       throw std::invalid_argument("value dtype must be F32 or F64");
+    // the caller's buffers may still be written by work on other streams
+    // (e.g. a generator on torch's stream): wait for the device first
+    CK(cudaDeviceSynchronize());
     ctx->nnz = nnz;
     ctx->tensor_kind = 2;
     ctx->tensor_version += 1;
@@ -2554,6 +2534,7 @@ int gcpb_set_dense_device(gcpb_ctx* ctx, const void* d_values, int storage) {
     if (!ctx->total_fits) throw std::invalid_argument("dense tensor too large to materialize");
     const size_t bytes = dense_bytes(storage, ctx->total);
     ctx->dense.alloc(bytes);
+    CK(cudaDeviceSynchronize());  // the source may be written on another stream
     CK(cudaMemcpyAsync(ctx->dense.p, d_values, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
     ctx->sync();
     ctx->dense_storage = storage;
@@ -2983,6 +2964,16 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
 }
 
 int gcpb_steps_path(const gcpb_ctx* ctx) { return ctx ? ctx->last_steps_path : -1; }
+
+int gcpb_debug_l2_fetch_granularity(size_t* out) {
+  return cudaDeviceGetLimit(out, cudaLimitMaxL2FetchGranularity) == cudaSuccess ? 0 : 1;
+}
+
+int gcpb_run_steps_launches(const gcpb_ctx* ctx, int64_t* kernels) {
+  if (!ctx || !kernels) return GCPB_ERR_USAGE;
+  *kernels = ctx->last_steps_path == 1 ? 1 : ctx->graph_kernels;
+  return GCPB_OK;
+}
 
 int gcpb_hot_rows(const gcpb_ctx* ctx, int* rows, int* copies) {
   if (!ctx) return GCPB_ERR_USAGE;

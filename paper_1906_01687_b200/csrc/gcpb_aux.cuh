@@ -31,10 +31,8 @@ struct DevState {
   uint64_t ref_ctr;      // RefStream counter (draws consumed so far)
   uint32_t ref_flag;     // RefStream: a draw hit the rejection region
   uint32_t ref_pad;
-  uint64_t graph_base;   // rng_iter at the start of a step-graph replay (ordering overlap)
 };
 
-__global__ void graph_base_kernel(DevState* st) { st->graph_base = st->rng_iter; }
 
 constexpr int kZcThreads = 256;
 constexpr int kZcItems = 8;
@@ -722,6 +720,125 @@ __global__ void __launch_bounds__(256) adam_kernel(T* __restrict__ A, T* __restr
         }
         store_chunk(B + i0, bo);
         store_chunk(C + i0, co);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->adam_done, 1u);
+    if (prev == gridDim.x - 1) {
+      st->t += 1;
+      if (advance_rng) st->rng_iter += 1;
+      st->adam_done = 0;
+    }
+  }
+}
+
+// Streaming adam_step for factor tables in HBM (no gradient replicas; C5):
+// the same update as adam_kernel's streaming path, with
+// * the per-chunk row arithmetic in 32 bits (cpr = rp / VW chunks per row,
+//   a power of two: shifts), the hot-row test one byte of hslot per row;
+// * FAST (fp32 only): the bias corrections folded into two scalars and one
+//   MUFU reciprocal square root per element,
+//     A -= (lr / c1) * B * rsqrt(C * (1 / c2) + eps)
+//   (optimizer.cpp:58-62 with its division and sqrt reassociated; fp32
+//   contexts are held to 1e-4 against the fp64 reference);
+// * NOPAD (r == rp): no padding-column test;
+// * U chunks per thread with all loads issued before any use.
+// Extra blocks fold the hot rows' copies exactly as adam_kernel does.
+template <typename T, bool IL, bool FAST, bool NOPAD, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    adam_stream_kernel(T* __restrict__ A, T* __restrict__ Gr, T* __restrict__ B,
+                       T* __restrict__ C, int64_t n, int rp, int cpr_shift, int r,
+                       DevState* st, int advance_rng, const HotAdam<T> hot,
+                       const ILTab<T> il) {
+  pdl_begin();
+  constexpr int VW = Vec<T>::W;
+  __shared__ double s_c1, s_c2;
+  if (threadIdx.x == 0) {
+    const double te = static_cast<double>(st->t + 1);
+    s_c1 = 1.0 - pow(st->beta1, te);
+    s_c2 = 1.0 - pow(st->beta2, te);
+  }
+  __syncthreads();
+  const T c1 = static_cast<T>(s_c1), c2 = static_cast<T>(s_c2);
+  const T lr = static_cast<T>(st->lr);
+  const T b1 = static_cast<T>(st->beta1), b2 = static_cast<T>(st->beta2);
+  const T ob1 = static_cast<T>(1.0 - st->beta1), ob2 = static_cast<T>(1.0 - st->beta2);
+  const T eps = static_cast<T>(st->eps);
+  const bool has_lb = st->has_lb != 0;
+  const T lb = static_cast<T>(st->lb);
+  const T step = static_cast<T>(st->lr / s_c1);  // FAST: lr / c1
+  const T ic2 = static_cast<T>(1.0 / s_c2);       // FAST: 1 / c2
+  const uint32_t nchunk = static_cast<uint32_t>(n / VW);
+  const int main_blocks = static_cast<int>(gridDim.x) - hot.n;
+  const uint32_t stride = static_cast<uint32_t>(main_blocks) * blockDim.x;
+  const uint32_t cmask = (1u << cpr_shift) - 1u;
+  if (static_cast<int>(blockIdx.x) >= main_blocks) {  // one hot row per extra block
+    const int slot = static_cast<int>(blockIdx.x) - main_blocks;
+    const int64_t row_off = hot.hot_off[slot];
+    const Vec<T> hs = hot_rows_sum(hot.Ghot, slot, hot.rh, rp, static_cast<T*>(nullptr), 0, 0,
+                                   row_off);
+    if (static_cast<int>(threadIdx.x) < rp / VW)
+      adam_chunk<T, true, IL>(A, Gr, B, C, row_off + threadIdx.x * VW,
+                              static_cast<int>(threadIdx.x) * VW, r, nullptr, 0, 0, c1, c2, lr,
+                              b1, b2, ob1, ob2, eps, has_lb, lb, hs, il);
+  } else {
+    for (uint32_t q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < nchunk; q0 += U * stride) {
+      Vec<T> a[U], g[U], b[U], c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t q = q0 + u * stride;
+        q = q < nchunk ? q : nchunk - 1;
+        const uint32_t col = (q & cmask) * VW;
+        const int64_t i0 = static_cast<int64_t>(q) * VW;
+        if (IL) {
+          T* ila = il.ag + 2 * i0 - col;
+          load_chunk_stream(ila, a[u]);
+          load_chunk_stream(il.gcontig ? Gr + i0 : ila + rp, g[u]);
+        } else {
+          load_chunk_stream(A + i0, a[u]);
+          load_chunk_stream(Gr + i0, g[u]);
+        }
+        load_chunk_stream(B + i0, b[u]);
+        load_chunk_stream(C + i0, c[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = q0 + u * stride;
+        if (q >= nchunk) break;
+        if (hot.n > 0 && __ldg(hot.hslot + (q >> cpr_shift)) != 0xFFu) continue;  // hot block
+        const uint32_t col = (q & cmask) * VW;
+        const int64_t i0 = static_cast<int64_t>(q) * VW;
+        Vec<T> ao = a[u], bo = b[u], co = c[u];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          if (NOPAD || static_cast<int>(col) + e < r) {
+            const T gv = g[u].v[e];
+            const T bv = b1 * b[u].v[e] + ob1 * gv;
+            const T cv = b2 * c[u].v[e] + ob2 * (gv * gv);
+            bo.v[e] = bv;
+            co.v[e] = cv;
+            T av;
+            if constexpr (FAST)
+              av = a[u].v[e] - step * bv * rsqrtf(cv * ic2 + eps);
+            else
+              av = a[u].v[e] - lr * (bv / c1) / sqrt((cv / c2) + eps);
+            if (has_lb) av = av > lb ? av : lb;
+            ao.v[e] = av;
+          }
+        }
+        if (IL) {
+          T* ila = il.ag + 2 * i0 - col;
+          store_chunk_stream(il.gcontig ? Gr + i0 : ila + rp, Vec<T>{});
+          store_chunk_stream(ila, ao);
+        } else {
+          store_chunk_stream(Gr + i0, Vec<T>{});
+          store_chunk_stream(A + i0, ao);
+        }
+        store_chunk_stream(B + i0, bo);
+        store_chunk_stream(C + i0, co);
       }
     }
   }

@@ -174,9 +174,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
     }
   } else if (kind == SEG_PICK) {
     uint64_t e;
-    if (a.pick_list) {  // drawn beforehand, in nonzero order (order_build)
-      e = a.pick_list[t];
-    } else if (a.refstream) {
+    if (a.refstream) {
       e = refstream_below(a.ref_key, *a.ref_ctr + static_cast<uint64_t>(sg.ref_off + t) + 1, a.eta,
                           a.thr64_eta, a.ref_flag);
     } else if (a.eta <= (1ull << 32)) {
@@ -202,7 +200,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (q * 4 < a.rec_words) v = a.l2hint ? ld_hint_u4(rp + q, policy_evict_first()) : __ldg(rp + q);
+        if (q * 4 < a.rec_words) v = __ldg(rp + q);
         wds[q * 4 + 0] = v.x;
         wds[q * 4 + 1] = v.y;
         wds[q * 4 + 2] = v.z;
@@ -277,21 +275,6 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
     for (int k = 0; k < DM; ++k)
       hs |= static_cast<uint32_t>(__ldg(a.hslot + a.rowbase[k] + ik[k])) << (8 * k);
     s.hs = hs | (DM < 4 ? (0xFFFFFFFFu << (8 * DM)) : 0u);
-  }
-  // Factor tables larger than L2 (C5: 531 MB): pull this sample's rows (and
-  // its gradient rows, so the reductions hit L2) in while the previous tile
-  // computes.  Rows are 32-byte aligned; one line prefetch per 128 bytes.
-  if (a.prefetch && s.valid) {
-#pragma unroll
-    for (int k = 0; k < DM; ++k) {
-      if (EXACT || k < d) {
-        const int64_t ro = a.off[k] + static_cast<int64_t>(ik[k]) * a.pitch;
-        for (int b = 0; b < a.rp * static_cast<int>(sizeof(T)); b += 128) {
-          prefetch_l2(reinterpret_cast<const char*>(a.A + ro) + b);
-          prefetch_l2(reinterpret_cast<const char*>(a.G + ro) + b);
-        }
-      }
-    }
   }
 }
 
@@ -373,7 +356,10 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
         for (int c = 0; c < VPL; ++c) {
           Vec<T> q;
-          load_chunk(a.A + roff[k] + cidx[c] * VW, q);
+          if (a.l2line)
+            load_chunk_l2line(a.A + roff[k] + cidx[c] * VW, q);
+          else
+            load_chunk(a.A + roff[k] + cidx[c] * VW, q);
 #pragma unroll
           for (int e = 0; e < VW; ++e) row[k][c * VW + e] = q.v[e];
         }
@@ -458,10 +444,107 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
+// Phase B of the slim hot-path kernels (no host-given samples, no records)
+// with PB passes per batch: the row gathers of PB passes are issued before
+// any of their arithmetic and reductions, so a warp keeps PB x DM row loads
+// in flight instead of DM (the tables beyond L2, C5, are bound by random-
+// access latency).
+template <typename T, int DM, int G, int PB, bool HOT>
+__device__ __forceinline__ void phase_b_batched(const FusedArgs<T>& a, const SegRegs& sg,
+                                                const uint32_t (&ik)[DM], const Drawn<T>& s,
+                                                T* __restrict__ Gb, uint32_t rsel) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int NGRP = 32 / G;
+  constexpr int NPASS = (32 + NGRP - 1) / NGRP;
+  constexpr bool POW2 = (G & (G - 1)) == 0;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const T wseg = static_cast<T>(sg.weight);
+  const int fv = sg.flag;
+  const int cidx = gl < a.nchunks ? gl : a.nchunks - 1;
+  const T cmask = gl < a.nchunks ? static_cast<T>(1) : static_cast<T>(0);
+  const bool owns = gl < a.nchunks;
+#pragma unroll 1
+  for (int p0 = 0; p0 < NPASS; p0 += PB) {
+    bool v[PB];
+    T xv[PB];
+    uint32_t hsv[PB];
+    uint32_t roff[PB][DM];
+    T row[PB][DM][VW];
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      const int pass = p0 + j;
+      const int src = (pass * NGRP + grp) & 31;
+      v[j] = __shfl_sync(FULL, s.valid, src) && pass < NPASS &&
+             (POW2 || (grp < NGRP && pass * NGRP + grp < 32));
+      xv[j] = __shfl_sync(FULL, s.x, src);
+      hsv[j] = HOT ? __shfl_sync(FULL, s.hs, src) : 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < DM; ++k) {
+        roff[j][k] = static_cast<uint32_t>(a.off[k]) +
+                     __shfl_sync(FULL, ik[k], src) * static_cast<uint32_t>(a.pitch);
+        Vec<T> q;
+        if (a.l2line)
+          load_chunk_l2line(a.A + roff[j][k] + cidx * VW, q);
+        else
+          load_chunk(a.A + roff[j][k] + cidx * VW, q);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) row[j][k][e] = q.v[e];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      T pre[DM][VW];
+      T mp = static_cast<T>(0);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        T p = row[j][0][e];
+        pre[0][e] = static_cast<T>(1);
+#pragma unroll
+        for (int k = 1; k < DM; ++k) {
+          pre[k][e] = p;
+          p = p * row[j][k][e];
+        }
+        mp += p;
+      }
+      mp *= cmask;
+      if constexpr (POW2) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
+      } else {
+        T tot = static_cast<T>(0);
+#pragma unroll
+        for (int jj = 0; jj < G; ++jj) tot += __shfl_sync(FULL, mp, (grp * G + jj) & 31);
+        mp = tot;
+      }
+      T g = loss_deriv_fast(a.loss, a.delta, xv[j], mp);
+      if (fv) g = g - loss_deriv_fast(a.loss, a.delta, static_cast<T>(0), mp);
+      const T y = wseg * g;
+      const bool act = v[j] && owns;
+      T suf[VW];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) suf[e] = static_cast<T>(1);
+#pragma unroll
+      for (int k = DM - 1; k >= 0; --k) {
+        T out[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          out[e] = y * (pre[k][e] * suf[e]);
+          suf[e] = suf[e] * row[j][k][e];
+        }
+        if (act) red_chunk(grad_row<T, HOT>(a, Gb, roff[j][k], hsv[j], k, rsel) + cidx * VW, out);
+      }
+    }
+  }
+}
+
 template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true,
-          bool HOT = false>
+          bool HOT = false, int PB = 1>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
                                                                int64_t total_tiles) {
+  static_assert(PB == 1 || (EXACT && VPL == 1 && !REC && !GV), "batched passes: slim path only");
   pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -493,7 +576,10 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
-    phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT>(a, sg, tile, ik, s, Gb, rsel);
+    if constexpr (PB > 1)
+      phase_b_batched<T, DM, G, PB, HOT>(a, sg, ik, s, Gb, rsel);
+    else
+      phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT>(a, sg, tile, ik, s, Gb, rsel);
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
     s = s2;
@@ -556,6 +642,17 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
                        : go(fused_grad_kernel<T, DM, EXACT, 6, 1, REC, GCPB_MINB_SLIM, false>);
           }
         }
+        if constexpr (sizeof(T) == 4 && DM <= 4) {
+          if (G == 4 && a.pb > 1) {  // batched passes (more row loads in flight)
+            if (a.rh > 0) {
+              *used_hot = true;
+              return a.pb >= 4 ? go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 2, false, true, 4>)
+                               : go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 3, false, true, 2>);
+            }
+            return a.pb >= 4 ? go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 2, false, false, 4>)
+                             : go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 3, false, false, 2>);
+          }
+        }
         if constexpr (DM <= 4) {
           if (a.rh > 0) {  // hot rows privatized (sparse, skewed modes)
             *used_hot = true;
@@ -593,235 +690,6 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
   return go(fused_grad_kernel<T, DM, EXACT, 32, 8, REC, 1>);
 }
 
-// ---------------------------------------------------------------------------
-// Staged variant for factor tables that exceed L2 (C5: 531 MB).  Phase A of
-// tile i+1 also issues cp.async copies of each sample's d factor rows into a
-// per-warp double buffer in shared memory (lane = sample, 16-byte copies, no
-// registers held), so the HBM gather latency of the next tile overlaps the
-// current tile's Phase B, which reads its rows from shared memory.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem),
-               "l"(pol)
-               : "memory");
-}
-// Per-segment L2 policy of the staged kernel (FusedArgs::l2hint); 0 = none.
-template <typename T>
-__device__ __forceinline__ uint64_t seg_policy(const FusedArgs<T>& a, int kind) {
-  if (a.l2hint == 0) return 0ull;
-  if (kind == SEG_PICK) return a.l2hint == 2 ? policy_evict_last() : 0ull;
-  return policy_evict_first();
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <typename T, int DM>
-__device__ __forceinline__ void stage_rows(const FusedArgs<T>& a, T* slot,
-                                           const uint32_t (&ik)[DM], bool valid, uint64_t pol) {
-  constexpr int VW = Vec<T>::W;
-  if (valid) {
-#pragma unroll
-    for (int k = 0; k < DM; ++k) {
-      const T* src = a.A + a.off[k] + static_cast<int64_t>(ik[k]) * a.pitch;
-      if (pol)
-        for (int c = 0; c < a.nchunks; ++c)
-          cp_async16_hint(slot + k * a.rp + c * VW, src + c * VW, pol);
-      else
-        for (int c = 0; c < a.nchunks; ++c) cp_async16(slot + k * a.rp + c * VW, src + c * VW);
-    }
-  }
-  cp_async_commit();
-}
-
-template <typename T, int DM, int G, bool HOT = false>
-__device__ __forceinline__ void phase_b_staged(const FusedArgs<T>& a, const SegRegs& sg,
-                                               const T* wbuf, const Drawn<T>& s,
-                                               const uint32_t (&ik)[DM], T* __restrict__ Gb,
-                                               uint32_t rsel = 0) {
-  constexpr int VW = Vec<T>::W;
-  constexpr int NGRP = 32 / G;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int grp = lane / G;
-  const int gl = lane % G;
-  const bool given = sg.kind == SEG_GIVEN;
-  const T wseg = static_cast<T>(sg.weight);
-  const uint64_t pol = seg_policy(a, sg.kind);
-  const int cidx = gl < a.nchunks ? gl : a.nchunks - 1;
-  const T cmask = gl < a.nchunks ? static_cast<T>(1) : static_cast<T>(0);
-  const bool owns = gl < a.nchunks;
-#pragma unroll 1
-  for (int pass = 0; pass < G; ++pass) {
-    const int src = pass * NGRP + grp;
-    const bool v = __shfl_sync(FULL, s.valid, src);
-    uint32_t ii[DM];
-#pragma unroll
-    for (int k = 0; k < DM; ++k) ii[k] = __shfl_sync(FULL, ik[k], src);
-    const T xv = __shfl_sync(FULL, s.x, src);
-    const uint32_t hsv = HOT ? __shfl_sync(FULL, s.hs, src) : 0xFFFFFFFFu;
-    T wv = wseg;
-    int fv = sg.flag;
-    if (given) {
-      wv = static_cast<T>(__shfl_sync(FULL, s.w, src));
-      fv = __shfl_sync(FULL, s.flag, src);
-    }
-    const T* rows = wbuf + src * DM * a.rp;
-    T row[DM][VW], pre[DM][VW];
-#pragma unroll
-    for (int k = 0; k < DM; ++k) {
-      Vec<T> q;
-      if constexpr (sizeof(T) == 4) {
-        const float4 f = *reinterpret_cast<const float4*>(rows + k * a.rp + cidx * VW);
-        q.v[0] = f.x, q.v[1] = f.y, q.v[2] = f.z, q.v[3] = f.w;
-      } else {
-        const double2 f = *reinterpret_cast<const double2*>(rows + k * a.rp + cidx * VW);
-        q.v[0] = f.x, q.v[1] = f.y;
-      }
-#pragma unroll
-      for (int e = 0; e < VW; ++e) row[k][e] = q.v[e];
-    }
-    T mp = static_cast<T>(0);
-#pragma unroll
-    for (int e = 0; e < VW; ++e) {
-      T p = row[0][e];
-      pre[0][e] = static_cast<T>(1);
-#pragma unroll
-      for (int k = 1; k < DM; ++k) {
-        pre[k][e] = p;
-        p = p * row[k][e];
-      }
-      mp += p;
-    }
-    mp *= cmask;
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
-    T g = loss_deriv_fast(a.loss, a.delta, xv, mp);
-    if (fv) g = g - loss_deriv_fast(a.loss, a.delta, static_cast<T>(0), mp);
-    const T y = wv * g;
-    if (a.scatter && v && owns) {
-      T suf[VW];
-#pragma unroll
-      for (int e = 0; e < VW; ++e) suf[e] = static_cast<T>(1);
-#pragma unroll
-      for (int k = DM - 1; k >= 0; --k) {
-        T out[VW];
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-          out[e] = y * (pre[k][e] * suf[e]);
-          suf[e] = suf[e] * row[k][e];
-        }
-        T* gp = grad_row<T, HOT>(a, Gb,
-                                 static_cast<uint32_t>(a.off[k]) +
-                                     ii[k] * static_cast<uint32_t>(a.pitch),
-                                 hsv, k, rsel) +
-                cidx * VW;
-        if (pol)
-          red_chunk_hint(gp, out, pol);
-        else
-          red_chunk(gp, out);
-      }
-    }
-  }
-}
-
-template <typename T, int DM, int G, bool HOT = false>
-__global__ void __launch_bounds__(256, 2) fused_staged_kernel(const FusedArgs<T> a,
-                                                              int64_t total_tiles) {
-  pdl_begin();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  T* Gb = a.G + static_cast<int64_t>(blockIdx.x % a.nrep) * a.rep_stride;
-  const int slot_elems = DM * a.rp;              // one sample's rows
-  T* wbuf = reinterpret_cast<T*>(smem_raw) + static_cast<int64_t>(wib) * 2 * 32 * slot_elems;
-  const uint64_t iter = a.iter + (a.iter_base ? __ldg(a.iter_base) : 0ull);
-  int64_t tile = warp0;
-  if (tile >= total_tiles) return;
-  uint32_t ik[DM];
-  Drawn<T> s;
-  const uint32_t rsel = HOT ? static_cast<uint32_t>(warp0) & static_cast<uint32_t>(a.rh - 1) : 0u;
-  SegRegs sg = seg_of<T>(a, tile);
-  phase_a<T, DM, true, true, HOT>(a, sg, sg.t_begin + (tile - sg.tiles_begin) * 32 + lane, iter,
-                                  ik, s);
-  int buf = 0;
-  stage_rows<T, DM>(a, wbuf + (buf * 32 + lane) * slot_elems, ik, s.valid, seg_policy(a, sg.kind));
-  for (; tile < total_tiles; tile += nwarps) {
-    const int64_t next = tile + nwarps;
-    uint32_t ik2[DM];
-    Drawn<T> s2;
-    SegRegs sg2 = sg;
-    if (next < total_tiles) {
-      sg2 = seg_of<T>(a, next);
-      phase_a<T, DM, true, true, HOT>(a, sg2, sg2.t_begin + (next - sg2.tiles_begin) * 32 + lane,
-                                      iter, ik2, s2);
-    } else {
-      s2.valid = false;
-      if (HOT) s2.hs = 0xFFFFFFFFu;
-#pragma unroll
-      for (int k = 0; k < DM; ++k) ik2[k] = 0;
-    }
-    stage_rows<T, DM>(a, wbuf + ((buf ^ 1) * 32 + lane) * slot_elems, ik2, s2.valid,
-                      seg_policy(a, sg2.kind));
-    cp_async_wait<1>();  // this tile's rows have landed; the next tile's stay in flight
-    __syncwarp();
-    phase_b_staged<T, DM, G, HOT>(a, sg, wbuf + buf * 32 * slot_elems, s, ik, Gb, rsel);
-    __syncwarp();        // the buffer is restaged two tiles later
-#pragma unroll
-    for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
-    s = s2;
-    sg = sg2;
-    buf ^= 1;
-  }
-  cp_async_wait<0>();
-}
-
-template <typename T, int DM>
-bool launch_staged(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream, int num_sms,
-                   cudaError_t* err, bool* used_hot) {
-  const int G = pow2ceil(a.nchunks);
-  const size_t smem = static_cast<size_t>(8) * 2 * 32 * DM * a.rp * sizeof(T);
-  if (G > 8 || smem > 110 * 1024) return false;
-  auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-    if (per_sm < 1) per_sm = 1;
-    int64_t blocks = (total_tiles + 7) / 8;
-    const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    *err = launch_k(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), smem, stream, a,
-                    total_tiles);
-  };
-  if (a.rh > 0) {
-    *used_hot = true;
-    switch (G) {
-      case 1: go(fused_staged_kernel<T, DM, 1, true>); break;
-      case 2: go(fused_staged_kernel<T, DM, 2, true>); break;
-      case 4: go(fused_staged_kernel<T, DM, 4, true>); break;
-      default: go(fused_staged_kernel<T, DM, 8, true>); break;
-    }
-    return true;
-  }
-  switch (G) {
-    case 1: go(fused_staged_kernel<T, DM, 1>); break;
-    case 2: go(fused_staged_kernel<T, DM, 2>); break;
-    case 4: go(fused_staged_kernel<T, DM, 4>); break;
-    default: go(fused_staged_kernel<T, DM, 8>); break;
-  }
-  return true;
-}
-
 template <typename T, bool REC>
 cudaError_t launch_fused_rec(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
                              int num_sms, bool* used_hot) {
@@ -844,15 +712,6 @@ cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record
                          cudaStream_t stream, int num_sms, bool* used_hot) {
   *used_hot = false;
   if (total_tiles <= 0) return cudaSuccess;
-  bool special = false;
-  for (int s = 0; s < a.nseg; ++s) special = special || a.seg[s].kind >= SEG_GIVEN;
-  if (!record && a.stage && !special && (a.d == 3 || a.d == 4)) {
-    cudaError_t err = cudaSuccess;
-    const bool done =
-        a.d == 3 ? launch_staged<T, 3>(a, total_tiles, stream, num_sms, &err, used_hot)
-                 : launch_staged<T, 4>(a, total_tiles, stream, num_sms, &err, used_hot);
-    if (done) return err;
-  }
   if (record) return launch_fused_rec<T, true>(a, total_tiles, stream, num_sms, used_hot);
   return launch_fused_rec<T, false>(a, total_tiles, stream, num_sms, used_hot);
 }

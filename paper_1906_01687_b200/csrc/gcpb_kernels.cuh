@@ -128,7 +128,6 @@ struct FusedArgs {
   int nseg;
   Seg seg[3];
   const uint64_t* zero_list;
-  const uint64_t* pick_list;  // optional: SEG_PICK reads its drawn ordinals e from here
   // given samples
   const int64_t* g_idx;
   const double* g_x;
@@ -143,6 +142,8 @@ struct FusedArgs {
   double* r_m;
   double* r_y;
   int scatter;
+  int pb;  // host-side: passes per batch of the slim kernels (1 = unbatched)
+  int l2line;  // row loads fetch whole 128-byte L2 lines (interleaved table)
   // RefStream mode: draws reproduce the reference's RngStream
   // (rng.cpp:43-61): u = mix64(key + phi * (counter + j + 1)), value u % n,
   // with j the draw's position in the reference's consumption order.
@@ -152,13 +153,6 @@ struct FusedArgs {
   uint64_t thr64[kMaxModes];  // (2^64 - n_k) mod n_k
   uint64_t thr64_eta;
   unsigned* ref_flag;         // set when a draw would have been rejected
-  int prefetch;  // 1: prefetch the next tile's rows into L2 (opt-in)
-  int stage;     // 1: factor tables exceed L2 -> cp.async-staged kernel variant
-  // L2 residency hints for factor tables that exceed L2 (staged kernel):
-  // 0 none; 1 rows of unrestricted/uniform draws and nonzero records
-  // evict_first (no reuse), so the nonzero picks' hot rows stay; 2 as 1 and
-  // the picks' rows evict_last.
-  int l2hint;
   // Hot rows: the most frequent rows of each mode among the
   // nonzeros (C3-C5 draw Zipf-skewed coordinates, so one row can take 12 % of
   // all picks) receive their reductions in rh privatized copies instead of the
@@ -280,6 +274,41 @@ __device__ __forceinline__ void load_chunk(const double* p, Vec<double>& out) {
   out.v[1] = q.y;
 }
 
+// Streaming (touch-once) chunk loads and stores: no L1 allocation on loads,
+// evict-first stores.  `stream_mode` picks the flavour under test.
+__device__ __forceinline__ void load_chunk_stream(const float* p, Vec<float>& out) {
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(out.v[0]), "=f"(out.v[1]), "=f"(out.v[2]), "=f"(out.v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void load_chunk_stream(const double* p, Vec<double>& out) {
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(out.v[0]), "=d"(out.v[1])
+               : "l"(p));
+}
+__device__ __forceinline__ void store_chunk_stream(float* p, const Vec<float>& v) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.v[0]), "f"(v.v[1]),
+               "f"(v.v[2]), "f"(v.v[3])
+               : "memory");
+}
+__device__ __forceinline__ void store_chunk_stream(double* p, const Vec<double>& v) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.v[0]), "d"(v.v[1]) : "memory");
+}
+
+// Row-chunk loads that ask L2 to fetch the whole 128-byte line on a miss
+// (interleaved [A row | G row] table: the gradient half the reduction needs
+// arrives in the same DRAM access as the factor half).
+__device__ __forceinline__ void load_chunk_l2line(const float* p, Vec<float>& out) {
+  asm("ld.global.nc.L2::128B.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(out.v[0]), "=f"(out.v[1]), "=f"(out.v[2]), "=f"(out.v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void load_chunk_l2line(const double* p, Vec<double>& out) {
+  asm("ld.global.nc.L2::128B.v2.f64 {%0, %1}, [%2];"
+               : "=d"(out.v[0]), "=d"(out.v[1])
+               : "l"(p));
+}
+
 __device__ __forceinline__ void store_chunk(float* p, const Vec<float>& v) {
   *reinterpret_cast<float4*>(p) = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
 }
@@ -297,36 +326,6 @@ __device__ __forceinline__ void red_chunk(float* p, const float (&v)[4]) {
 __device__ __forceinline__ void red_chunk(double* p, const double (&v)[2]) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v[0]) : "memory");
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(v[1]) : "memory");
-}
-
-// L2 eviction-priority policies (createpolicy) and hinted accesses.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint4 ld_hint_u4(const uint4* p, uint64_t pol) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void red_chunk_hint(float* p, const float (&v)[4], uint64_t pol) {
-  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
-               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void red_chunk_hint(double* p, const double (&v)[2], uint64_t pol) {
-  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v[0]), "l"(pol)
-               : "memory");
-  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p + 1), "d"(v[1]), "l"(pol)
-               : "memory");
 }
 
 // Streaming loads of tensor data that should not displace factor rows in L1.
@@ -366,10 +365,6 @@ __device__ __forceinline__ uint64_t refstream_below(uint64_t key, uint64_t ctr, 
   const uint64_t u = mix64(key + 0x9e3779b97f4a7c15ull * ctr);
   if (u < thr) atomicOr(flag, 1u);
   return u % n;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
 // Open-addressing membership test: 2^b buckets of four u64 keys (one 32-byte

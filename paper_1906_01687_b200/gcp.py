@@ -492,6 +492,12 @@ class Engine:
         """Engine of the last run_steps: "graph" or "small" (cluster kernel)."""
         return {0: "graph", 1: "small"}.get(int(lib.gcpb_steps_path(self._h)), "unknown")
 
+    def run_steps_launches(self) -> int:
+        """Kernels the last run_steps launched (step-graph kernel nodes)."""
+        n = C.c_int64()
+        self._ck(lib.gcpb_run_steps_launches(self._h, C.byref(n)))
+        return int(n.value)
+
     @property
     def hot_rows(self) -> tuple:
         """(hot rows selected, copies per hot row used by the last scatter)."""

@@ -504,28 +504,3 @@ def test_bit_and_byte_storage_agree(orc):
     assert rc == 0
     grad = orc.mttkrp(dims, r, F32, want["idx"], want["y"])
     assert O.rel_error(e.grad_flat(), grad) <= TOL["f32"]
-
-
-@pytest.mark.parametrize("dims,r,strategy", [((60, 40, 50), 16, 2), ((30, 20, 25, 10), 8, 1),
-                                             ((50, 40, 30), 20, 0)])
-def test_staged_kernel_parity(orc, monkeypatch, dims, r, strategy):
-    """The cp.async-staged kernel (opt-in, GCPB_STAGE=1) forced on a
-    small problem: same gradient as the oracle."""
-    monkeypatch.setenv("GCPB_STAGE", "1")
-    g = G()
-    rs = np.random.default_rng(sum(dims) + r)
-    coords, vals = _sparse_problem(rs, dims, 1500, values="count")
-    F = _as_dtype([rs.uniform(0.05, 1.0, (n, r)) for n in dims], "f32")
-    e = g.Engine(dims, r, dtype="f32")
-    e.set_sparse(coords, vals)
-    e.set_factors(F)
-    sk = {0: g.SamplerKind.uniform(3000), 1: g.SamplerKind.stratified(1000, 2000),
-          2: g.SamplerKind.semi_stratified(1000, 2000)}[strategy]
-    e.stoch_grad(sk, g.LossFunction.poisson(), 21, 4)
-    t = O.Tensor(dims, coords, vals)
-    rc, want = orc.draw_gradient_samples(t, r, F, 1, 0.0, strategy, sk.num_samples,
-                                         sk.nonzero_samples, sk.zero_samples, sk.oversample,
-                                         orc.source(1, seed=21, it=4))
-    assert rc == 0
-    grad = orc.mttkrp(dims, r, F, want["idx"], want["y"])
-    assert O.rel_error(e.grad_flat(), grad) <= TOL["f32"]
