@@ -347,8 +347,10 @@ def config_of(w, world):
             "samples_per_gpu_step": w.samples_per_step,
             "global_batch": w.samples_per_step * world,
             "rank": w.rank, "dims": list(w.dims), "loss": w.loss, "sampler": w.sampler,
-            "parallelism": (f"dp{world}: sample ordinals sharded, factors replicated, NCCL "
-                            f"all-reduce of the gradient") if world > 1 else "single GPU",
+            "parallelism": (f"dp{world}: nonzeros (contiguous ranges) and sample ordinals "
+                            "sharded, factors replicated; gradient reduce-scatter + sharded "
+                            "Adam + factor all-gather in one peer-memory kernel over NVLink "
+                            "(NCCL rank barriers)") if world > 1 else "single GPU",
             "l2": "inputs larger than L2 (tensor in HBM); factor rows L1/L2-resident by "
                   "design (they are the model)"}
 
@@ -386,7 +388,12 @@ def run_ours(args, w):
     if world > 1:
         uid = [G.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        e.comm_init(uid[0], rank, world)
+        e.comm_init(uid[0], rank, world)  # also shards the nonzeros (contiguous ranges)
+        # every rank's factor/gradient table mapped into every rank (CUDA IPC):
+        # the step's exchange is one reduce-scatter + Adam + all-gather kernel
+        handles = [None] * world
+        dist.all_gather_object(handles, e.peer_handle())
+        e.peer_open(handles)
     e.set_shard(rank, world)
     sk = sampler_of(w, G, world)
     loss = G.LossFunction.parse(w.loss)

@@ -350,6 +350,23 @@ int gcpb_snapshot_restore(gcpb_ctx* ctx);
 int gcpb_nccl_unique_id(char out[128]);
 int gcpb_comm_init(gcpb_ctx* ctx, const char unique_id[128], int rank, int nranks);
 int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks);
+/* Peer-mapped tables (NVLink / NVSwitch peer memory), the multi-GPU exchange
+ * of the reference's per-worker partial reduction (src/kernels.cpp:148-166)
+ * fused with adam_step (src/optimizer.cpp:47-66): after gcpb_peer_open every
+ * sharded step runs ONE kernel per rank that reads its shard of rows' gradient
+ * from every rank's table (P2P loads), sums it in rank order, re-zeroes it
+ * there, applies Adam with its own moment rows (ZeRO-1) and writes the updated
+ * factor rows into every rank's table (P2P stores), between two rank
+ * barriers (NCCL, or the host communicator's all-gather).
+ * gcpb_peer_handle exports this rank's table (CUDA IPC handle + layout) into
+ * GCPB_PEER_HANDLE_BYTES bytes; every rank exchanges them out of band and
+ * calls gcpb_peer_open with all nranks blobs in rank order (same-process peers
+ * are used directly, others mapped with cudaIpcOpenMemHandle).  Only this
+ * rank's moment rows are maintained afterwards (gcpb_get_moment returns the
+ * shard's rows current, the others stale). */
+#define GCPB_PEER_HANDLE_BYTES 256
+int gcpb_peer_handle(gcpb_ctx* ctx, void* out);
+int gcpb_peer_open(gcpb_ctx* ctx, const void* handles, int nranks);
 int gcpb_allreduce_grad(gcpb_ctx* ctx);
 /* Host-callback communicator, an alternative to NCCL for process groups the
  * caller already has (gloo, MPI) and for in-process multi-context tests:

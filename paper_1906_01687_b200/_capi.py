@@ -20,6 +20,7 @@ lib = C.CDLL(str(_LIB_PATH))
 
 # status codes (gcpb.h)
 OK, ERR_RUNTIME, ERR_USAGE, ERR_DOMAIN, ERR_RANGE, ERR_LOGIC = 0, 1, 2, 3, 4, 5
+PEER_HANDLE_BYTES = 256  # GCPB_PEER_HANDLE_BYTES (include/gcpb.h)
 F32, F64 = 0, 1
 STORE_U8, STORE_F32, STORE_F64, STORE_BIT = 0, 1, 2, 3
 UNIFORM, STRATIFIED, SEMI_STRATIFIED = 0, 1, 2
@@ -152,6 +153,8 @@ SIGNATURES = [
     ("gcpb_nccl_unique_id", C.c_int, [C.c_char_p]),
     ("gcpb_comm_init", C.c_int, [ctx_p, C.c_char_p, C.c_int, C.c_int]),
     ("gcpb_set_shard", C.c_int, [ctx_p, C.c_int, C.c_int]),
+    ("gcpb_peer_handle", C.c_int, [ctx_p, C.c_void_p]),
+    ("gcpb_peer_open", C.c_int, [ctx_p, C.c_char_p, C.c_int]),
     ("gcpb_allreduce_grad", C.c_int, [ctx_p]),
     ("gcpb_comm_init_host", C.c_int, [ctx_p, C.c_int, C.c_int, ALLGATHER_FN, ALLREDUCE_FN,
                                       C.c_void_p]),

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -185,13 +187,9 @@ struct Tuning {
   int replicas = 0;     // GCPB_REPLICAS: forced gradient replica count (0: by load)
   bool no_small = false;  // GCPB_NO_SMALL: no one-launch small-problem path
   bool no_bloom = false;  // GCPB_NO_BLOOM: zero sampler without the Bloom prefilter
-  int pb = 1;             // GCPB_PB: passes per batch of the slim fused kernels
-  int l2line = 0;         // GCPB_L2LINE: interleaved-table row loads fetch 128-byte lines
   int adam = 1;           // GCPB_ADAM: streaming Adam variant for tables in HBM (0 = off)
   void read_env() {
     if (const char* e = getenv("GCPB_ADAM")) adam = atoi(e);
-    if (const char* e = getenv("GCPB_L2LINE")) l2line = atoi(e) != 0;
-    if (const char* e = getenv("GCPB_PB")) pb = std::max(1, atoi(e));
     if (const char* e = getenv("GCPB_IL")) il = atoi(e) != 0;
     if (const char* e = getenv("GCPB_SORTQ")) sortq = atoi(e) != 0;
     if (const char* e = getenv("GCPB_QSHIFT")) qshift = std::max(0, std::min(20, atoi(e)));
@@ -262,6 +260,13 @@ struct gcpb_ctx {
   DBuf dense;
   int64_t nnz = 0;
   DBuf nzrec, vals, keys;  // AoS nonzero records, values, sorted linear keys
+  // Nonzero sharding: with nranks > 1 the records hold only
+  // this rank's contiguous range [nz_begin, nz_end) of the sorted order; keys
+  // and values stay whole (membership hash, value lookups).
+  int64_t nz_begin = 0, nz_end = 0;
+  DBuf pick_list;           // picks of the global stream in range (pick_compact_kernel)
+  int64_t pick_cap = 0;
+  DBuf mr_counts;           // multi-rank stratified: all-gathered accept counts
   int rec_words = 4;
   DBuf hkeys, hvals;
   uint64_t hmask = 0;
@@ -301,6 +306,12 @@ struct gcpb_ctx {
   gcpb_allreduce_f64_fn host_allreduce = nullptr;
   void* host_user = nullptr;
   DBuf comm_buf;
+  // peer-mapped factor/gradient tables of every rank (gcpb_peer_open): the
+  // fused reduce-scatter + Adam + all-gather kernel (peer_adam_kernel)
+  bool peer_ok = false;
+  std::vector<void*> peer_a, peer_g;  // row bases per rank
+  std::vector<void*> peer_ipc;        // mappings to close
+  DBuf barrier_buf;                   // one int64 all-reduced as a rank barrier
   DBuf zscratch;  // multi-rank stratified: this rank's accepts of one batch
   int64_t zscratch_cap = 0;
 
@@ -344,6 +355,7 @@ struct gcpb_ctx {
       cudaFreeHost(xfer_host);
     }
     if (xfer_done) cudaEventDestroy(xfer_done);
+    for (void* pmap : peer_ipc) cudaIpcCloseMemHandle(pmap);
     if (comm) ncclCommDestroy(comm);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
@@ -632,6 +644,53 @@ void check_data_domain(gcpb_ctx* c, int loss_kind) {
                             " loss: data value out of domain (x >= 0 required)");
 }
 
+bool nz_sharded(const gcpb_ctx* c) { return c->tensor_kind == 2 && c->nranks > 1; }
+
+void no_nz_shard(const gcpb_ctx* c, const char* what) {
+  if (nz_sharded(c))
+    throw std::invalid_argument(std::string(what) +
+                                " needs the whole nonzero set: not available on a "
+                                "nonzero-sharded context (gcpb_set_shard with nranks > 1)");
+}
+
+// (Re)builds the nonzero records for this rank's range (all of them on one
+// rank) from the sorted keys and values; the hot-row selection and cached
+// step graphs follow the tensor version.
+template <typename T>
+void apply_nz_shard_t(gcpb_ctx* c) {
+  int64_t b = 0, e = c->nnz;
+  if (c->nranks > 1) gcpb_shard_range(c->nnz, c->rank, c->nranks, &b, &e);
+  const bool whole = b == 0 && e == c->nnz;
+  if (c->tensor_kind != 2 || (b == c->nz_begin && e == c->nz_end)) {
+    c->nz_begin = b;
+    c->nz_end = e;
+    return;
+  }
+  const bool had_whole = c->nz_begin == 0 && c->nz_end == c->nnz;
+  c->nz_begin = b;
+  c->nz_end = e;
+  c->tensor_version += 1;
+  if (whole && had_whole) return;
+  const int64_t n = e - b;
+  c->nzrec.reset();  // shrink to the range
+  c->nzrec.alloc(static_cast<size_t>(std::max<int64_t>(n, 1)) * c->rec_words * sizeof(uint32_t));
+  if (n > 0) {
+    T* v = c->vals.as<T>() + b;
+    keys_to_records_kernel<T, T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
+        c->keys.as<uint64_t>() + b, v, n, c->d, c->dims_dev.as<int64_t>(), c->nzrec.as<uint32_t>(),
+        c->rec_words, v);
+    CK(cudaGetLastError());
+  }
+  c->sync();
+}
+
+void apply_nz_shard(gcpb_ctx* c) {
+  if (c->dtype == GCPB_F32)
+    apply_nz_shard_t<float>(c);
+  else
+    apply_nz_shard_t<double>(c);
+}
+
 template <typename T>
 FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64_t iter) {
   FusedArgs<T> a;
@@ -684,8 +743,8 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     a.thr_eta = c->nnz > 0 && static_cast<uint64_t>(c->nnz) <= (1ull << 32)
                     ? lemire_threshold32(static_cast<uint64_t>(c->nnz))
                     : 0u;
-    a.nz_begin = 0;
-    a.nz_end = c->nnz;
+    a.nz_begin = c->nz_begin;
+    a.nz_end = c->nz_end;
     if (c->hash_ready) {
       a.hkeys = c->hkeys.as<uint64_t>();
       a.hvals = c->hvals.as<uint32_t>();
@@ -693,7 +752,6 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     }
   }
   a.scatter = 1;
-  a.pb = c->tune.pb;
   return a;
 }
 
@@ -737,7 +795,7 @@ void ensure_hot(gcpb_ctx* c) {
   if (c->hot_version == c->tensor_version) return;
   c->hot_version = c->tensor_version;
   c->hot_n = 0;
-  if (c->tensor_kind != 2 || c->nnz <= 0 || c->d > 4) return;
+  if (c->tensor_kind != 2 || c->nz_end <= c->nz_begin || c->d > 4) return;
   int64_t rows = 0;
   for (int k = 0; k < c->d; ++k) {
     c->row_base[k] = static_cast<uint32_t>(rows);
@@ -751,8 +809,9 @@ void ensure_hot(gcpb_ctx* c) {
   RowBase rb;
   std::memset(&rb, 0, sizeof(rb));
   for (int k = 0; k < c->d; ++k) rb.v[k] = c->row_base[k];
-  row_hist_kernel<<<grid_for(c->nnz, 256, c->num_sms), 256, 0, c->stream>>>(
-      c->nzrec.as<uint32_t>(), c->rec_words, static_cast<int>(c->tsize / 4), c->nnz, c->d, rb,
+  const int64_t nloc = c->nz_end - c->nz_begin;  // this rank's records
+  row_hist_kernel<<<grid_for(nloc, 256, c->num_sms), 256, 0, c->stream>>>(
+      c->nzrec.as<uint32_t>(), c->rec_words, static_cast<int>(c->tsize / 4), nloc, c->d, rb,
       hist.as<uint32_t>());
   CK(cudaGetLastError());
   std::vector<uint32_t> h(static_cast<size_t>(rows));
@@ -761,7 +820,7 @@ void ensure_hot(gcpb_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
   std::vector<uint8_t> slot(static_cast<size_t>(rows), 0xFF);
   std::vector<int64_t> hoff;
-  const double nnz = static_cast<double>(c->nnz);
+  const double nnz = static_cast<double>(std::max<int64_t>(1, nloc));
   for (int k = 0; k < c->d; ++k) {
     c->hot_base[k] = static_cast<uint32_t>(hoff.size());
     c->hot_fmax[k] = 0.0;
@@ -879,7 +938,6 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     a.A = c->AG.as<T>();
     a.G = c->AG.as<T>() + c->rp;
     a.pitch = static_cast<int>(2 * c->rp);
-    a.l2line = c->tune.l2line;
     for (int k = 0; k < c->d; ++k) a.off[k] = 2 * c->off[k];
     c->nrep = 1;
     a.nrep = 1;
@@ -913,7 +971,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot));
   if (a.scatter) c->hot_last = used_hot ? a.rh : 0;
   if (ev1) CK(cudaEventRecord(ev1, c->stream));
-  if (il && !fold) {  // the all-reduce needs the gradient contiguous
+  if (il && !fold && !c->peer_ok) {  // the all-reduce needs the gradient contiguous
     const int64_t nchunk = c->nelem / c->vw;
     CK(launch_k(ag_pack_kernel<T>, dim3(grid_for(nchunk, 256, c->num_sms, 8)), dim3(256), 0,
                 c->stream, c->AG.as<T>(), c->Gr.as<T>(), nchunk, static_cast<int>(c->rp)));
@@ -926,9 +984,12 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
   c->hot_pending = 0;
   if (used_hot && fold) {  // the fused Adam folds the hot rows' copies itself
     c->hot_pending = a.rh;
+  } else if (used_hot && il && c->peer_ok) {  // into the table's gradient rows (peer path)
+    CK(launch_k(hot_fold_kernel<T>, dim3(c->hot_n), dim3(256), 0, c->stream, c->Ghot.as<T>(), a.rh,
+                static_cast<int>(c->rp), c->hot_off.as<int64_t>(), c->AG.as<T>(), 1));
   } else if (used_hot) {   // hot rows' copies into the gradient
     CK(launch_k(hot_fold_kernel<T>, dim3(c->hot_n), dim3(256), 0, c->stream, c->Ghot.as<T>(), a.rh,
-                static_cast<int>(c->rp), c->hot_off.as<int64_t>(), c->Gr.as<T>()));
+                static_cast<int>(c->rp), c->hot_off.as<int64_t>(), c->Gr.as<T>(), 0));
   }
 }
 
@@ -1004,10 +1065,8 @@ void launch_zero_cand(const gcpb_ctx* c, int grid, const ZeroArgs& za) {
   }
 }
 
-void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
-                      const uint64_t* iter_base, uint32_t tag, int mode, int64_t p_ref = 0) {
-  if (mode != ZERO_CAPTURE) prepare_zero_sampler(c, q, rho);
-  const int64_t nchunks = c->z_nchunks_first;
+ZeroArgs zero_args(gcpb_ctx* c, uint64_t seed, uint64_t iter, const uint64_t* iter_base,
+                   uint32_t tag, int64_t p_ref) {
   DevState* st = c->dst();
   ZeroArgs za;
   std::memset(&za, 0, sizeof(za));
@@ -1032,6 +1091,15 @@ void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_
   za.tbits = c->ztbits.as<uint32_t>();
   za.zero_list = c->zero_list.as<uint64_t>();
   fill_refstream(c, za, seed, p_ref);
+  return za;
+}
+
+void run_zero_sampler(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
+                      const uint64_t* iter_base, uint32_t tag, int mode, int64_t p_ref = 0) {
+  if (mode != ZERO_CAPTURE) prepare_zero_sampler(c, q, rho);
+  const int64_t nchunks = c->z_nchunks_first;
+  DevState* st = c->dst();
+  const ZeroArgs za = zero_args(c, seed, iter, iter_base, tag, p_ref);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
   for (int b = 0; b < 3; ++b) {
     CK(launch_k(zero_plan_kernel, dim3(1), dim3(1), 0, c->stream, st, b == 0 ? 1 : 0));
@@ -1102,89 +1170,154 @@ void comm_allreduce_grad(gcpb_ctx* c) {
   c->sync();
 }
 
-// Multi-rank stratified zero sampler: every rank runs the
-// reference's batch formula on the global shortfall, tests its contiguous
-// slice of the batch's candidate ordinals, all-gathers its accept count, and
-// keeps the accepts whose global rank (candidate order = rank order) is below
-// the remaining need — exactly the first q non-hits of the single-rank run.
-// Returns this rank's kept count (its zero_list prefix).
-int64_t run_zero_sampler_multirank(gcpb_ctx* c, int64_t q, double rho, uint64_t seed,
-                                   uint64_t iter, uint32_t tag, gcpb_stats* stats,
-                                   int64_t p_ref = 0) {
+// Multi-rank stratified zero sampler, device-planned
+// (zero_plan_mr_kernel and friends, gcpb_aux.cuh): per batch, plan -> test
+// this rank's slice -> all-gather the accept counts -> keep the accepts below
+// the global need -> commit.  Three batches per call are queued; inside a
+// step graph (ZERO_CAPTURE, NCCL all-gather captured) a shortfall is flagged
+// like the single-rank sampler's; eager calls continue on the host until q
+// accepts exist.  This rank's kept list is zero_list[0, zg_kept).
+
+// Sizes the multi-rank scratch and uploads the per-call scalars (not inside
+// a graph capture).
+void prepare_zero_sampler_mr(gcpb_ctx* c, int64_t q, double rho) {
   ensure_hash(c);
   const double zeta = static_cast<double>(c->total128 - static_cast<unsigned __int128>(c->nnz));
+  const int64_t first_batch = zero_batch_size_dev(c->total_d, zeta, rho, q);
+  const int64_t slice = first_batch / c->nranks + 1;  // batches shrink with the shortfall
+  const int64_t nchunks = (slice + kZcChunk - 1) / kZcChunk;
   if (c->zero_cap < q) {
     c->zero_list.alloc(static_cast<size_t>(q) * sizeof(uint64_t));
     c->zero_cap = q;
   }
-  DevState* st = c->dst();
-  ZeroArgs za;
-  std::memset(&za, 0, sizeof(za));
-  za.d = c->d;
-  uint64_t stride = 1;
-  for (int k = 0; k < c->d; ++k) {
-    za.dims[k] = static_cast<uint32_t>(c->dims[k]);
-    za.thr[k] = lemire_threshold32(static_cast<uint64_t>(c->dims[k]));
-    za.stride[k] = stride;
-    stride *= static_cast<uint64_t>(c->dims[k]);
+  if (c->zscratch_cap < slice) {
+    c->zscratch.alloc(static_cast<size_t>(slice) * sizeof(uint64_t));
+    c->zscratch_cap = slice;
   }
-  za.seed = seed;
-  za.iter = iter;
-  za.tag = tag;
-  za.hkeys = c->nnz > 0 ? c->hkeys.as<uint64_t>() : nullptr;
-  za.hmask = c->hmask;
-  za.bloom = c->nnz > 0 && !c->tune.no_bloom ? c->bloom.as<uint32_t>() : nullptr;
-  za.bmask = c->bmask;
-  za.st = st;
-  fill_refstream(c, za, seed, p_ref);
-  int64_t tested = 0, accepted = 0, kept_local = 0;
-  while (std::min(accepted, q) < q) {
-    const int64_t batch = zero_batch_size_dev(c->total_d, zeta, rho, q - accepted);
-    int64_t lo = 0, hi = 0;
-    gcpb_shard_range(batch, c->rank, c->nranks, &lo, &hi);
-    const int64_t size = hi - lo;
-    int64_t mine = 0;
-    if (size > 0) {
-      const int64_t nchunks = (size + kZcChunk - 1) / kZcChunk;
-      if (c->zstatus_cap < nchunks) {
-        c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
-        c->ztbits.alloc(static_cast<size_t>(nchunks) * kZcThreads * sizeof(uint32_t));
-        c->zstatus_cap = nchunks;
-      }
-      if (c->zscratch_cap < size) {
-        c->zscratch.alloc(static_cast<size_t>(size) * sizeof(uint64_t));
-        c->zscratch_cap = size;
-      }
-      CK(cudaMemcpyAsync(&st->z_status_cap, &c->zstatus_cap, 8, cudaMemcpyHostToDevice,
-                         c->stream));
-      zero_plan_slice_kernel<<<1, 1, 0, c->stream>>>(st, tested + lo, size, nchunks);
-      za.status = c->zstatus.as<unsigned long long>();
-      za.tbits = c->ztbits.as<uint32_t>();
-      za.zero_list = c->zscratch.as<uint64_t>();
-      const int grid =
-          static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, c->num_sms * 4)));
-      launch_zero_cand(c, grid, za);
-      CK(launch_k(zero_scatter_kernel, dim3(grid), dim3(kZcThreads), 0, c->stream, za));
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(&mine, &st->z_accepted, 8, cudaMemcpyDeviceToHost, c->stream));
-      c->sync();
-    }
-    const std::vector<int64_t> counts = comm_allgather_i64(c, mine);
-    int64_t offset = 0, keep = 0;
-    gcpb_stratified_keep(counts.data(), c->nranks, c->rank, q - accepted, &offset, &keep);
-    if (keep > 0)
-      CK(cudaMemcpyAsync(c->zero_list.as<uint64_t>() + kept_local, c->zscratch.p,
-                         static_cast<size_t>(keep) * 8, cudaMemcpyDeviceToDevice, c->stream));
-    kept_local += keep;
-    for (int64_t v : counts) accepted += v;
-    tested += batch;
+  if (c->zstatus_cap < nchunks) {
+    c->zstatus.alloc(static_cast<size_t>(nchunks) * sizeof(unsigned long long));
+    c->ztbits.alloc(static_cast<size_t>(nchunks) * kZcThreads * sizeof(uint32_t));
+    c->zstatus_cap = nchunks;
+  }
+  c->mr_counts.alloc(static_cast<size_t>(c->nranks + 1) * sizeof(int64_t));
+  c->z_nchunks_first = nchunks;
+  DevState* st = c->dst();
+  c->host_state.zg_q = q;
+  c->host_state.z_total = c->total_d;
+  c->host_state.z_zeta = zeta;
+  c->host_state.z_rho = rho;
+  c->host_state.z_status_cap = c->zstatus_cap;
+  CK(cudaMemcpyAsync(&st->zg_q, &c->host_state.zg_q, sizeof(int64_t), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(&st->z_total, &c->host_state.z_total, 3 * sizeof(double),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&st->z_status_cap, &c->host_state.z_status_cap, sizeof(int64_t),
+                     cudaMemcpyHostToDevice, c->stream));
+}
+
+// All ranks' z_accepted (this batch's accepts) -> mr_counts[0, nranks).
+void allgather_accepts(gcpb_ctx* c) {
+  int64_t* counts = c->mr_counts.as<int64_t>();
+  if (c->comm) {
+    nck(ncclAllGather(&c->dst()->z_accepted, counts, 1, ncclInt64, c->comm, c->stream),
+        "ncclAllGather");
+    return;
+  }
+  if (!c->host_allgather) throw std::logic_error("multi-rank call without a communicator");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(c->stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    throw std::logic_error("the host communicator cannot be captured in a step graph");
+  int64_t mine = 0;
+  CK(cudaMemcpyAsync(&mine, &c->dst()->z_accepted, 8, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  std::vector<int64_t> all(static_cast<size_t>(c->nranks), 0);
+  if (c->host_allgather(c->host_user, mine, all.data()) != 0)
+    throw std::runtime_error("host allgather callback failed");
+  CK(cudaMemcpyAsync(counts, all.data(), all.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  c->sync();
+}
+
+void zero_batch_mr(gcpb_ctx* c, const ZeroArgs& za, int grid, bool first) {
+  DevState* st = c->dst();
+  CK(launch_k(zero_plan_mr_kernel, dim3(1), dim3(1), 0, c->stream, st, first ? 1 : 0, c->rank,
+              c->nranks));
+  launch_zero_cand(c, grid, za);
+  CK(launch_k(zero_scatter_kernel, dim3(grid), dim3(kZcThreads), 0, c->stream, za));
+  allgather_accepts(c);
+  const int64_t* counts = c->mr_counts.as<int64_t>();
+  const int kgrid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>((c->zscratch_cap + 255) / 256, c->num_sms * 2)));
+  CK(launch_k(zero_keep_mr_kernel, dim3(kgrid), dim3(256), 0, c->stream,
+              static_cast<const DevState*>(st), counts, c->rank,
+              static_cast<const uint64_t*>(c->zscratch.as<uint64_t>()), c->zero_list.as<uint64_t>()));
+  CK(launch_k(zero_commit_mr_kernel, dim3(1), dim3(1), 0, c->stream, st, counts, c->rank,
+              c->nranks));
+  CK(cudaGetLastError());
+}
+
+void run_zero_sampler_mr(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint64_t iter,
+                         const uint64_t* iter_base, uint32_t tag, int mode, int64_t p_ref,
+                         gcpb_stats* stats) {
+  if (mode != ZERO_CAPTURE) prepare_zero_sampler_mr(c, q, rho);
+  ZeroArgs za = zero_args(c, seed, iter, iter_base, tag, p_ref);
+  za.zero_list = c->zscratch.as<uint64_t>();  // this rank's accepts of one batch
+  const int grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(c->z_nchunks_first, c->num_sms * 4)));
+  for (int b = 0; b < 3; ++b) zero_batch_mr(c, za, grid, b == 0);
+  if (mode == ZERO_CAPTURE) {
+    CK(launch_k(zero_check_mr_kernel, dim3(1), dim3(1), 0, c->stream, c->dst()));
+    CK(cudaGetLastError());
+    return;
+  }
+  for (;;) {
+    c->pull_state();
+    if (c->host_state.z_overflow) throw std::logic_error("zero sampler: status overflow");
+    if (c->host_state.zg_accepted >= q) break;
+    zero_batch_mr(c, za, grid, false);
   }
   if (stats) {
-    stats->tested = tested;
-    stats->accepted = accepted;
-    stats->rejected = tested - accepted;
+    stats->tested = c->host_state.zg_tested;
+    stats->accepted = c->host_state.zg_accepted;
+    stats->rejected = c->host_state.zg_rejected;
   }
-  return kept_local;
+}
+
+// Nonzero-sharded ranks: the picks of the global stream that fall in this
+// rank's nonzero range, compacted into pick_list[0, pick_n) (pick_compact_kernel).
+template <typename T>
+void build_pick_list(gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int64_t p) {
+  if (c->pick_cap < p) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      throw std::logic_error("pick list not reserved before the step-graph capture");
+    c->pick_list.alloc(static_cast<size_t>(p) * sizeof(uint64_t));
+    c->pick_cap = p;
+  }
+  PickSpec ps;
+  std::memset(&ps, 0, sizeof(ps));
+  ps.seed = a.seed;
+  ps.iter = a.iter;
+  ps.iter_base = a.iter_base;
+  ps.tag = tag;
+  ps.thr_eta = a.thr_eta;
+  ps.p = p;
+  ps.eta = a.eta;
+  ps.nz_begin = c->nz_begin;
+  ps.nz_end = c->nz_end;
+  ps.refstream = a.refstream;
+  ps.ref_key = a.ref_key;
+  ps.thr64_eta = a.thr64_eta;
+  ps.ref_ctr = a.ref_ctr;
+  ps.ref_flag = a.ref_flag;
+  int64_t* cnt = &c->dst()->pick_n;
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t), c->stream));
+  const int grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, static_cast<int64_t>(c->num_sms) * 8)));
+  CK(launch_k(pick_compact_kernel, dim3(grid), dim3(256), 0, c->stream, ps,
+              c->pick_list.as<uint64_t>(), cnt));
+  CK(cudaGetLastError());
 }
 
 // ---- unrestricted draws walked in memory order (tables beyond L2) ----------
@@ -1414,17 +1547,17 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   }
   const double eta_over_p = p > 0 ? static_cast<double>(eta) / static_cast<double>(p) : 0.0;
   const bool strat = sk->strategy == GCPB_STRATIFIED;
-  int64_t zero_kept_local = q;
+  bool zero_mr = false;  // multi-rank: this rank's zero list length is on the device
   if (strat && q > 0) {
     if (zeta128 < static_cast<unsigned __int128>(q))
       throw std::invalid_argument("sample_zeros_rejection: requested " + std::to_string(q) +
                                   " zeros but only " + u128_to_string(zeta128) + " exist");
     if (c->nranks > 1) {
-      if (zero_mode != ZERO_HOST_CHECK || record)
-        throw std::invalid_argument(
-            "multi-rank stratified sampling runs host-checked (gcpb_stoch_grad / gcpb_step)");
-      zero_kept_local = run_zero_sampler_multirank(c, q, sk->oversample, seed, iter, tag_z,
-                                                   &res.stats, p);
+      if (record)
+        throw std::invalid_argument("multi-rank stratified sampling records no samples");
+      run_zero_sampler_mr(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p,
+                          &res.stats);
+      zero_mr = true;
     } else {
       run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p);
     }
@@ -1438,13 +1571,24 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     // (walking the picks in COO order measured slower on C5 at every bin
     // width: fused 2.84 -> 3.11 ms plus 0.5 ms of ordering)
     const int pflag = (!strat && est_kind < 0) ? 1 : 0;
-    a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p, pflag, 0);
+    if (nz_sharded(c)) {
+      // every rank draws the whole global pick stream and keeps its range
+      if (record) throw std::invalid_argument("nonzero-sharded ranks record no samples");
+      build_pick_list<T>(c, a, tag_p, p);
+      a.pick_list = c->pick_list.as<uint64_t>();
+      Seg sg = make_seg(SEG_PICK, tag_p, 0, p, eta_over_p, pflag, 0);
+      sg.len_dev = &c->dst()->pick_n;
+      a.seg[a.nseg++] = sg;
+    } else {
+      a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p, pflag, 0);
+    }
   }
   if (q > 0) {
     const double zeta_d = static_cast<double>(zeta128);
     if (strat) {
-      a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, tag_z, 0, zero_kept_local,
-                                 zeta_d / static_cast<double>(q), 0, p, p);
+      Seg sg = make_seg(SEG_ZERO_LIST, tag_z, 0, q, zeta_d / static_cast<double>(q), 0, p, p);
+      if (zero_mr) sg.len_dev = &c->dst()->zg_kept;
+      a.seg[a.nseg++] = sg;
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       const double wq = c->total_d / static_cast<double>(q);
@@ -1459,9 +1603,9 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   res.n = p + q;
   run_fused(c, a, record, fold);
   if (c->draw_stream == 1) {  // p picks, then d draws per tested candidate / q draw
-    if (strat && q > 0 && c->nranks > 1)
-      CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, 
-          c->dst(), static_cast<uint64_t>(p + res.stats.tested * c->d), 0, c->d));
+    if (strat && q > 0 && zero_mr)
+      CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, c->dst(),
+                  static_cast<uint64_t>(p), 2, c->d));
     else if (strat && q > 0)
       CK(launch_k(ref_advance_kernel, dim3(1), dim3(1), 0, c->stream, c->dst(), static_cast<uint64_t>(p), 1, c->d));
     else
@@ -1646,6 +1790,9 @@ void set_sparse_normalized_device(gcpb_ctx* c, const uint64_t* d_keys, const dou
     CK(cudaGetLastError());
   }
   c->sync();
+  c->nz_begin = 0;
+  c->nz_end = n;
+  apply_nz_shard(c);
 }
 
 void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
@@ -1682,6 +1829,9 @@ void set_sparse_normalized(gcpb_ctx* c, const std::vector<uint64_t>& keys,
     c->sync();
   }
   c->sync();
+  c->nz_begin = 0;
+  c->nz_end = n;
+  apply_nz_shard(c);
 }
 
 template <typename T>
@@ -1747,6 +1897,57 @@ void check_step_args(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss
   check_data_domain(ctx, loss->kind);
 }
 
+// Barrier over the ranks: every rank's queued work completes before any
+// rank's later work starts (NCCL: a one-element all-reduce in stream order,
+// capturable; host communicator: synchronise + an all-gather callback).
+void rank_barrier(gcpb_ctx* c) {
+  if (c->nranks == 1) return;
+  if (c->comm) {
+    c->barrier_buf.alloc(sizeof(int64_t));
+    nck(ncclAllReduce(c->barrier_buf.p, c->barrier_buf.p, 1, ncclInt64, ncclSum, c->comm,
+                      c->stream),
+        "ncclAllReduce(barrier)");
+    return;
+  }
+  if (!c->host_allgather) throw std::logic_error("multi-rank call without a communicator");
+  c->sync();
+  std::vector<int64_t> sink(static_cast<size_t>(c->nranks));
+  if (c->host_allgather(c->host_user, 0, sink.data()) != 0)
+    throw std::runtime_error("host allgather callback failed");
+}
+
+template <typename T>
+void peer_adam_launch(gcpb_ctx* c, int advance_rng) {
+  PeerTabs<T> pt;
+  std::memset(&pt, 0, sizeof(pt));
+  for (int p = 0; p < c->nranks; ++p) {
+    pt.a[p] = static_cast<T*>(c->peer_a[static_cast<size_t>(p)]);
+    pt.g[p] = static_cast<T*>(c->peer_g[static_cast<size_t>(p)]);
+  }
+  pt.npeers = c->nranks;
+  pt.self = c->rank;
+  const bool il = c->il_enabled;
+  pt.pitch = static_cast<int>(il ? 2 * c->rp : c->rp);
+  int cpr_shift = 0;
+  while ((int64_t{1} << cpr_shift) < c->rp / c->vw) ++cpr_shift;
+  const int64_t rows = c->nelem / c->rp;
+  int64_t row0 = 0, row1 = 0;
+  gcpb_shard_range(rows, c->rank, c->nranks, &row0, &row1);
+  const int grid = grid_for(std::max<int64_t>(1, (row1 - row0) << cpr_shift), 256, c->num_sms, 4);
+  constexpr bool FAST = sizeof(T) == 4;
+  CK(launch_k(peer_adam_kernel<T, FAST>, dim3(grid), dim3(256), 0, c->stream, pt, c->B.as<T>(),
+              c->C.as<T>(), row0, row1, static_cast<int>(c->rp), cpr_shift,
+              static_cast<int>(c->r), c->dst(), advance_rng));
+  CK(cudaGetLastError());
+  if (il) {
+    c->a_stale = true;  // the factors live in the tables (AG)
+    c->il_pending = false;
+    c->il_gpack = false;
+  } else {
+    c->ag_ok = false;
+  }
+}
+
 // One iteration: fused sample->MTTKRP, all-reduce when sharded, fused Adam
 // (which folds the replica reduction when not sharded).
 template <typename T>
@@ -1761,8 +1962,15 @@ void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint6
     int fold = 0;
     if (multi) {
       if (!has_comm(c)) throw std::logic_error("sharded step without a communicator");
-      if (!c->comm && zero_mode == ZERO_CAPTURE)
-        throw std::invalid_argument("graph-replayed multi-rank steps need an NCCL communicator");
+      if (c->peer_ok) {  // reduce-scatter + sharded Adam + all-gather, one kernel
+        rank_barrier(c);
+        peer_adam_launch<T>(c, iter_base ? 1 : 0);
+        rank_barrier(c);
+        c->in_step = false;
+        c->hot_pending = 0;
+        c->grad_zero = true;
+        return;
+      }
       comm_allreduce_grad<T>(c);
     } else if (c->nrep > 1) {
       fold = c->nrep;
@@ -1914,6 +2122,19 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
                     uint64_t iter0, int64_t n, const gcpb_adam* adam) {
   set_adam_params(c, adam);
   ensure_grad_zero(c);
+  if (c->nranks > 1 && !c->comm) {
+    // the host communicator cannot be captured in a graph: step eagerly
+    for (int64_t k = 0; k < n; ++k)
+      step_impl<T>(c, sk, loss, seed, iter0 + static_cast<uint64_t>(k), nullptr, ZERO_HOST_CHECK);
+    c->last_steps_path = 0;
+    c->graph_kernels = 0;
+    return;
+  }
+  if (nz_sharded(c) && sk->strategy != GCPB_UNIFORM && sk->nonzero_samples > 0 &&
+      c->pick_cap < sk->nonzero_samples) {  // pick list, before the capture
+    c->pick_list.alloc(static_cast<size_t>(sk->nonzero_samples) * sizeof(uint64_t));
+    c->pick_cap = sk->nonzero_samples;
+  }
   if (sk->strategy == GCPB_STRATIFIED) {
     int64_t q = sk->zero_samples + (c->nnz == 0 ? sk->nonzero_samples : 0);
     if (q > 0) {
@@ -1921,7 +2142,10 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
       if (zeta < static_cast<unsigned __int128>(q))
         throw std::invalid_argument("sample_zeros_rejection: requested " + std::to_string(q) +
                                     " zeros but only " + u128_to_string(zeta) + " exist");
-      prepare_zero_sampler(c, q, sk->oversample);
+      if (c->nranks > 1)
+        prepare_zero_sampler_mr(c, q, sk->oversample);
+      else
+        prepare_zero_sampler(c, q, sk->oversample);
     }
   } else if (sk->strategy == GCPB_UNIFORM && c->tensor_kind == 2) {
     ensure_hash(c);
@@ -2270,6 +2494,35 @@ void set_global_error(const std::string& msg) { g_global_err = msg; }
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+// ---- peer-mapped tables (NVLink / NVSwitch peer memory) ---------------------
+namespace {
+struct PeerBlob {  // gcpb_peer_handle's export: one rank's table, mappable anywhere
+  uint32_t magic;
+  int32_t pid, device, il, dtype, rp, pitch, pad;
+  int64_t nelem;
+  cudaIpcMemHandle_t ha, hg;  // allocations holding the factor / gradient rows
+  uint64_t raw_a, raw_g;      // row bases (same-process peers use them as is)
+  uint64_t base_a, base_g;    // allocation bases (row base = base + offset)
+};
+constexpr uint32_t kPeerMagic = 0x47435042u;  // "GCPB"
+static_assert(sizeof(PeerBlob) <= GCPB_PEER_HANDLE_BYTES, "peer blob size");
+
+template <typename T>
+void peer_tables(gcpb_ctx* c, void** a, void** g, int* pitch) {
+  if (c->il_enabled) {  // the interleaved table: factor rows at +0, gradient rows at +rp
+    ag_prepare<T>(c);
+    *a = c->AG.p;
+    *g = c->AG.as<T>() + c->rp;
+    *pitch = static_cast<int>(2 * c->rp);
+  } else {
+    a_current(c);
+    *a = c->A.p;
+    *g = c->Gr.p;
+    *pitch = static_cast<int>(c->rp);
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char* gcpb_version(void) { return "gcpb 0.1 (sm_100a)"; }
@@ -2455,6 +2708,9 @@ int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_so
       CK(cudaGetLastError());
     }
     ctx->sync();
+    ctx->nz_begin = 0;
+    ctx->nz_end = nnz;
+    apply_nz_shard(ctx);
   });
 }
 
@@ -2965,10 +3221,6 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
 
 int gcpb_steps_path(const gcpb_ctx* ctx) { return ctx ? ctx->last_steps_path : -1; }
 
-int gcpb_debug_l2_fetch_granularity(size_t* out) {
-  return cudaDeviceGetLimit(out, cudaLimitMaxL2FetchGranularity) == cudaSuccess ? 0 : 1;
-}
-
 int gcpb_run_steps_launches(const gcpb_ctx* ctx, int64_t* kernels) {
   if (!ctx || !kernels) return GCPB_ERR_USAGE;
   *kernels = ctx->last_steps_path == 1 ? 1 : ctx->graph_kernels;
@@ -3007,6 +3259,7 @@ int gcpb_gradient_full(gcpb_ctx* ctx, const gcpb_loss* loss) {
 int gcpb_gradient_poisson_implicit(gcpb_ctx* ctx, const gcpb_loss* loss) {
   return guard(ctx, [&] {
     validate_loss(loss);
+    no_nz_shard(ctx, "gradient_poisson_implicit");
     if (ctx->dtype == GCPB_F32)
       poisson_implicit_impl<float>(ctx, loss);
     else
@@ -3018,6 +3271,7 @@ int gcpb_gradient_moments(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb
                           int64_t trials, uint64_t seed, double* mean, double* variance) {
   return guard(ctx, [&] {
     check_step_args(ctx, sampler, loss);
+    no_nz_shard(ctx, "gradient_moments");
     if (ctx->dtype == GCPB_F32)
       gradient_moments_impl<float>(ctx, sampler, loss, trials, seed, mean, variance);
     else
@@ -3030,6 +3284,7 @@ int gcpb_bias_variance(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_lo
                        double* variance) {
   return guard(ctx, [&] {
     check_step_args(ctx, sampler, loss);
+    no_nz_shard(ctx, "empirical_bias_variance");
     if (ctx->dtype == GCPB_F32)
       bias_variance_impl<float>(ctx, sampler, loss, trials, seed, exact, bias, variance);
     else
@@ -3389,6 +3644,84 @@ int gcpb_comm_init(gcpb_ctx* ctx, const char unique_id[128], int rank, int nrank
     nck(ncclCommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
     ctx->rank = rank;
     ctx->nranks = nranks;
+    apply_nz_shard(ctx);
+  });
+}
+
+int gcpb_peer_handle(gcpb_ctx* ctx, void* out) {
+  return guard(ctx, [&] {
+    if (!out) throw std::invalid_argument("peer handle: null output");
+    PeerBlob b;
+    std::memset(&b, 0, sizeof(b));
+    void *a = nullptr, *g = nullptr;
+    int pitch = 0;
+    if (ctx->dtype == GCPB_F32)
+      peer_tables<float>(ctx, &a, &g, &pitch);
+    else
+      peer_tables<double>(ctx, &a, &g, &pitch);
+    ensure_grad_zero(ctx);
+    ctx->sync();
+    b.magic = kPeerMagic;
+    b.pid = static_cast<int32_t>(getpid());
+    b.device = ctx->device;
+    b.il = ctx->il_enabled ? 1 : 0;
+    b.dtype = ctx->dtype;
+    b.rp = static_cast<int32_t>(ctx->rp);
+    b.pitch = pitch;
+    b.nelem = ctx->nelem;
+    void* base_a = ctx->il_enabled ? ctx->AG.p : ctx->A.p;
+    void* base_g = ctx->il_enabled ? ctx->AG.p : ctx->Gr.p;
+    CK(cudaIpcGetMemHandle(&b.ha, base_a));
+    CK(cudaIpcGetMemHandle(&b.hg, base_g));
+    b.raw_a = reinterpret_cast<uint64_t>(a);
+    b.raw_g = reinterpret_cast<uint64_t>(g);
+    b.base_a = reinterpret_cast<uint64_t>(base_a);
+    b.base_g = reinterpret_cast<uint64_t>(base_g);
+    std::memset(out, 0, GCPB_PEER_HANDLE_BYTES);
+    std::memcpy(out, &b, sizeof(b));
+  });
+}
+
+int gcpb_peer_open(gcpb_ctx* ctx, const void* handles, int nranks) {
+  return guard(ctx, [&] {
+    if (!handles) throw std::invalid_argument("peer open: null handles");
+    if (nranks != ctx->nranks || nranks < 1 || nranks > kMaxPeers)
+      throw std::invalid_argument("peer open: need one handle per rank of the communicator "
+                                  "(<= 16 ranks)");
+    for (void* pmap : ctx->peer_ipc) cudaIpcCloseMemHandle(pmap);
+    ctx->peer_ipc.clear();
+    ctx->peer_a.assign(static_cast<size_t>(nranks), nullptr);
+    ctx->peer_g.assign(static_cast<size_t>(nranks), nullptr);
+    ctx->peer_ok = false;
+    const char* hb = static_cast<const char*>(handles);
+    const int32_t me = static_cast<int32_t>(getpid());
+    PeerBlob mine;
+    std::memcpy(&mine, hb + static_cast<size_t>(ctx->rank) * GCPB_PEER_HANDLE_BYTES, sizeof(mine));
+    for (int p = 0; p < nranks; ++p) {
+      PeerBlob b;
+      std::memcpy(&b, hb + static_cast<size_t>(p) * GCPB_PEER_HANDLE_BYTES, sizeof(b));
+      if (b.magic != kPeerMagic) throw std::invalid_argument("peer open: not a gcpb peer handle");
+      if (b.il != mine.il || b.dtype != mine.dtype || b.rp != mine.rp || b.pitch != mine.pitch ||
+          b.nelem != mine.nelem)
+        throw std::invalid_argument("peer open: ranks hold differently shaped tables");
+      if (b.pid == me) {  // same process (threads / one-GPU emulation): raw pointers
+        ctx->peer_a[static_cast<size_t>(p)] = reinterpret_cast<void*>(b.raw_a);
+        ctx->peer_g[static_cast<size_t>(p)] = reinterpret_cast<void*>(b.raw_g);
+        continue;
+      }
+      void *ma = nullptr, *mg = nullptr;
+      CK(cudaIpcOpenMemHandle(&ma, b.ha, cudaIpcMemLazyEnablePeerAccess));
+      ctx->peer_ipc.push_back(ma);
+      if (b.base_g == b.base_a) {
+        mg = ma;
+      } else {
+        CK(cudaIpcOpenMemHandle(&mg, b.hg, cudaIpcMemLazyEnablePeerAccess));
+        ctx->peer_ipc.push_back(mg);
+      }
+      ctx->peer_a[static_cast<size_t>(p)] = static_cast<char*>(ma) + (b.raw_a - b.base_a);
+      ctx->peer_g[static_cast<size_t>(p)] = static_cast<char*>(mg) + (b.raw_g - b.base_g);
+    }
+    ctx->peer_ok = nranks > 1;
   });
 }
 
@@ -3397,6 +3730,7 @@ int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks) {
     if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank/nranks");
     ctx->rank = rank;
     ctx->nranks = nranks;
+    apply_nz_shard(ctx);
   });
 }
 
@@ -3421,6 +3755,7 @@ int gcpb_comm_init_host(gcpb_ctx* ctx, int rank, int nranks, gcpb_allgather_i64_
     ctx->host_user = user;
     ctx->rank = rank;
     ctx->nranks = nranks;
+    apply_nz_shard(ctx);
   });
 }
 

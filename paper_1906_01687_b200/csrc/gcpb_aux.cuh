@@ -31,7 +31,23 @@ struct DevState {
   uint64_t ref_ctr;      // RefStream counter (draws consumed so far)
   uint32_t ref_flag;     // RefStream: a draw hit the rejection region
   uint32_t ref_pad;
+  // multi-rank stratified zero sampler (global state): the
+  // z_* fields above then describe this rank's slice of the current batch
+  int64_t zg_q, zg_tested, zg_accepted, zg_rejected;
+  int64_t zg_kept;   // accepted candidates this rank keeps (its zero-list length)
+  int64_t zg_batch;  // global size of the current batch
+  int64_t pick_n;    // nonzero-sharded ranks: picks of the global stream in range
 };
+
+// Contiguous shard [begin, end) of n items for `rank` of `nranks` -- the
+// device twin of gcpb_shard_range (gcpb.cu).
+__host__ __device__ __forceinline__ void shard_range_dev(int64_t n, int rank, int nranks,
+                                                         int64_t* begin, int64_t* end) {
+  const int64_t base = n / nranks, rem = n % nranks;
+  const int64_t b = rank * base + (rank < rem ? rank : rem);
+  *begin = b;
+  *end = b + base + (rank < rem ? 1 : 0);
+}
 
 
 constexpr int kZcThreads = 256;
@@ -122,6 +138,149 @@ __global__ void zero_plan_slice_kernel(DevState* st, int64_t begin, int64_t size
   st->z_nchunks = nchunks;
 }
 
+// ---- multi-rank stratified zero sampler, device-planned ------
+// Every rank plans the same batch from the global shortfall (the reference's
+// formula, samplers.hpp:119-121), tests its contiguous slice of the batch's
+// candidate ordinals (zero_cand/zero_scatter into a local scratch list, all
+// of the slice's accepts kept), then the ranks' accept counts are
+// all-gathered (ncclAllGather inside a step graph, or the host communicator)
+// and each rank keeps the accepts whose global rank -- candidate order, which
+// is rank order since the slices are contiguous -- is below the remaining
+// need: exactly the single-rank "first q non-hits" (samplers.hpp:123-132).
+__global__ void zero_plan_mr_kernel(DevState* st, int first, int rank, int nranks) {
+  pdl_begin();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (first) {
+    st->zg_tested = 0;
+    st->zg_accepted = 0;
+    st->zg_rejected = 0;
+    st->zg_kept = 0;
+  }
+  st->z_ticket = 0;
+  st->z_batch_tag += 1;
+  st->z_tested = 0;
+  st->z_accepted = 0;
+  st->z_rejected = 0;
+  st->z_acc_before = 0;
+  const int64_t kept = st->zg_accepted < st->zg_q ? st->zg_accepted : st->zg_q;
+  const int64_t shortfall = st->zg_q - kept;
+  st->z_batch_begin = st->zg_tested;
+  if (shortfall <= 0) {
+    st->zg_batch = 0;
+    st->z_batch_size = 0;
+    st->z_nchunks = 0;
+    st->z_q = 0;
+    return;
+  }
+  const int64_t batch = zero_batch_size_dev(st->z_total, st->z_zeta, st->z_rho, shortfall);
+  int64_t lo = 0, hi = 0;
+  shard_range_dev(batch, rank, nranks, &lo, &hi);
+  int64_t nchunks = (hi - lo + kZcChunk - 1) / kZcChunk;
+  if (nchunks > st->z_status_cap) {  // cannot happen: batches shrink with the shortfall
+    st->z_overflow = 1;
+    nchunks = 0;
+  }
+  st->zg_batch = batch;
+  st->z_batch_begin = st->zg_tested + lo;
+  st->z_batch_size = hi - lo;
+  st->z_nchunks = nchunks;
+  st->z_q = hi - lo;  // the slice's accepts all go to the scratch list
+}
+
+__device__ __forceinline__ int64_t zero_keep_mr(const DevState* st, const int64_t* counts,
+                                                int rank) {
+  int64_t off = 0;
+  for (int r = 0; r < rank; ++r) off += counts[r];
+  const int64_t need = st->zg_q - (st->zg_accepted < st->zg_q ? st->zg_accepted : st->zg_q);
+  const int64_t room = need - off;
+  return room <= 0 ? 0 : (counts[rank] < room ? counts[rank] : room);
+}
+
+__global__ void zero_keep_mr_kernel(const DevState* st, const int64_t* counts, int rank,
+                                    const uint64_t* __restrict__ scratch,
+                                    uint64_t* __restrict__ list) {
+  pdl_begin();
+  const int64_t keep = zero_keep_mr(st, counts, rank);
+  const int64_t at = st->zg_kept;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < keep;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    list[at + i] = scratch[i];
+}
+
+__global__ void zero_commit_mr_kernel(DevState* st, const int64_t* counts, int rank, int nranks) {
+  pdl_begin();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t keep = zero_keep_mr(st, counts, rank);
+  int64_t total = 0;
+  for (int r = 0; r < nranks; ++r) total += counts[r];
+  st->zg_kept += keep;
+  st->zg_accepted += total;
+  st->zg_tested += st->zg_batch;
+  st->zg_rejected += st->zg_batch - total;
+}
+
+// Graph mode: counts steps whose device-planned batches fell short of q.
+__global__ void zero_check_mr_kernel(DevState* st) {
+  pdl_begin();
+  if (threadIdx.x == 0 && blockIdx.x == 0 && st->zg_accepted < st->zg_q) st->z_incomplete += 1;
+}
+
+// ---- nonzero-sharded picks --------------------------------------------------
+// A rank holding nonzero ordinals [nz_begin, nz_end) draws the whole global
+// pick stream (the same draws phase_a makes for SEG_PICK, so the sample
+// multiset is independent of the rank count) and keeps the picks in its
+// range, appended to `list` (warp-aggregated; the order only changes the
+// gradient's summation order).
+struct PickSpec {
+  uint64_t seed, iter;
+  const uint64_t* iter_base;
+  uint32_t tag, thr_eta;
+  int64_t p;
+  uint64_t eta;
+  int64_t nz_begin, nz_end;
+  int refstream;
+  uint64_t ref_key, thr64_eta;
+  const uint64_t* ref_ctr;
+  unsigned* ref_flag;
+};
+
+__global__ void __launch_bounds__(256) pick_compact_kernel(const PickSpec ps, uint64_t* list,
+                                                           int64_t* count) {
+  pdl_begin();
+  const uint64_t it = ps.iter + (ps.iter_base ? *ps.iter_base : 0ull);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) & ~int64_t{31};
+       base < ps.p; base += stride) {
+    const int64_t t = base + lane;
+    uint64_t e = 0;
+    bool keep = false;
+    if (t < ps.p) {
+      const uint64_t tt = static_cast<uint64_t>(t);
+      if (ps.refstream) {
+        e = refstream_below(ps.ref_key, *ps.ref_ctr + tt + 1, ps.eta, ps.thr64_eta, ps.ref_flag);
+      } else if (ps.eta <= (1ull << 32)) {
+        const U4 b = philox_block(ps.seed, ps.tag, 0u, 0u, it, tt);
+        const uint64_t prod = static_cast<uint64_t>(b.x) * ps.eta;
+        e = (static_cast<uint32_t>(prod) >= ps.thr_eta)
+                ? (prod >> 32)
+                : bounded32_from(ps.seed, ps.tag, it, tt, 0, ps.eta, ps.thr_eta, 1u);
+      } else {
+        e = bounded64(ps.seed, ps.tag, it, tt, 0, ps.eta);
+      }
+      keep = static_cast<int64_t>(e) >= ps.nz_begin && static_cast<int64_t>(e) < ps.nz_end;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (mask == 0u) continue;
+    unsigned long long at = 0;
+    if (lane == __ffs(mask) - 1)
+      at = atomicAdd(reinterpret_cast<unsigned long long*>(count),
+                     static_cast<unsigned long long>(__popc(mask)));
+    at = __shfl_sync(0xffffffffu, at, __ffs(mask) - 1);
+    if (keep) list[at + __popc(mask & ((1u << lane) - 1u))] = e;
+  }
+}
+
 // Column sums of every factor in fp64 (gradient_poisson_implicit's all-ones
 // part, kernels.cpp:213-216): one block per (mode, column).
 template <typename T>
@@ -203,11 +362,13 @@ __global__ void to_double_kernel(const T* __restrict__ in, double* out, int64_t 
 }
 
 // RefStream: advance the counter by the draws one sampler call consumed:
-// fixed + (per_tested ? tested * d : 0)  (stratified: p + tested * d).
+// fixed + (per_tested ? tested * d : 0)  (stratified: p + tested * d; 2 = the
+// multi-rank global tested count).
 __global__ void ref_advance_kernel(DevState* st, uint64_t fixed, int per_tested, int d) {
   pdl_begin();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  st->ref_ctr += fixed + (per_tested ? static_cast<uint64_t>(st->z_tested) * d : 0ull);
+  const int64_t tested = per_tested == 2 ? st->zg_tested : st->z_tested;
+  st->ref_ctr += fixed + (per_tested ? static_cast<uint64_t>(tested) * d : 0ull);
 }
 
 // Graph mode: counts steps whose device-planned batches did not yield q zeros.
@@ -854,6 +1015,128 @@ __global__ void __launch_bounds__(256, MINB)
   }
 }
 
+// ---- multi-GPU: reduce-scatter + sharded Adam + all-gather in one kernel ----
+// (the reference's per-worker partial reduction,
+// kernels.cpp:148-166, and adam_step, optimizer.cpp:47-66).  Every rank's
+// factor/gradient table is mapped into every rank (CUDA IPC over NVLink /
+// NVSwitch peer memory, gcpb_peer_open).  Rank `self` owns the global rows
+// [row0, row1) (all modes' rows are contiguous: global row i at element
+// i * rp of the contiguous layout, i * pitch of the table).  For each chunk
+// of its rows it loads the gradient chunk from every peer's table (P2P
+// loads), sums them in rank order, re-zeroes them there (P2P stores; only the
+// owner touches those addresses in this phase), applies the Adam update with
+// its local moments (ZeRO-1: only the owner's moment rows are used), and
+// writes the new factor chunk into every peer's table (P2P stores) -- so the
+// reduce-scatter, the optimizer and the all-gather are one pass, the
+// incoming (gradient) and outgoing (factor) NVLink traffic overlap, and no
+// contiguous staging copy of the interleaved table is needed.  The ranks
+// synchronise before (all scatters complete) and after (all factor writes
+// complete) through the communicator; no kernel waits on another.
+constexpr int kMaxPeers = 16;
+template <typename T>
+struct PeerTabs {
+  T* a[kMaxPeers];  // factor row base (row 0) of each rank's table
+  T* g[kMaxPeers];  // gradient row base of each rank's table
+  int npeers, self;
+  int pitch;        // elements between rows of the tables
+};
+
+template <typename T, bool FAST>
+__global__ void __launch_bounds__(256) peer_adam_kernel(const PeerTabs<T> pt, T* __restrict__ B,
+                                                        T* __restrict__ C, int64_t row0,
+                                                        int64_t row1, int rp, int cpr_shift,
+                                                        int r, DevState* st, int advance_rng) {
+  pdl_begin();
+  constexpr int VW = Vec<T>::W;
+  constexpr int U = 2;  // chunks per thread per pass: U * npeers P2P loads in flight
+  __shared__ double s_c1, s_c2;
+  if (threadIdx.x == 0) {
+    const double te = static_cast<double>(st->t + 1);
+    s_c1 = 1.0 - pow(st->beta1, te);
+    s_c2 = 1.0 - pow(st->beta2, te);
+  }
+  __syncthreads();
+  const T c1 = static_cast<T>(s_c1), c2 = static_cast<T>(s_c2);
+  const T lr = static_cast<T>(st->lr);
+  const T b1 = static_cast<T>(st->beta1), b2 = static_cast<T>(st->beta2);
+  const T ob1 = static_cast<T>(1.0 - st->beta1), ob2 = static_cast<T>(1.0 - st->beta2);
+  const T eps = static_cast<T>(st->eps);
+  const bool has_lb = st->has_lb != 0;
+  const T lb = static_cast<T>(st->lb);
+  const T step = static_cast<T>(st->lr / s_c1);
+  const T ic2 = static_cast<T>(1.0 / s_c2);
+  const int64_t nch = (row1 - row0) << cpr_shift;
+  const int64_t cmask = (int64_t{1} << cpr_shift) - 1;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t q0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q0 < nch;
+       q0 += U * stride) {
+    Vec<T> g[U];
+    int64_t toff[U], coff[U];
+    int col[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride < nch ? q0 + u * stride : nch - 1;
+      const int64_t row = row0 + (q >> cpr_shift);
+      col[u] = static_cast<int>(q & cmask) * VW;
+      toff[u] = row * pt.pitch + col[u];
+      coff[u] = row * rp + col[u];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) g[u].v[e] = static_cast<T>(0);
+    }
+    for (int p = 0; p < pt.npeers; ++p) {  // rank order: every replica sees the same sum
+      Vec<T> x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) load_chunk_cg(pt.g[p] + toff[u], x[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) g[u].v[e] += x[u].v[e];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (q0 + u * stride >= nch) break;
+      Vec<T> a, b, c;
+      load_chunk_cg(pt.a[pt.self] + toff[u], a);
+      load_chunk_cg(B + coff[u], b);
+      load_chunk_cg(C + coff[u], c);
+      Vec<T> ao = a, bo = b, co = c;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        if (col[u] + e < r) {
+          const T gv = g[u].v[e];
+          const T bv = b1 * b.v[e] + ob1 * gv;
+          const T cv = b2 * c.v[e] + ob2 * (gv * gv);
+          bo.v[e] = bv;
+          co.v[e] = cv;
+          T av;
+          if constexpr (FAST)
+            av = a.v[e] - step * bv * rsqrtf(cv * ic2 + eps);
+          else
+            av = a.v[e] - lr * (bv / c1) / sqrt((cv / c2) + eps);
+          if (has_lb) av = av > lb ? av : lb;
+          ao.v[e] = av;
+        }
+      }
+      store_chunk(B + coff[u], bo);
+      store_chunk(C + coff[u], co);
+      for (int p = 0; p < pt.npeers; ++p) {
+        store_chunk(pt.g[p] + toff[u], Vec<T>{});
+        store_chunk(pt.a[p] + toff[u], ao);
+      }
+    }
+  }
+  __threadfence_system();  // peer stores visible before the ranks' barrier
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&st->adam_done, 1u);
+    if (prev == gridDim.x - 1) {
+      st->t += 1;
+      if (advance_rng) st->rng_iter += 1;
+      st->adam_done = 0;
+    }
+  }
+}
+
 // AG <- [A row | 0]: (re)builds the interleaved factor/gradient table from
 // the contiguous factors (after any factor write other than the IL Adam).
 template <typename T>
@@ -949,13 +1232,15 @@ __global__ void row_hist_kernel(const uint32_t* __restrict__ rec, int rec_words,
 template <typename T>
 __global__ void __launch_bounds__(256) hot_fold_kernel(T* __restrict__ Ghot, int rh, int rp,
                                                        const int64_t* __restrict__ hot_off,
-                                                       T* __restrict__ G) {
+                                                       T* __restrict__ G, int il = 0) {
   pdl_begin();
   constexpr int VW = Vec<T>::W;
   const Vec<T> acc =
       hot_rows_sum<T>(Ghot, static_cast<int>(blockIdx.x), rh, rp, nullptr, 0, 0, 0);
   if (static_cast<int>(threadIdx.x) < rp / VW) {
-    T* g = G + hot_off[blockIdx.x] + threadIdx.x * VW;
+    // G: the contiguous gradient, or (il) the interleaved table's gradient rows
+    const int64_t ro = il ? 2 * hot_off[blockIdx.x] + rp : hot_off[blockIdx.x];
+    T* g = G + ro + threadIdx.x * VW;
 #pragma unroll
     for (int e = 0; e < VW; ++e) g[e] += acc.v[e];
   }

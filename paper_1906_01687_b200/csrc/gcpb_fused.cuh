@@ -96,6 +96,10 @@ __device__ __forceinline__ SegRegs seg_of(const FusedArgs<T>& a, int64_t tile) {
   r.tiles_begin = g.tiles_begin;
   r.out_offset = g.out_offset;
   r.ref_off = g.ref_off;
+  if (g.len_dev) {
+    const int64_t n = *g.len_dev;
+    if (n < r.t_end - r.t_begin) r.t_end = r.t_begin + (n > 0 ? n : 0);
+  }
   return r;
 }
 
@@ -174,7 +178,9 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
     }
   } else if (kind == SEG_PICK) {
     uint64_t e;
-    if (a.refstream) {
+    if (a.pick_list) {  // drawn beforehand (pick_compact_kernel)
+      e = a.pick_list[t];
+    } else if (a.refstream) {
       e = refstream_below(a.ref_key, *a.ref_ctr + static_cast<uint64_t>(sg.ref_off + t) + 1, a.eta,
                           a.thr64_eta, a.ref_flag);
     } else if (a.eta <= (1ull << 32)) {
@@ -356,10 +362,7 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
         for (int c = 0; c < VPL; ++c) {
           Vec<T> q;
-          if (a.l2line)
-            load_chunk_l2line(a.A + roff[k] + cidx[c] * VW, q);
-          else
-            load_chunk(a.A + roff[k] + cidx[c] * VW, q);
+          load_chunk(a.A + roff[k] + cidx[c] * VW, q);
 #pragma unroll
           for (int e = 0; e < VW; ++e) row[k][c * VW + e] = q.v[e];
         }
@@ -444,107 +447,10 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
-// Phase B of the slim hot-path kernels (no host-given samples, no records)
-// with PB passes per batch: the row gathers of PB passes are issued before
-// any of their arithmetic and reductions, so a warp keeps PB x DM row loads
-// in flight instead of DM (the tables beyond L2, C5, are bound by random-
-// access latency).
-template <typename T, int DM, int G, int PB, bool HOT>
-__device__ __forceinline__ void phase_b_batched(const FusedArgs<T>& a, const SegRegs& sg,
-                                                const uint32_t (&ik)[DM], const Drawn<T>& s,
-                                                T* __restrict__ Gb, uint32_t rsel) {
-  constexpr int VW = Vec<T>::W;
-  constexpr int NGRP = 32 / G;
-  constexpr int NPASS = (32 + NGRP - 1) / NGRP;
-  constexpr bool POW2 = (G & (G - 1)) == 0;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int grp = lane / G;
-  const int gl = lane % G;
-  const T wseg = static_cast<T>(sg.weight);
-  const int fv = sg.flag;
-  const int cidx = gl < a.nchunks ? gl : a.nchunks - 1;
-  const T cmask = gl < a.nchunks ? static_cast<T>(1) : static_cast<T>(0);
-  const bool owns = gl < a.nchunks;
-#pragma unroll 1
-  for (int p0 = 0; p0 < NPASS; p0 += PB) {
-    bool v[PB];
-    T xv[PB];
-    uint32_t hsv[PB];
-    uint32_t roff[PB][DM];
-    T row[PB][DM][VW];
-#pragma unroll
-    for (int j = 0; j < PB; ++j) {
-      const int pass = p0 + j;
-      const int src = (pass * NGRP + grp) & 31;
-      v[j] = __shfl_sync(FULL, s.valid, src) && pass < NPASS &&
-             (POW2 || (grp < NGRP && pass * NGRP + grp < 32));
-      xv[j] = __shfl_sync(FULL, s.x, src);
-      hsv[j] = HOT ? __shfl_sync(FULL, s.hs, src) : 0xFFFFFFFFu;
-#pragma unroll
-      for (int k = 0; k < DM; ++k) {
-        roff[j][k] = static_cast<uint32_t>(a.off[k]) +
-                     __shfl_sync(FULL, ik[k], src) * static_cast<uint32_t>(a.pitch);
-        Vec<T> q;
-        if (a.l2line)
-          load_chunk_l2line(a.A + roff[j][k] + cidx * VW, q);
-        else
-          load_chunk(a.A + roff[j][k] + cidx * VW, q);
-#pragma unroll
-        for (int e = 0; e < VW; ++e) row[j][k][e] = q.v[e];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < PB; ++j) {
-      T pre[DM][VW];
-      T mp = static_cast<T>(0);
-#pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        T p = row[j][0][e];
-        pre[0][e] = static_cast<T>(1);
-#pragma unroll
-        for (int k = 1; k < DM; ++k) {
-          pre[k][e] = p;
-          p = p * row[j][k][e];
-        }
-        mp += p;
-      }
-      mp *= cmask;
-      if constexpr (POW2) {
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
-      } else {
-        T tot = static_cast<T>(0);
-#pragma unroll
-        for (int jj = 0; jj < G; ++jj) tot += __shfl_sync(FULL, mp, (grp * G + jj) & 31);
-        mp = tot;
-      }
-      T g = loss_deriv_fast(a.loss, a.delta, xv[j], mp);
-      if (fv) g = g - loss_deriv_fast(a.loss, a.delta, static_cast<T>(0), mp);
-      const T y = wseg * g;
-      const bool act = v[j] && owns;
-      T suf[VW];
-#pragma unroll
-      for (int e = 0; e < VW; ++e) suf[e] = static_cast<T>(1);
-#pragma unroll
-      for (int k = DM - 1; k >= 0; --k) {
-        T out[VW];
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-          out[e] = y * (pre[k][e] * suf[e]);
-          suf[e] = suf[e] * row[j][k][e];
-        }
-        if (act) red_chunk(grad_row<T, HOT>(a, Gb, roff[j][k], hsv[j], k, rsel) + cidx * VW, out);
-      }
-    }
-  }
-}
-
 template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true,
-          bool HOT = false, int PB = 1>
+          bool HOT = false>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
                                                                int64_t total_tiles) {
-  static_assert(PB == 1 || (EXACT && VPL == 1 && !REC && !GV), "batched passes: slim path only");
   pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -576,9 +482,7 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
-    if constexpr (PB > 1)
-      phase_b_batched<T, DM, G, PB, HOT>(a, sg, ik, s, Gb, rsel);
-    else
+    if (__any_sync(0xffffffffu, s.valid))  // tiles past a device-resident length
       phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT>(a, sg, tile, ik, s, Gb, rsel);
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
@@ -640,17 +544,6 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
             return nchunks == 5
                        ? go(fused_grad_kernel<T, DM, EXACT, 5, 1, REC, GCPB_MINB_SLIM, false>)
                        : go(fused_grad_kernel<T, DM, EXACT, 6, 1, REC, GCPB_MINB_SLIM, false>);
-          }
-        }
-        if constexpr (sizeof(T) == 4 && DM <= 4) {
-          if (G == 4 && a.pb > 1) {  // batched passes (more row loads in flight)
-            if (a.rh > 0) {
-              *used_hot = true;
-              return a.pb >= 4 ? go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 2, false, true, 4>)
-                               : go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 3, false, true, 2>);
-            }
-            return a.pb >= 4 ? go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 2, false, false, 4>)
-                             : go(fused_grad_kernel<T, DM, EXACT, 4, 1, REC, 3, false, false, 2>);
           }
         }
         if constexpr (DM <= 4) {

@@ -90,6 +90,9 @@ struct Seg {
   int64_t out_offset;   // record position of ordinal t_begin
   double weight;
   int64_t ref_off;      // RefStream: draw index of this segment's first draw
+  // Device-resident length (multi-rank lists whose length is known only on
+  // the device): the segment ends at t_begin + min(t_end - t_begin, *len_dev).
+  const int64_t* len_dev;
 };
 
 template <typename T>
@@ -128,6 +131,10 @@ struct FusedArgs {
   int nseg;
   Seg seg[3];
   const uint64_t* zero_list;
+  // optional: SEG_PICK reads its (global) nonzero ordinals from here instead
+  // of drawing them (nonzero-sharded ranks: the picks of the global stream
+  // that fall in this rank's range, compacted by pick_compact_kernel)
+  const uint64_t* pick_list;
   // given samples
   const int64_t* g_idx;
   const double* g_x;
@@ -142,8 +149,6 @@ struct FusedArgs {
   double* r_m;
   double* r_y;
   int scatter;
-  int pb;  // host-side: passes per batch of the slim kernels (1 = unbatched)
-  int l2line;  // row loads fetch whole 128-byte L2 lines (interleaved table)
   // RefStream mode: draws reproduce the reference's RngStream
   // (rng.cpp:43-61): u = mix64(key + phi * (counter + j + 1)), value u % n,
   // with j the draw's position in the reference's consumption order.
@@ -275,7 +280,7 @@ __device__ __forceinline__ void load_chunk(const double* p, Vec<double>& out) {
 }
 
 // Streaming (touch-once) chunk loads and stores: no L1 allocation on loads,
-// evict-first stores.  `stream_mode` picks the flavour under test.
+// plain stores.
 __device__ __forceinline__ void load_chunk_stream(const float* p, Vec<float>& out) {
   asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(out.v[0]), "=f"(out.v[1]), "=f"(out.v[2]), "=f"(out.v[3])
@@ -293,20 +298,6 @@ __device__ __forceinline__ void store_chunk_stream(float* p, const Vec<float>& v
 }
 __device__ __forceinline__ void store_chunk_stream(double* p, const Vec<double>& v) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.v[0]), "d"(v.v[1]) : "memory");
-}
-
-// Row-chunk loads that ask L2 to fetch the whole 128-byte line on a miss
-// (interleaved [A row | G row] table: the gradient half the reduction needs
-// arrives in the same DRAM access as the factor half).
-__device__ __forceinline__ void load_chunk_l2line(const float* p, Vec<float>& out) {
-  asm("ld.global.nc.L2::128B.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(out.v[0]), "=f"(out.v[1]), "=f"(out.v[2]), "=f"(out.v[3])
-               : "l"(p));
-}
-__device__ __forceinline__ void load_chunk_l2line(const double* p, Vec<double>& out) {
-  asm("ld.global.nc.L2::128B.v2.f64 {%0, %1}, [%2];"
-               : "=d"(out.v[0]), "=d"(out.v[1])
-               : "l"(p));
 }
 
 __device__ __forceinline__ void store_chunk(float* p, const Vec<float>& v) {

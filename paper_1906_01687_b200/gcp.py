@@ -643,6 +643,18 @@ class Engine:
     def set_shard(self, rank: int, nranks: int) -> None:
         self._ck(lib.gcpb_set_shard(self._h, rank, nranks))
 
+    def peer_handle(self) -> bytes:
+        """This rank's table, exportable to the other ranks (gcpb_peer_handle)."""
+        buf = C.create_string_buffer(_capi.PEER_HANDLE_BYTES)
+        self._ck(lib.gcpb_peer_handle(self._h, buf))
+        return buf.raw
+
+    def peer_open(self, handles: Sequence[bytes]) -> None:
+        """Map every rank's table (rank order) for the fused reduce-scatter +
+        Adam + all-gather kernel (gcpb_peer_open)."""
+        blob = b"".join(bytes(h) for h in handles)
+        self._ck(lib.gcpb_peer_open(self._h, blob, len(handles)))
+
     def comm_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
         self._ck(lib.gcpb_comm_init(self._h, unique_id, rank, nranks))
 

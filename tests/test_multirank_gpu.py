@@ -129,3 +129,95 @@ def test_multirank_steps_match_single_rank():
     for got in _run_ranks(2, rank_fn):
         for x, y in zip(got, want):
             assert O.rel_error(x, y) <= 1e-12
+
+
+def _skewed_problem(seed, dims=(60, 40, 30), nnz=1500, r=8):
+    rs = np.random.default_rng(seed)
+    cols = [np.minimum((rs.pareto(1.2, nnz * 2) * 2).astype(np.int64), n - 1) for n in dims]
+    lin = np.unique(sum(c * int(np.prod(dims[:k])) for k, c in enumerate(cols)))[:nnz]
+    coords = np.stack(np.unravel_index(lin, dims, order="F"), 1)
+    vals = 1.0 + rs.poisson(2.0, len(lin))
+    F = [rs.uniform(0.1, 1.0, (n, r)) for n in dims]
+    return dims, r, coords, vals, F
+
+
+@pytest.mark.parametrize("il", ["0", "1"])
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_peer_adam_steps_match_single_rank(monkeypatch, il, nranks, strategy, dtype):
+    """The peer-memory step: nonzero-sharded ranks (records of a contiguous
+    range, the global pick stream compacted per rank), the device-planned
+    multi-rank zero sampler, and the fused reduce-scatter + sharded Adam +
+    all-gather kernel on peer-mapped tables (one GPU: the ranks' tables are
+    peers in one process, rank barriers through the host communicator), on
+    the interleaved and the plain layout.  Factor replicas must equal a
+    single-rank run, with identical RejectionStats for stratified draws."""
+    import paper_1906_01687_b200.gcp as G
+    monkeypatch.setenv("GCPB_IL", il)
+    monkeypatch.setenv("GCPB_HOT_T", "4")  # hot rows on: folded into the table before the exchange
+    dims, r, coords, vals, F = _skewed_problem(40 + strategy)
+    if dtype == "f32":
+        F = [np.asarray(f, np.float32).astype(np.float64) for f in F]
+    sk = {0: G.SamplerKind.uniform(4000), 1: G.SamplerKind.stratified(1500, 2500, 1.05),
+          2: G.SamplerKind.semi_stratified(1500, 2500)}[strategy]
+    lf = G.LossFunction.poisson()
+    single = G.Engine(dims, r, dtype)
+    single.set_sparse(coords, vals)
+    single.set_factors(F)
+    for it in range(3):
+        single.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+    want = single.factors()
+    hub = Hub(nranks)
+    engines = [None] * nranks
+
+    def make(rank):
+        e = G.Engine(dims, r, dtype)
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.comm_init_host(rank, nranks, lambda v: hub.allgather(rank, v),
+                         lambda a: hub.allreduce(rank, a))
+        engines[rank] = e
+        return e.peer_handle()
+
+    handles = _run_ranks(nranks, make)
+
+    def run(rank):
+        e = engines[rank]
+        e.peer_open(handles)
+        for it in range(3):
+            e.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+        return e.factors()
+
+    tol = 1e-12 if dtype == "f64" else 2e-5
+    for got in _run_ranks(nranks, run):
+        for x, y in zip(got, want):
+            assert O.rel_error(x, y) <= tol
+
+
+def test_multirank_run_steps_with_host_communicator():
+    """run_steps on ranks with the host communicator (not capturable in a
+    graph): the iterations run eagerly and equal single-rank stepping."""
+    import paper_1906_01687_b200.gcp as G
+    dims, r, coords, vals, F = _problem(31)
+    sk, lf = G.SamplerKind.stratified(800, 1200, 1.1), G.LossFunction.bernoulli_odds()
+    single = G.Engine(dims, r, "f64")
+    single.set_sparse(coords, vals)
+    single.set_factors(F)
+    for it in range(5):
+        single.step(sk, lf, 3, it, 1e-2, lower_bound=0.0)
+    want = single.factors()
+    hub = Hub(2)
+
+    def rank_fn(rank):
+        e = G.Engine(dims, r, "f64")
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.comm_init_host(rank, 2, lambda v: hub.allgather(rank, v),
+                         lambda a: hub.allreduce(rank, a))
+        e.run_steps(sk, lf, 3, 0, 5, 1e-2, lower_bound=0.0)
+        return e.factors()
+
+    for got in _run_ranks(2, rank_fn):
+        for x, y in zip(got, want):
+            assert O.rel_error(x, y) <= 1e-12
