@@ -361,6 +361,7 @@ class Reference:
                                        C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_double,
                                        C.c_int, C.c_double, C.c_int64, C.c_int, C.c_int64,
                                        C.c_uint64, C.c_int, C.c_int64, f64p, i64p, f64p, f64p]
+        L.ref_tensor_value_at.argtypes = [vp, i64p, C.POINTER(C.c_double)]
         L.ref_bench_model_new.argtypes = [C.c_int, i64p, C.c_int64, f64p, C.POINTER(vp)]
         L.ref_bench_model_free.argtypes = [vp]
         L.ref_bench_step_given.argtypes = [vp, C.c_int, C.c_double, C.c_int64, i64p, f64p,
@@ -589,6 +590,13 @@ class RefTensor:
 
     def norm(self):
         return float(self.ref.lib.ref_tensor_norm(self.h))
+
+    def value_at(self, idx):
+        """TensorView::value_at (tensor.hpp:95-97): lookup / dense read."""
+        ix = np.ascontiguousarray(idx, dtype=np.int64).reshape(-1)
+        out = C.c_double()
+        self.ref._ck(self.ref.lib.ref_tensor_value_at(self.h, _i64(ix), C.byref(out)))
+        return out.value
 
     def write_tns(self, path):
         self.ref._ck(self.ref.lib.ref_write_tns(self.h, str(path).encode()))

@@ -216,6 +216,9 @@ struct gcpb_ctx {
   int vw = 4;  // elements per 16-byte chunk
   unsigned __int128 total128 = 0;
   bool total_fits = true;  // N < 2^64
+  bool wide = false;        // N >= 2^64: 128-bit keys (sparse tensors only)
+  bool off64 = false;       // > 2^31 padded factor elements: 64-bit row offsets
+  uint64_t stride_lo[kMaxModes] = {}, stride_hi[kMaxModes] = {};  // 128-bit strides
   uint64_t total = 0;
   double total_d = 0.0;
   int64_t off[kMaxModes + 1] = {};
@@ -260,6 +263,7 @@ struct gcpb_ctx {
   DBuf dense;
   int64_t nnz = 0;
   DBuf nzrec, vals, keys;  // AoS nonzero records, values, sorted linear keys
+  DBuf keys_hi, hkeys_hi;  // wide: high words of the keys and of the hash slots
   // Nonzero sharding: with nranks > 1 the records hold only
   // this rank's contiguous range [nz_begin, nz_end) of the sorted order; keys
   // and values stay whole (membership hash, value lookups).
@@ -563,11 +567,66 @@ void ensure_grad_zero(gcpb_ctx* c) {
 }
 
 // Hash of the nonzero linear keys, built on first use.
+// Membership hash + Bloom prefilter of 128-bit keys (N >= 2^64), built on the
+// host from the sorted keys (same bucket layout as the 64-bit hash, high
+// words in a parallel table; hash_find_wide / wide_digest).
+void build_hash_wide(gcpb_ctx* c) {
+  const int64_t n = c->nnz;
+  std::vector<uint64_t> lo(static_cast<size_t>(n)), hi(static_cast<size_t>(n));
+  if (n > 0) {
+    CK(cudaMemcpyAsync(lo.data(), c->keys.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(hi.data(), c->keys_hi.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  }
+  uint64_t buckets = 1;
+  while (buckets * 2 < static_cast<uint64_t>(n)) buckets <<= 1;
+  c->hmask = buckets - 1;
+  std::vector<uint64_t> tlo(buckets * 4, kEmptyKey), thi(buckets * 4, kEmptyKey);
+  std::vector<uint32_t> tv(buckets * 4, 0u);
+  uint64_t blocks = 1;
+  while (blocks * 32 < static_cast<uint64_t>(n)) blocks <<= 1;
+  c->bmask = blocks - 1;
+  std::vector<uint32_t> bl(static_cast<size_t>(blocks) * 8, 0u);
+  for (int64_t e = 0; e < n; ++e) {
+    const uint64_t dg = wide_digest(lo[e], hi[e]);
+    for (uint64_t b = mix64(dg) & c->hmask;; b = (b + 1) & c->hmask) {
+      int s = 0;
+      while (s < 4 && !(tlo[b * 4 + s] == kEmptyKey && thi[b * 4 + s] == kEmptyKey)) ++s;
+      if (s < 4) {
+        tlo[b * 4 + s] = lo[e];
+        thi[b * 4 + s] = hi[e];
+        tv[b * 4 + s] = static_cast<uint32_t>(e);
+        break;
+      }
+    }
+    const uint64_t h = bloom_hash(dg);  // bloom_build_kernel's bits
+    uint32_t* blk = bl.data() + (h & c->bmask) * 8;
+    for (int b = 0; b < 3; ++b) {
+      const uint32_t pos = static_cast<uint32_t>(h >> (40 + 8 * b)) & 255u;
+      blk[pos >> 5] |= 1u << (pos & 31u);
+    }
+  }
+  c->hkeys.alloc(tlo.size() * 8);
+  c->hkeys_hi.alloc(thi.size() * 8);
+  c->hvals.alloc(tv.size() * 4);
+  c->bloom.alloc(bl.size() * 4);
+  CK(cudaMemcpyAsync(c->hkeys.p, tlo.data(), tlo.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->hkeys_hi.p, thi.data(), thi.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->hvals.p, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->bloom.p, bl.data(), bl.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  c->sync();  // host vectors die here
+  c->hash_ready = true;
+}
+
 void ensure_hash(gcpb_ctx* c) {
   if (c->tensor_kind != 2) throw std::logic_error("hash requested without a sparse tensor");
   if (c->hash_ready) return;
   if (c->nnz >= (int64_t{1} << 32))
     throw std::invalid_argument("membership hash supports nnz < 2^32");
+  if (c->wide) {
+    build_hash_wide(c);
+    return;
+  }
   uint64_t buckets = 1;
   while (buckets * 2 < static_cast<uint64_t>(c->nnz)) buckets <<= 1;  // load <= 0.5
   if (buckets < 1) buckets = 1;
@@ -678,7 +737,7 @@ void apply_nz_shard_t(gcpb_ctx* c) {
     T* v = c->vals.as<T>() + b;
     keys_to_records_kernel<T, T><<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(
         c->keys.as<uint64_t>() + b, v, n, c->d, c->dims_dev.as<int64_t>(), c->nzrec.as<uint32_t>(),
-        c->rec_words, v);
+        c->rec_words, v, c->wide ? c->keys_hi.as<uint64_t>() + b : nullptr);
     CK(cudaGetLastError());
   }
   c->sync();
@@ -712,6 +771,13 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     a.thr[k] = lemire_threshold32(static_cast<uint64_t>(c->dims[k]));
     a.stride[k] = stride;
     stride *= static_cast<uint64_t>(c->dims[k]);
+  }
+  if (c->wide) {
+    a.wide = 1;
+    for (int k = 0; k < c->d; ++k) {
+      a.stride[k] = c->stride_lo[k];
+      a.stride_hi[k] = c->stride_hi[k];
+    }
   }
   a.seed = seed;
   a.iter = iter;
@@ -747,11 +813,17 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
     a.nz_end = c->nz_end;
     if (c->hash_ready) {
       a.hkeys = c->hkeys.as<uint64_t>();
+      a.hkeys_hi = c->hkeys_hi.as<uint64_t>();
       a.hvals = c->hvals.as<uint32_t>();
       a.hmask = c->hmask;
     }
   }
   a.scatter = 1;
+  a.off64 = c->off64 ? 1 : 0;
+  if (c->off64 && !((c->d == 3 || c->d == 4) && a.nchunks <= 32))
+    throw std::invalid_argument("factor tables beyond 2^31 padded elements: the device path "
+                                "supports d = 3, 4 and rows of at most 32 chunks (r <= 128 fp32, "
+                                "r <= 64 fp64)");
   return a;
 }
 
@@ -1058,6 +1130,10 @@ void fill_refstream(const gcpb_ctx* c, ZeroArgs& za, uint64_t key, int64_t p_ref
 }
 
 void launch_zero_cand(const gcpb_ctx* c, int grid, const ZeroArgs& za) {
+  if (c->wide) {  // 128-bit keys: the general-d instantiation
+    CK(launch_k(zero_cand_kernel<0>, dim3(grid), dim3(kZcThreads), 0, c->stream, za));
+    return;
+  }
   switch (c->d) {
     case 3: CK(launch_k(zero_cand_kernel<3>, dim3(grid), dim3(kZcThreads), 0, c->stream, za)); break;
     case 4: CK(launch_k(zero_cand_kernel<4>, dim3(grid), dim3(kZcThreads), 0, c->stream, za)); break;
@@ -1077,6 +1153,14 @@ ZeroArgs zero_args(gcpb_ctx* c, uint64_t seed, uint64_t iter, const uint64_t* it
     za.thr[k] = lemire_threshold32(static_cast<uint64_t>(c->dims[k]));
     za.stride[k] = stride;
     stride *= static_cast<uint64_t>(c->dims[k]);
+  }
+  if (c->wide) {
+    za.wide = 1;
+    for (int k = 0; k < c->d; ++k) {
+      za.stride[k] = c->stride_lo[k];
+      za.stride_hi[k] = c->stride_hi[k];
+    }
+    za.hkeys_hi = c->hkeys_hi.as<uint64_t>();
   }
   za.seed = seed;
   za.iter = iter;
@@ -1521,6 +1605,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     if (c->tensor_kind == 2) {
       ensure_hash(c);
       a.hkeys = c->hkeys.as<uint64_t>();
+      a.hkeys_hi = c->hkeys_hi.as<uint64_t>();
       a.hvals = c->hvals.as<uint32_t>();
       a.hmask = c->hmask;
     }
@@ -2026,7 +2111,7 @@ constexpr size_t kSmallModelMax = 200 * 1024;  // A, B, C replicas in shared mem
 
 template <typename T>
 bool small_eligible(const gcpb_ctx* c, const gcpb_sampler* sk) {
-  if (c->tune.no_small || c->nranks != 1 || c->draw_stream != 0 || c->timing) return false;
+  if (c->tune.no_small || c->wide || c->nranks != 1 || c->draw_stream != 0 || c->timing) return false;
   // red.global issue costs ~1.3 cycles per lane on the issuing SM: keep the
   // per-iteration scatter of the 8 cluster SMs well under a microsecond
   if (sk->strategy != GCPB_UNIFORM || sk->num_samples * c->d * c->r > 16384) return false;
@@ -2422,6 +2507,72 @@ void bias_variance_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* lo
 // zero sums dropped, then the usual records.  Same result as a host stable
 // sort; the reference's std::sort can order duplicates differently, which
 // only matters in the last bit of sums of three or more duplicates.
+// SparseTensor normalisation with 128-bit keys (N >= 2^64; tensor.cpp:10-53
+// with Index128 keys, shape.cpp:87-96): keys, sort, sum duplicates, drop
+// zeros on the host; keys (low / high words), values and records to the
+// device.
+void normalize_wide(gcpb_ctx* c, int64_t nnz, const int64_t* coords, const double* values) {
+  const int d = c->d;
+  std::vector<unsigned __int128> key(static_cast<size_t>(nnz));
+  for (int64_t e = 0; e < nnz; ++e) {
+    check_index_host(c, coords + e * d);  // tensor.cpp:21 (out_of_range)
+    unsigned __int128 l = 0;
+    for (int k = 0; k < d; ++k)
+      l += static_cast<unsigned __int128>(coords[e * d + k]) *
+           ((static_cast<unsigned __int128>(c->stride_hi[k]) << 64) | c->stride_lo[k]);
+    key[static_cast<size_t>(e)] = l;
+  }
+  std::vector<int64_t> ord(static_cast<size_t>(nnz));
+  std::iota(ord.begin(), ord.end(), int64_t{0});
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  std::vector<uint64_t> lo, hi;
+  std::vector<double> v;
+  for (size_t i = 0; i < ord.size();) {
+    const unsigned __int128 k = key[static_cast<size_t>(ord[i])];
+    double sum = 0.0;
+    for (; i < ord.size() && key[static_cast<size_t>(ord[i])] == k; ++i) sum += values[ord[i]];
+    if (sum != 0.0) {  // exact zeros dropped (tensor.cpp:35)
+      lo.push_back(static_cast<uint64_t>(k));
+      hi.push_back(static_cast<uint64_t>(k >> 64));
+      v.push_back(sum);
+    }
+  }
+  const int64_t n = static_cast<int64_t>(lo.size());
+  c->nnz = n;
+  c->tensor_kind = 2;
+  c->tensor_version += 1;
+  c->hash_ready = false;
+  c->domain_flags = -1;
+  c->dense.reset();
+  c->rec_words = record_words(d, c->tsize);
+  const size_t nn = static_cast<size_t>(std::max<int64_t>(n, 1));
+  c->keys.alloc(nn * 8);
+  c->keys_hi.alloc(nn * 8);
+  c->nzrec.alloc(nn * c->rec_words * sizeof(uint32_t));
+  c->vals.alloc(nn * c->tsize);
+  if (n > 0) {
+    DBuf dv;
+    dv.alloc(n * 8);
+    CK(cudaMemcpyAsync(c->keys.p, lo.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->keys_hi.p, hi.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dv.p, v.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    const int g = grid_for(n, 256, c->num_sms);
+    if (c->dtype == GCPB_F32)
+      keys_to_records_kernel<double, float><<<g, 256, 0, c->stream>>>(
+          c->keys.as<uint64_t>(), dv.as<double>(), n, d, c->dims_dev.as<int64_t>(),
+          c->nzrec.as<uint32_t>(), c->rec_words, c->vals.as<float>(), c->keys_hi.as<uint64_t>());
+    else
+      keys_to_records_kernel<double, double><<<g, 256, 0, c->stream>>>(
+          c->keys.as<uint64_t>(), dv.as<double>(), n, d, c->dims_dev.as<int64_t>(),
+          c->nzrec.as<uint32_t>(), c->rec_words, c->vals.as<double>(), c->keys_hi.as<uint64_t>());
+    CK(cudaGetLastError());
+    c->sync();
+  }
+  c->nz_begin = 0;
+  c->nz_end = n;
+  apply_nz_shard(c);
+}
+
 void normalize_on_device(gcpb_ctx* c, int64_t nnz, const int64_t* coords, const double* values) {
   const int d = c->d;
   if (nnz == 0) {
@@ -2563,6 +2714,17 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
     }
     c->total128 = total;
     c->total_fits = total <= static_cast<unsigned __int128>(UINT64_MAX);
+    c->wide = !c->total_fits;
+    if (total >> 127)  // keys stay below 2^127 (the wide hash's empty marker)
+      throw std::invalid_argument("device path supports N < 2^127 entries");
+    {
+      unsigned __int128 st = 1;
+      for (int k = 0; k < ndims; ++k) {
+        c->stride_lo[k] = static_cast<uint64_t>(st);
+        c->stride_hi[k] = static_cast<uint64_t>(st >> 64);
+        st *= static_cast<unsigned __int128>(dims[k]);
+      }
+    }
     c->total = c->total_fits ? static_cast<uint64_t>(total) : 0;
     c->total_d = static_cast<double>(total);
     int64_t o = 0;
@@ -2572,8 +2734,10 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
     }
     c->off[ndims] = o;
     c->nelem = o;
-    if (o >= (int64_t{1} << 31))
-      throw std::invalid_argument("factor matrices exceed 2^31 padded elements (device path)");
+    // beyond 2^31 padded elements (2^32 in the interleaved table) the fused
+    // kernel needs 64-bit row offsets: its OFF64 instantiations (d = 3, 4;
+    // rows of at most 32 chunks)
+    c->off64 = o >= (int64_t{1} << 31);
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
@@ -2637,8 +2801,10 @@ int gcpb_set_sparse(gcpb_ctx* ctx, int64_t nnz, const int64_t* coords, const dou
   return guard(ctx, [&] {
     if (nnz < 0) throw std::invalid_argument("sparse tensor: negative nnz");
     if (nnz > 0 && (!coords || !values)) throw std::invalid_argument("sparse tensor: null buffers");
-    if (!ctx->total_fits) throw std::invalid_argument("sparse tensor: N >= 2^64 unsupported (u64 keys)");
-    normalize_on_device(ctx, nnz, coords, values);
+    if (ctx->wide)
+      normalize_wide(ctx, nnz, coords, values);
+    else
+      normalize_on_device(ctx, nnz, coords, values);
   });
 }
 
@@ -2646,7 +2812,8 @@ int gcpb_set_sparse_device(gcpb_ctx* ctx, int64_t nnz, const uint64_t* d_keys_so
                            const void* d_values, int value_dtype) {
   return guard(ctx, [&] {
     if (nnz < 0) throw std::invalid_argument("sparse tensor: negative nnz");
-    if (!ctx->total_fits) throw std::invalid_argument("sparse tensor: N >= 2^64 unsupported (u64 keys)");
+    if (!ctx->total_fits)
+      throw std::invalid_argument("device ingest takes u64 keys: N >= 2^64 needs gcpb_set_sparse");
     if (value_dtype != GCPB_F32 && value_dtype != GCPB_F64)
       throw std::invalid_argument("value dtype must be F32 or F64");
     // the caller's buffers may still be written by work on other streams
@@ -2720,9 +2887,12 @@ int gcpb_get_sparse(gcpb_ctx* ctx, int64_t* coords_out, double* values_out) {
   return guard(ctx, [&] {
     if (ctx->tensor_kind != 2) throw std::invalid_argument("no sparse tensor set");
     const int64_t n = ctx->nnz;
-    std::vector<uint64_t> keys(static_cast<size_t>(n));
+    std::vector<uint64_t> keys(static_cast<size_t>(n)), keys_hi(static_cast<size_t>(n), 0);
     if (n > 0)
       CK(cudaMemcpyAsync(keys.data(), ctx->keys.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (n > 0 && ctx->wide)
+      CK(cudaMemcpyAsync(keys_hi.data(), ctx->keys_hi.p, n * 8, cudaMemcpyDeviceToHost,
+                         ctx->stream));
     std::vector<double> v(static_cast<size_t>(n));
     if (ctx->dtype == GCPB_F32) {
       std::vector<float> f(static_cast<size_t>(n));
@@ -2735,11 +2905,13 @@ int gcpb_get_sparse(gcpb_ctx* ctx, int64_t* coords_out, double* values_out) {
         CK(cudaMemcpyAsync(v.data(), ctx->vals.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
     }
+    ctx->sync();
     for (int64_t e = 0; e < n; ++e) {
-      uint64_t rem = keys[e];
+      unsigned __int128 rem = (static_cast<unsigned __int128>(keys_hi[e]) << 64) | keys[e];
       for (int k = 0; k < ctx->d; ++k) {
-        coords_out[e * ctx->d + k] = static_cast<int64_t>(rem % static_cast<uint64_t>(ctx->dims[k]));
-        rem /= static_cast<uint64_t>(ctx->dims[k]);
+        const unsigned __int128 nk = static_cast<unsigned __int128>(ctx->dims[k]);
+        coords_out[e * ctx->d + k] = static_cast<int64_t>(rem % nk);
+        rem /= nk;
       }
       values_out[e] = v[e];
     }
@@ -2883,19 +3055,23 @@ int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out) {
     for (int64_t e = 0; e < n; ++e) check_index_host(ctx, idx + e * ctx->d);
     if (n == 0) return;
     if (ctx->tensor_kind == 2) ensure_hash(ctx);
-    std::vector<uint64_t> lin(static_cast<size_t>(n));
-    for (int64_t e = 0; e < n; ++e) {
-      uint64_t l = 0, s = 1;
-      for (int k = 0; k < ctx->d; ++k) {
-        l += static_cast<uint64_t>(idx[e * ctx->d + k]) * s;
-        s *= static_cast<uint64_t>(ctx->dims[k]);
-      }
-      lin[e] = l;
+    std::vector<uint64_t> lin(static_cast<size_t>(n)), lin_hi(static_cast<size_t>(n));
+    for (int64_t e = 0; e < n; ++e) {  // linear_index (shape.cpp:87-96), 128-bit
+      unsigned __int128 l = 0;
+      for (int k = 0; k < ctx->d; ++k)
+        l += static_cast<unsigned __int128>(idx[e * ctx->d + k]) *
+             ((static_cast<unsigned __int128>(ctx->stride_hi[k]) << 64) | ctx->stride_lo[k]);
+      lin[e] = static_cast<uint64_t>(l);
+      lin_hi[e] = static_cast<uint64_t>(l >> 64);
     }
-    DBuf dl, dx;
+    DBuf dl, dlh, dx;
     dl.alloc(n * 8);
     dx.alloc(n * 8);
     CK(cudaMemcpyAsync(dl.p, lin.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->wide) {
+      dlh.alloc(n * 8);
+      CK(cudaMemcpyAsync(dlh.p, lin_hi.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
     int xkind = X_SPARSE;
     if (ctx->tensor_kind == 1)
       xkind = ctx->dense_storage == GCPB_STORE_BIT
@@ -2907,12 +3083,14 @@ int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out) {
       value_at_kernel<float><<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
           dl.as<uint64_t>(), n, xkind, ctx->dense.p, ctx->vals.as<float>(),
           ctx->hash_ready ? ctx->hkeys.as<uint64_t>() : nullptr, ctx->hvals.as<uint32_t>(),
-          ctx->hmask, dx.as<double>());
+          ctx->hmask, dx.as<double>(), ctx->wide ? dlh.as<uint64_t>() : nullptr,
+          ctx->hkeys_hi.as<uint64_t>());
     else
       value_at_kernel<double><<<grid_for(n, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
           dl.as<uint64_t>(), n, xkind, ctx->dense.p, ctx->vals.as<double>(),
           ctx->hash_ready ? ctx->hkeys.as<uint64_t>() : nullptr, ctx->hvals.as<uint32_t>(),
-          ctx->hmask, dx.as<double>());
+          ctx->hmask, dx.as<double>(), ctx->wide ? dlh.as<uint64_t>() : nullptr,
+          ctx->hkeys_hi.as<uint64_t>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(x_out, dx.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
@@ -3317,6 +3495,7 @@ int gcpb_gen_binary_problem(gcpb_ctx* ctx, const gcpb_binary_spec* spec, gcpb_rn
                             double* truth_out) {
   return guard(ctx, [&] {
     if (!rng || !spec) throw std::invalid_argument("gen_binary_problem: null argument");
+    if (ctx->wide) throw std::invalid_argument("gen_binary_problem: N >= 2^64 not supported");
     gen_binary_impl(ctx, spec, rng, truth_out);
   });
 }

@@ -59,6 +59,9 @@ struct ZeroArgs {
   uint32_t dims[kMaxModes];
   uint32_t thr[kMaxModes];
   uint64_t stride[kMaxModes];
+  int wide;                          // N >= 2^64: 128-bit keys (stride_hi, hkeys_hi)
+  uint64_t stride_hi[kMaxModes];
+  const uint64_t* hkeys_hi;
   uint64_t seed;
   uint64_t iter;
   const uint64_t* iter_base;  // optional device-resident iteration base
@@ -382,7 +385,7 @@ __global__ void zero_check_kernel(DevState* st) {
 // of 1e-5 — is rejected from one L2-resident sector instead of a random HBM
 // probe of the 4-way hash; the ~1 % false positives and the true hits fall
 // through to the exact hash lookup.
-__device__ __forceinline__ uint64_t bloom_hash(uint64_t key) {
+GCPB_HD uint64_t bloom_hash(uint64_t key) {
   return mix64(key ^ 0x5bd1e9955bd1e995ull);
 }
 __global__ void bloom_build_kernel(const uint64_t* __restrict__ keys, int64_t n, uint32_t* bloom,
@@ -444,11 +447,14 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
       if (c >= bend) break;
       ++nvalid;
       uint64_t lin = 0;
+      uint32_t ikw[DM > 0 ? DM : kMaxModes];  // per-mode indices (128-bit keys only)
       if (a.refstream) {
         for (int k = 0; k < d; ++k) {
           const uint64_t jj = static_cast<uint64_t>(a.ref_off + c * d + k);
-          lin += refstream_below(a.ref_key, rbase + jj + 1, a.dims[k], a.thr64[k], &st->ref_flag) *
-                 a.stride[k];
+          const uint64_t ik =
+              refstream_below(a.ref_key, rbase + jj + 1, a.dims[k], a.thr64[k], &st->ref_flag);
+          lin += ik * a.stride[k];
+          if (DM == 0) ikw[k] = static_cast<uint32_t>(ik);
         }
       }
 #pragma unroll
@@ -466,11 +472,21 @@ __global__ void __launch_bounds__(kZcThreads) zero_cand_kernel(const ZeroArgs a)
                             : bounded32_from(a.seed, a.tag, iter, static_cast<uint64_t>(c), k,
                                              a.dims[k], a.thr[k], 1u);
           lin += static_cast<uint64_t>(ik) * a.stride[k];
+          if (DM == 0) ikw[k] = ik;
         }
       }
-      const bool hit = a.hkeys != nullptr &&
-                       (a.bloom == nullptr || bloom_maybe(a.bloom, a.bmask, lin)) &&
-                       hash_find(a.hkeys, a.hmask, lin) >= 0;
+      bool hit;
+      if (DM == 0 && a.wide) {  // N >= 2^64 (general-d instantiation only)
+        const unsigned __int128 l = wide_lin(ikw, a.stride, a.stride_hi, d);
+        const uint64_t lo = static_cast<uint64_t>(l), hi = static_cast<uint64_t>(l >> 64);
+        hit = a.hkeys != nullptr &&
+              (a.bloom == nullptr || bloom_maybe(a.bloom, a.bmask, wide_digest(lo, hi))) &&
+              hash_find_wide(a.hkeys, a.hkeys_hi, a.hmask, lo, hi) >= 0;
+      } else {
+        hit = a.hkeys != nullptr &&
+              (a.bloom == nullptr || bloom_maybe(a.bloom, a.bmask, lin)) &&
+              hash_find(a.hkeys, a.hmask, lin) >= 0;
+      }
       if (!hit) bits |= 1u << j;
     }
     const int cnt = __popc(bits);
@@ -1390,7 +1406,9 @@ __global__ void popcount_kernel(const uint32_t* __restrict__ w, int64_t n, doubl
 template <typename T>
 __global__ void value_at_kernel(const uint64_t* __restrict__ lin, int64_t n, int xkind,
                                 const void* dense, const T* vals, const uint64_t* hkeys,
-                                const uint32_t* hvals, uint64_t hmask, double* out) {
+                                const uint32_t* hvals, uint64_t hmask, double* out,
+                                const uint64_t* lin_hi = nullptr,
+                                const uint64_t* hkeys_hi = nullptr) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t l = lin[e];
@@ -1410,7 +1428,8 @@ __global__ void value_at_kernel(const uint64_t* __restrict__ lin, int64_t n, int
         break;
       default: {
         if (hkeys) {
-          const int64_t slot = hash_find(hkeys, hmask, l);
+          const int64_t slot = lin_hi ? hash_find_wide(hkeys, hkeys_hi, hmask, l, lin_hi[e])
+                                      : hash_find(hkeys, hmask, l);
           if (slot >= 0) x = static_cast<double>(vals[hvals[slot]]);
         }
       }
@@ -1425,7 +1444,7 @@ template <typename V, typename T>
 __global__ void keys_to_records_kernel(const uint64_t* __restrict__ keys,
                                        const V* __restrict__ vals_in, int64_t n, int d,
                                        const int64_t* dims, uint32_t* rec, int rec_words,
-                                       T* vals_out) {
+                                       T* vals_out, const uint64_t* __restrict__ keys_hi = nullptr) {
   constexpr int VWD = sizeof(T) / 4;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1435,11 +1454,20 @@ __global__ void keys_to_records_kernel(const uint64_t* __restrict__ keys,
     uint32_t vw[2] = {0u, 0u};
     memcpy(vw, &v, sizeof(T));
     for (int w = 0; w < VWD; ++w) r[w] = vw[w];
-    uint64_t rem = keys[e];
-    for (int k = 0; k < d; ++k) {
-      const uint64_t nk = static_cast<uint64_t>(dims[k]);
-      r[VWD + k] = static_cast<uint32_t>(rem % nk);
-      rem /= nk;
+    if (keys_hi) {  // 128-bit keys (N >= 2^64)
+      unsigned __int128 rem = (static_cast<unsigned __int128>(keys_hi[e]) << 64) | keys[e];
+      for (int k = 0; k < d; ++k) {
+        const unsigned __int128 nk = static_cast<unsigned __int128>(dims[k]);
+        r[VWD + k] = static_cast<uint32_t>(rem % nk);
+        rem /= nk;
+      }
+    } else {
+      uint64_t rem = keys[e];
+      for (int k = 0; k < d; ++k) {
+        const uint64_t nk = static_cast<uint64_t>(dims[k]);
+        r[VWD + k] = static_cast<uint32_t>(rem % nk);
+        rem /= nk;
+      }
     }
     for (int w = VWD + d; w < rec_words; ++w) r[w] = 0u;
   }

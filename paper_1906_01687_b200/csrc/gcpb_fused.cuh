@@ -31,6 +31,8 @@
 // every BASELINE config), so every per-mode parameter is a constant-bank
 // operand.
 #pragma once
+#include <type_traits>
+
 #include "gcpb_kernels.cuh"
 
 // Minimum resident blocks per SM requested for the common (VPL = 1) kernels;
@@ -59,6 +61,12 @@
 #endif
 
 namespace gcpb {
+
+// Element offset of a factor / gradient row inside its table: 32 bits (one
+// register per mode) unless the tables exceed 2^31 padded elements
+// (FusedArgs::off64, the OFF64 instantiations).
+template <bool OFF64>
+using RowOffT = typename std::conditional<OFF64, uint64_t, uint32_t>::type;
 
 template <typename T>
 struct Drawn {
@@ -168,7 +176,14 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
           s.x = static_cast<T>(ld_stream_f64(static_cast<const double*>(a.dense) + lin));
           break;
         case X_SPARSE: {
-          const int64_t slot = hash_find(a.hkeys, a.hmask, lin);
+          int64_t slot;
+          if (a.wide) {  // N >= 2^64: 128-bit keys
+            const unsigned __int128 l = wide_lin(ik, a.stride, a.stride_hi, d);
+            slot = hash_find_wide(a.hkeys, a.hkeys_hi, a.hmask, static_cast<uint64_t>(l),
+                                  static_cast<uint64_t>(l >> 64));
+          } else {
+            slot = hash_find(a.hkeys, a.hmask, lin);
+          }
           s.x = slot < 0 ? static_cast<T>(0) : a.vals[a.hvals[slot]];
           break;
         }
@@ -286,8 +301,8 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
 
 // Reduction target of one (mode, row): the hot-row copy rsel of the row's
 // slot when it is hot, else the block's gradient replica.
-template <typename T, bool HOT>
-__device__ __forceinline__ T* grad_row(const FusedArgs<T>& a, T* Gb, uint32_t roff, uint32_t hsv,
+template <typename T, bool HOT, typename RowOff>
+__device__ __forceinline__ T* grad_row(const FusedArgs<T>& a, T* Gb, RowOff roff, uint32_t hsv,
                                        int k, uint32_t rsel) {
   if (HOT) {
     const uint32_t sl = (hsv >> (8 * k)) & 0xFFu;
@@ -298,7 +313,8 @@ __device__ __forceinline__ T* grad_row(const FusedArgs<T>& a, T* Gb, uint32_t ro
   return Gb + roff;
 }
 
-template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, bool GV, bool HOT = false>
+template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, bool GV, bool HOT = false,
+          bool OFF64 = false>
 __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg, int64_t tile,
                                         const uint32_t (&ik)[DM], const Drawn<T>& s,
                                         T* __restrict__ Gb, uint32_t rsel = 0) {
@@ -350,10 +366,11 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
       }
     }
     // Row offsets (32-bit element offsets; factor buffers < 2^32 elements).
-    uint32_t roff[DM];
+    using RowOff = RowOffT<OFF64>;
+    RowOff roff[DM];
 #pragma unroll
     for (int k = 0; k < DM; ++k)
-      roff[k] = static_cast<uint32_t>(a.off[k]) + ii[k] * static_cast<uint32_t>(a.pitch);
+      roff[k] = static_cast<RowOff>(a.off[k]) + static_cast<RowOff>(ii[k]) * static_cast<RowOff>(a.pitch);
     T row[DM][SL];
     T pre[DM][SL];
 #pragma unroll
@@ -448,7 +465,7 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
 }
 
 template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true,
-          bool HOT = false>
+          bool HOT = false, bool OFF64 = false>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
                                                                int64_t total_tiles) {
   pdl_begin();
@@ -483,7 +500,7 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
     if (__any_sync(0xffffffffu, s.valid))  // tiles past a device-resident length
-      phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT>(a, sg, tile, ik, s, Gb, rsel);
+      phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT, OFF64>(a, sg, tile, ik, s, Gb, rsel);
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
     s = s2;
@@ -528,6 +545,12 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
     return launch_k(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream, a,
                     total_tiles);
   };
+  if (a.off64) {  // tables beyond 2^31 padded elements: 64-bit row offsets
+    if constexpr (EXACT && (DM == 3 || DM == 4)) {
+      if (vpl == 1) return go(fused_grad_kernel<T, DM, EXACT, 32, 1, REC, 1, true, false, true>);
+    }
+    return cudaErrorNotSupported;  // the host checks the shape before launching
+  }
   if (vpl == 1) {
     if constexpr (!REC && EXACT) {
       if (!given) {  // hot path: no host-given samples -> slim live state

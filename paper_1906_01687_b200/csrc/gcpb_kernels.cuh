@@ -112,6 +112,11 @@ struct FusedArgs {
   uint32_t dims[kMaxModes];
   uint32_t thr[kMaxModes];  // Lemire thresholds (2^32 - n_k) mod n_k
   uint64_t stride[kMaxModes];
+  // N >= 2^64 (sparse only): 128-bit linear keys, stride_hi the strides' high
+  // words, hkeys_hi the membership hash's high words (hash_find_wide)
+  int wide;
+  uint64_t stride_hi[kMaxModes];
+  const uint64_t* hkeys_hi;
   uint64_t seed;
   uint64_t iter;
   const uint64_t* iter_base;  // optional device-resident iteration base (graph replay)
@@ -149,6 +154,7 @@ struct FusedArgs {
   double* r_m;
   double* r_y;
   int scatter;
+  int off64;  // host-side: tables beyond 2^31 padded elements -> 64-bit row offsets
   // RefStream mode: draws reproduce the reference's RngStream
   // (rng.cpp:43-61): u = mix64(key + phi * (counter + j + 1)), value u % n,
   // with j the draw's position in the reference's consumption order.
@@ -375,6 +381,38 @@ __device__ __forceinline__ int64_t hash_find(const uint64_t* __restrict__ keys, 
       return -1;
     b = (b + 1) & mask;
   }
+}
+
+// 128-bit linear keys (N >= 2^64; shape.hpp:12-14, shape.cpp:87-96).  The
+// hash keeps the low words in `keys` (the layout above) and the high words in
+// the parallel `keys_hi`; the bucket comes from a 64-bit digest of both.  A
+// slot is empty when both words are ~0 (keys stay below 2^127), so a probe
+// reads the high word only when the low word matches or is ~0.
+GCPB_HD uint64_t wide_digest(uint64_t lo, uint64_t hi) {
+  return lo ^ mix64(hi + 0x9e3779b97f4a7c15ull);
+}
+__device__ __forceinline__ int64_t hash_find_wide(const uint64_t* __restrict__ keys,
+                                                  const uint64_t* __restrict__ keys_hi,
+                                                  uint64_t mask, uint64_t lo, uint64_t hi) {
+  uint64_t b = mix64(wide_digest(lo, hi)) & mask;
+  for (;;) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const uint64_t v = keys[b * 4 + s];
+      if (v == lo && keys_hi[b * 4 + s] == hi) return static_cast<int64_t>(b * 4 + s);
+      if (v == kEmptyKey && keys_hi[b * 4 + s] == kEmptyKey) return -1;
+    }
+    b = (b + 1) & mask;
+  }
+}
+// Sum_k ik[k] * stride_k in 128 bits (strides as low / high words).
+__device__ __forceinline__ unsigned __int128 wide_lin(const uint32_t* ik, const uint64_t* stride,
+                                                      const uint64_t* stride_hi, int d) {
+  unsigned __int128 l = 0;
+  for (int k = 0; k < d; ++k)
+    l += static_cast<unsigned __int128>(ik[k]) *
+         ((static_cast<unsigned __int128>(stride_hi[k]) << 64) | stride[k]);
+  return l;
 }
 
 // ---------------------------------------------------------------------------

@@ -378,6 +378,23 @@ class Engine:
     def set_factors(self, mats) -> None:
         self._ck(lib.gcpb_set_factors(self._h, -1, _f64(self._flat(mats))))
 
+    def set_factor(self, mode: int, mat) -> None:
+        """One mode's factor matrix (n_k x r, row-major)."""
+        m = np.ascontiguousarray(np.asarray(mat, np.float64).reshape(-1))
+        if m.size != self.dims[mode] * self.rank:
+            raise InvalidArgument(f"mode {mode}: expected shape {(self.dims[mode], self.rank)}")
+        self._ck(lib.gcpb_set_factors(self._h, mode, _f64(m)))
+
+    def factor(self, mode: int) -> np.ndarray:
+        out = np.zeros((self.dims[mode], self.rank))
+        self._ck(lib.gcpb_get_factors(self._h, mode, _f64(out)))
+        return out
+
+    def grad_mode(self, mode: int) -> np.ndarray:
+        out = np.zeros((self.dims[mode], self.rank))
+        self._ck(lib.gcpb_get_grad(self._h, mode, _f64(out)))
+        return out
+
     def factors(self):
         flat = np.zeros(sum(self._mode_sizes()), dtype=np.float64)
         self._ck(lib.gcpb_get_factors(self._h, -1, _f64(flat)))

@@ -248,16 +248,13 @@ def test_random_sparse_parity(orc, dtype, strategy, loss, r):
 
 @pytest.mark.parametrize("dims,r,dtype", [((7,), 3, "f64"), ((9, 8), 5, "f32"),
                                           ((5, 4, 3, 4, 3), 6, "f32"), ((3,) * 9, 4, "f64"),
-                                          ((11, 9, 7), 130, "f32"), ((11, 9, 7), 40, "f64"),
-                                          ((2**30, 3, 5), 4, "f32")])
+                                          ((11, 9, 7), 130, "f32"), ((11, 9, 7), 40, "f64")])
 def test_shapes_and_ranks(orc, dims, r, dtype):
     """d = 1..9 (all mode-count instantiations), r from 3 to 130 (all lane
-    geometries incl. multi-chunk lanes), and a 2^30 extent."""
+    geometries incl. multi-chunk lanes).  Extents of 2^29 and tables beyond
+    2^32 elements: tests/test_large_tables_gpu.py."""
     g = G()
     rs = np.random.default_rng(len(dims) * 100 + r)
-    big = max(dims) > 10**6
-    if big:  # factor matrices of a 2^30 mode are too large for a test: use a dense-free
-        pytest.skip("2^30-row factor matrix exceeds test memory budget")
     F = _as_dtype([rs.uniform(-1, 1, (n, r)) for n in dims], dtype)
     total = int(np.prod(dims))
     dense = rs.uniform(-1, 1, total)
