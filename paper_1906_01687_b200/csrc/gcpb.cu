@@ -1443,64 +1443,58 @@ __global__ void __launch_bounds__(256) order_count_kernel(SortSpec sp, uint32_t*
   }
 }
 
+// out[position] = ordinal relative to sp.b0 (32 bits: order_build takes n < 2^32).
 __global__ void __launch_bounds__(256) order_scatter_kernel(SortSpec sp, uint32_t* cursor,
-                                                            uint64_t* out) {
+                                                            uint32_t* out) {
   const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t t = static_cast<uint64_t>(sp.b0 + i);
-    out[atomicAdd(cursor + sort_bin(sp, it, t), 1u)] = t;
+    out[atomicAdd(cursor + sort_bin(sp, it, t), 1u)] = static_cast<uint32_t>(i);
   }
 }
 
-// Exclusive scan of the bin counts into the cursors: one block walks the bins
-// in tiles of 16 per thread (the counts are L2-resident, <= a few 100k bins).
+// Exclusive scan of the bin counts into the cursors, without any dependency
+// between blocks: block b owns bins [b * 1024, (b + 1) * 1024), sums every
+// count before them itself (coalesced, L2-resident: <= a few 100k bins) and
+// scans its own 1024.  (A one-block scan of C5's 75k bins took 64 us.)
 constexpr int kScanThreads = 1024;
-constexpr int kScanPer = 16;
 __global__ void __launch_bounds__(kScanThreads) order_scan_kernel(const uint32_t* __restrict__ cnt,
                                                                   uint32_t* __restrict__ cur,
                                                                   int64_t n) {
   __shared__ uint32_t wsum[32];
-  __shared__ uint32_t carry_s;
+  __shared__ uint32_t wpre[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t carry = 0;
-  for (int64_t base = 0; base < n; base += int64_t{kScanThreads} * kScanPer) {
-    const int64_t b = base + static_cast<int64_t>(threadIdx.x) * kScanPer;
-    uint32_t v[kScanPer];
-    uint32_t tot = 0;
+  const int64_t start = static_cast<int64_t>(blockIdx.x) * kScanThreads;
+  uint32_t before = 0;
+  for (int64_t i = threadIdx.x; i < start; i += kScanThreads) before += __ldg(cnt + i);
+  const int64_t mine = start + threadIdx.x;
+  const uint32_t v = mine < n ? __ldg(cnt + mine) : 0u;
+  uint32_t inc = v;  // inclusive warp scan of this block's bins
 #pragma unroll
-    for (int j = 0; j < kScanPer; ++j) {
-      v[j] = b + j < n ? cnt[b + j] : 0u;
-      tot += v[j];
-    }
-    uint32_t inc = tot;  // inclusive warp scan of the per-thread totals
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+  if (lane == 31) wpre[wid] = inc;
+  if (lane == 0) wsum[wid] = before;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = wpre[lane];
+    uint32_t tot = wsum[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
+      const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
     }
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      uint32_t w = wsum[lane];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += u;
-      }
-      wsum[lane] = w - wsum[lane];  // exclusive warp offsets
-      if (lane == 31) carry_s = w;
-    }
-    __syncthreads();
-    uint32_t run = carry + wsum[wid] + inc - tot;
-#pragma unroll
-    for (int j = 0; j < kScanPer; ++j) {
-      if (b + j < n) cur[b + j] = run;
-      run += v[j];
-    }
-    carry += carry_s;
-    __syncthreads();  // wsum / carry_s reused by the next tile
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    wpre[lane] = w - wpre[lane] + tot;  // exclusive warp offset + everything before the block
   }
+  __syncthreads();
+  if (mine < n) cur[mine] = wpre[wid] + inc - v;
 }
 
 bool order_wanted(const gcpb_ctx* c) {
@@ -1517,7 +1511,7 @@ bool order_reserve(gcpb_ctx* c, OrderBufs& ob, int64_t n, int64_t nbins) {
   cudaStreamIsCapturing(c->stream, &cs);
   if (cs != cudaStreamCaptureStatusNone) return false;
   if (n > ob.out_cap) {
-    ob.out.alloc(static_cast<size_t>(n) * sizeof(uint64_t));
+    ob.out.alloc(static_cast<size_t>(n) * sizeof(uint32_t));
     ob.out_cap = n;
   }
   if (nbins > ob.bins_cap) {
@@ -1544,9 +1538,10 @@ bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
   CK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nbins) * sizeof(uint32_t), stream));
   order_count_kernel<<<grid, 256, 0, stream>>>(sp, cnt);
   CK(cudaGetLastError());
-  order_scan_kernel<<<1, kScanThreads, 0, stream>>>(cnt, cur, nbins);
+  order_scan_kernel<<<static_cast<unsigned>((nbins + kScanThreads - 1) / kScanThreads), kScanThreads, 0,
+                      stream>>>(cnt, cur, nbins);
   CK(cudaGetLastError());
-  order_scatter_kernel<<<grid, 256, 0, stream>>>(sp, cur, ob.out.as<uint64_t>());
+  order_scatter_kernel<<<grid, 256, 0, stream>>>(sp, cur, ob.out.as<uint32_t>());
   CK(cudaGetLastError());
   return true;
 }
@@ -1678,7 +1673,8 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       const double wq = c->total_d / static_cast<double>(q);
       if (ordered && order_build(c, c->qorder, order_spec(c, a, TAG_GRAD_SEMI_Q, b0, b1))) {
-        a.zero_list = c->qorder.out.as<uint64_t>();  // the same draws, in mode-0 row order
+        a.zero_list32 = c->qorder.out.as<uint32_t>();  // the same draws, in mode-0 row order
+        a.zl_base = static_cast<uint64_t>(b0);
         a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
       } else {
         a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1, wq, 0, p, p);

@@ -129,7 +129,9 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
   if (!s.valid) return;
   const int kind = sg.kind;
   if (kind == SEG_UNIFORM || kind == SEG_DRAW_ZERO || kind == SEG_ZERO_LIST) {
-    const uint64_t tt = (kind == SEG_ZERO_LIST) ? a.zero_list[t] : static_cast<uint64_t>(t);
+    const uint64_t tt = (kind == SEG_ZERO_LIST)
+                            ? (a.zero_list32 ? a.zl_base + __ldcs(a.zero_list32 + t) : a.zero_list[t])
+                            : static_cast<uint64_t>(t);
     if (a.refstream) {  // parity mode: the reference's RngStream sequence
       const uint64_t rbase = *a.ref_ctr;
 #pragma unroll

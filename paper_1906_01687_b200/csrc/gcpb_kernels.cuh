@@ -136,6 +136,11 @@ struct FusedArgs {
   int nseg;
   Seg seg[3];
   const uint64_t* zero_list;
+  // ordered lists (order_build): 32-bit ordinals relative to zl_base, read
+  // instead of zero_list when set (half the list traffic; the whole list of a
+  // C5 step, 64 MB, stays in L2 between its scatter and its walk)
+  const uint32_t* zero_list32;
+  uint64_t zl_base;
   // optional: SEG_PICK reads its (global) nonzero ordinals from here instead
   // of drawing them (nonzero-sharded ranks: the picks of the global stream
   // that fall in this rank's range, compacted by pick_compact_kernel)

@@ -13,7 +13,10 @@ from collections import defaultdict
 
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__sectors_read.sum", "dram__sectors_write.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+    "lts__t_sectors_srcunit_tex_lookup_miss.sum", "lts__t_sectors_srcunit_tex_lookup_hit.sum",
+    "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_red.sum",
     "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum",
