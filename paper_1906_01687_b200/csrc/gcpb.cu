@@ -188,7 +188,14 @@ struct Tuning {
   bool no_small = false;  // GCPB_NO_SMALL: no one-launch small-problem path
   bool no_bloom = false;  // GCPB_NO_BLOOM: zero sampler without the Bloom prefilter
   int adam = 1;           // GCPB_ADAM: streaming Adam variant for tables in HBM (0 = off)
+  int fused_bps = 3;      // GCPB_FUSED_BPS: resident fused blocks per SM on the interleaved table
+                          // (C5 fused 3.46 / 2.87 / 2.95 ms at 2 / 3 / 4; 0 = as many as fit)
+  int fused_bps2 = -1;    // GCPB_FUSED_BPS2: the same for the ordered segment's own launch (-1: fused_bps)
+  int ord_side = 1;       // GCPB_ORD_SIDE: ordering on the side stream, under the pick half
   void read_env() {
+    if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = atoi(e);
+    if (const char* e = getenv("GCPB_ORD_SIDE")) ord_side = atoi(e);
+    if (const char* e = getenv("GCPB_FUSED_BPS")) fused_bps = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ADAM")) adam = atoi(e);
     if (const char* e = getenv("GCPB_IL")) il = atoi(e) != 0;
     if (const char* e = getenv("GCPB_SORTQ")) sortq = atoi(e) != 0;
@@ -226,6 +233,13 @@ struct gcpb_ctx {
   int num_sms = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  // Side stream for the ordering of the unrestricted draws (order_build): it
+  // depends only on (seed, iteration), so it runs under the pick half of the
+  // fused launch and joins before the ordered half (stoch_grad_impl,
+  // run_fused); inside a step-graph capture the fork/join become graph edges.
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool join_pending = false;  // run_fused: wait for ev_join before the last segment
   std::string err;
 
   DBuf A, Gr, B, C, As, Bs, Cs;
@@ -361,6 +375,9 @@ struct gcpb_ctx {
     if (xfer_done) cudaEventDestroy(xfer_done);
     for (void* pmap : peer_ipc) cudaIpcCloseMemHandle(pmap);
     if (comm) ncclCommDestroy(comm);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side_stream) cudaStreamDestroy(side_stream);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -1040,7 +1057,32 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     }
   }
   bool used_hot = false;
-  CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot));
+  const int bps = il ? c->tune.fused_bps : 0;
+  if (c->join_pending) {
+    // the last segment's ordered list is being built on the side stream: the
+    // segments before it go first, the join, then the ordered segment
+    c->join_pending = false;
+    if (a.nseg >= 2) {
+      FusedArgs<T> a1 = a;
+      a1.nseg = a.nseg - 1;
+      const int64_t t1 = finish_segments(a1);
+      CK(launch_fused<T>(a1, t1, record, c->stream, c->num_sms, &used_hot, bps));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+      FusedArgs<T> a2 = a;
+      a2.seg[0] = a.seg[a.nseg - 1];
+      a2.nseg = 1;
+      const int64_t t2 = finish_segments(a2);
+      bool hot2 = false;
+      CK(launch_fused<T>(a2, t2, record, c->stream, c->num_sms, &hot2,
+                         il && c->tune.fused_bps2 >= 0 ? c->tune.fused_bps2 : bps));
+      used_hot = used_hot || hot2;
+    } else {
+      CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+      CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot, bps));
+    }
+  } else {
+    CK(launch_fused<T>(a, tiles, record, c->stream, c->num_sms, &used_hot, bps));
+  }
   if (a.scatter) c->hot_last = used_hot ? a.rh : 0;
   if (ev1) CK(cudaEventRecord(ev1, c->stream));
   if (il && !fold && !c->peer_ok) {  // the all-reduce needs the gradient contiguous
@@ -1435,22 +1477,45 @@ __device__ __forceinline__ uint32_t sort_bin(const SortSpec& sp, uint64_t it, ui
   return static_cast<uint32_t>(key >> sp.shift);
 }
 
-__global__ void __launch_bounds__(256) order_count_kernel(SortSpec sp, uint32_t* cnt) {
+// Both passes keep kOrdIlp atomics in flight per thread: they are bound by the
+// L2 atomic round trip, and next to the fused kernel's pick half they get one
+// or two blocks per SM.
+constexpr int kOrdIlp = 8;
+__global__ void __launch_bounds__(256, 4) order_count_kernel(SortSpec sp, uint32_t* cnt) {
   const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    atomicAdd(cnt + sort_bin(sp, it, static_cast<uint64_t>(sp.b0 + i)), 1u);
+       i += nthr * kOrdIlp) {
+    uint32_t bin[kOrdIlp];
+#pragma unroll
+    for (int j = 0; j < kOrdIlp; ++j) {
+      const int64_t ij = i + j * nthr;
+      bin[j] = ij < sp.n ? sort_bin(sp, it, static_cast<uint64_t>(sp.b0 + ij)) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int j = 0; j < kOrdIlp; ++j)
+      if (bin[j] != 0xFFFFFFFFu) atomicAdd(cnt + bin[j], 1u);
   }
 }
 
 // out[position] = ordinal relative to sp.b0 (32 bits: order_build takes n < 2^32).
-__global__ void __launch_bounds__(256) order_scatter_kernel(SortSpec sp, uint32_t* cursor,
+__global__ void __launch_bounds__(256, 4) order_scatter_kernel(SortSpec sp, uint32_t* cursor,
                                                             uint32_t* out) {
   const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < sp.n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t t = static_cast<uint64_t>(sp.b0 + i);
-    out[atomicAdd(cursor + sort_bin(sp, it, t), 1u)] = static_cast<uint32_t>(i);
+       i += nthr * kOrdIlp) {
+    uint32_t pos[kOrdIlp];
+#pragma unroll
+    for (int j = 0; j < kOrdIlp; ++j) {
+      const int64_t ij = i + j * nthr;
+      pos[j] = 0xFFFFFFFFu;
+      if (ij < sp.n)
+        pos[j] = atomicAdd(cursor + sort_bin(sp, it, static_cast<uint64_t>(sp.b0 + ij)), 1u);
+    }
+#pragma unroll
+    for (int j = 0; j < kOrdIlp; ++j)
+      if (pos[j] != 0xFFFFFFFFu) out[pos[j]] = static_cast<uint32_t>(i + j * nthr);
   }
 }
 
@@ -1525,8 +1590,7 @@ int64_t order_bins(const SortSpec& sp) {
   return static_cast<int64_t>((sp.range - 1) >> sp.shift) + 1;
 }
 
-bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp) {
-  cudaStream_t stream = c->stream;
+bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp, cudaStream_t stream) {
   if (sp.n <= 0 || sp.n >= (int64_t{1} << 32)) return false;
   const int64_t nbins = order_bins(sp);
   if (nbins >= (int64_t{1} << 31)) return false;
@@ -1672,7 +1736,25 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     } else {
       gcpb_shard_range(q, c->rank, c->nranks, &b0, &b1);
       const double wq = c->total_d / static_cast<double>(q);
-      if (ordered && order_build(c, c->qorder, order_spec(c, a, TAG_GRAD_SEMI_Q, b0, b1))) {
+      bool built = false;
+      if (ordered) {
+        // The ordering depends only on (seed, iteration): with a pick segment
+        // ahead of it, it runs on the side stream under that segment's launch
+        // and run_fused joins before the ordered segment.
+        const bool side = c->tune.ord_side != 0 && a.nseg == 1 && c->side_stream != nullptr;
+        cudaStream_t os = c->stream;
+        if (side) {
+          CK(cudaEventRecord(c->ev_fork, c->stream));
+          CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+          os = c->side_stream;
+        }
+        built = order_build(c, c->qorder, order_spec(c, a, TAG_GRAD_SEMI_Q, b0, b1), os);
+        if (side) {
+          CK(cudaEventRecord(c->ev_join, c->side_stream));
+          c->join_pending = true;
+        }
+      }
+      if (built) {
         a.zero_list32 = c->qorder.out.as<uint32_t>();  // the same draws, in mode-0 row order
         a.zl_base = static_cast<uint64_t>(b0);
         a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
@@ -2738,6 +2820,13 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
+    {
+      int lo = 0, hi = 0;  // the ordering's few blocks go ahead of the fused kernel's
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, hi));
+      CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
     const size_t bytes = static_cast<size_t>(c->nelem) * c->tsize;
     DBuf* bufs[4] = {&c->A, &c->Gr, &c->B, &c->C};
     for (DBuf* b : bufs) {

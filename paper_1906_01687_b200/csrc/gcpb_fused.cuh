@@ -520,7 +520,7 @@ inline int pow2ceil(int v) {
 
 template <typename T, int DM, bool EXACT, bool REC>
 cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
-                            int num_sms, bool* used_hot) {
+                            int num_sms, bool* used_hot, int bps_cap) {
   constexpr int MHOT = DM == 3 ? GCPB_MINB_HOT3 : GCPB_MINB_HOT;
   constexpr int MHOT8 = DM == 4 ? GCPB_MINB_HOT8 : MHOT;
   const int nchunks = a.nchunks;
@@ -541,7 +541,9 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
       return v < 1 ? 1 : v;
     }();
     int64_t blocks = (total_tiles + 7) / 8;
-    const int64_t cap = static_cast<int64_t>(num_sms) * per_sm;
+    // bps_cap > 0: fewer resident blocks per SM than fit (random HBM access
+    // peaks below full occupancy, profiles/r01_randbw.md)
+    const int64_t cap = static_cast<int64_t>(num_sms) * (bps_cap > 0 && bps_cap < per_sm ? bps_cap : per_sm);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return launch_k(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream, a,
@@ -610,16 +612,16 @@ cudaError_t launch_fused_dm(const FusedArgs<T>& a, int64_t total_tiles, cudaStre
 
 template <typename T, bool REC>
 cudaError_t launch_fused_rec(const FusedArgs<T>& a, int64_t total_tiles, cudaStream_t stream,
-                             int num_sms, bool* used_hot) {
+                             int num_sms, bool* used_hot, int bps_cap) {
   switch (a.d) {
-    case 3: return launch_fused_dm<T, 3, true, REC>(a, total_tiles, stream, num_sms, used_hot);
-    case 4: return launch_fused_dm<T, 4, true, REC>(a, total_tiles, stream, num_sms, used_hot);
+    case 3: return launch_fused_dm<T, 3, true, REC>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
+    case 4: return launch_fused_dm<T, 4, true, REC>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
     case 1:
-    case 2: return launch_fused_dm<T, 2, false, REC>(a, total_tiles, stream, num_sms, used_hot);
+    case 2: return launch_fused_dm<T, 2, false, REC>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
     default:
       if (a.d <= 8)
-        return launch_fused_dm<T, 8, false, REC>(a, total_tiles, stream, num_sms, used_hot);
-      return launch_fused_dm<T, 16, false, REC>(a, total_tiles, stream, num_sms, used_hot);
+        return launch_fused_dm<T, 8, false, REC>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
+      return launch_fused_dm<T, 16, false, REC>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
   }
 }
 
@@ -627,11 +629,11 @@ cudaError_t launch_fused_rec(const FusedArgs<T>& a, int64_t total_tiles, cudaStr
 // (only the hot-path variants do; the caller folds Ghot back only then).
 template <typename T>
 cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
-                         cudaStream_t stream, int num_sms, bool* used_hot) {
+                         cudaStream_t stream, int num_sms, bool* used_hot, int bps_cap) {
   *used_hot = false;
   if (total_tiles <= 0) return cudaSuccess;
-  if (record) return launch_fused_rec<T, true>(a, total_tiles, stream, num_sms, used_hot);
-  return launch_fused_rec<T, false>(a, total_tiles, stream, num_sms, used_hot);
+  if (record) return launch_fused_rec<T, true>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
+  return launch_fused_rec<T, false>(a, total_tiles, stream, num_sms, used_hot, bps_cap);
 }
 
 }  // namespace gcpb

@@ -4,5 +4,5 @@
 
 namespace gcpb {
 template cudaError_t launch_fused<float>(const FusedArgs<float>&, int64_t, bool, cudaStream_t, int,
-                                                bool*);
+                                                bool*, int);
 }  // namespace gcpb

@@ -425,6 +425,6 @@ __device__ __forceinline__ unsigned __int128 wide_lin(const uint32_t* ik, const 
 // ---------------------------------------------------------------------------
 template <typename T>
 cudaError_t launch_fused(const FusedArgs<T>& a, int64_t total_tiles, bool record,
-                         cudaStream_t stream, int num_sms, bool* used_hot);
+                         cudaStream_t stream, int num_sms, bool* used_hot, int bps_cap = 0);
 
 }  // namespace gcpb
