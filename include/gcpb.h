@@ -231,6 +231,17 @@ int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
  * chosen when uniform draws, one rank, Philox, the model fits in shared
  * memory and s*d*r <= 16384; GCPB_NO_SMALL=1 disables it). */
 int gcpb_steps_path(const gcpb_ctx* ctx);
+/* Debug: with GCPB_GUARD=1 in the environment every device buffer is
+ * allocated between two 4 KB guard bands that are verified when it is released
+ * or regrown (the engine's own out-of-bounds-write check; no reference
+ * counterpart).  Returns the corrupted guard bytes seen so far in this process
+ * (-1 when guard mode is off); *buffers_checked = buffers verified. */
+int64_t gcpb_debug_guard_failures(int64_t* buffers_checked);
+/* Debug: in a checked build (-DGCPB_CHECKED, tools/checked_build.sh) the
+ * gather / scatter sites of the hot path assert their indices on the device.
+ * Returns the failed assertions so far (-1 when the library is not a checked
+ * build) and the first failing site and value. */
+int64_t gcpb_debug_check_failures(int64_t* first_site, int64_t* first_value);
 /* Kernels launched by the last gcpb_run_steps call: the kernel nodes of the
  * replayed step graph (every kernel is this library's own), or 1 for the
  * one-launch small-problem path. */

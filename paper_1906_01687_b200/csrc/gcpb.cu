@@ -63,16 +63,58 @@ void nck(ncclResult_t r, const char* what) {
 // replayed through a stale graph.
 std::atomic<uint64_t> g_dbuf_gen{0};
 
+#ifdef GCPB_CHECKED
+__device__ unsigned long long g_chk_dev[4];  // GCPB_CHECK: failures, first site, first value
+#endif
+unsigned long long* chk_counters() {
+#ifdef GCPB_CHECKED
+  void* p = nullptr;
+  ck(cudaGetSymbolAddress(&p, g_chk_dev), "cudaGetSymbolAddress");
+  return static_cast<unsigned long long*>(p);
+#else
+  return nullptr;
+#endif
+}
+
+// Guarded allocations (GCPB_GUARD=1; the pool has compute-sanitizer closed, so
+// this is the engine's own out-of-bounds-write check): every device buffer
+// sits between two 4 KB bands of 0xA5, the tail band starting at the exact
+// requested size, and the bands are verified when the buffer is released or
+// regrown.  gcpb_debug_guard_failures() reports the corrupted bytes seen so
+// far; tests/conftest.py asserts it stays zero after every GPU test.
+constexpr size_t kGuardBytes = 4096;
+const bool g_guard_on = getenv("GCPB_GUARD") != nullptr && atoi(getenv("GCPB_GUARD")) != 0;
+std::atomic<long long> g_guard_bad{0}, g_guard_checked{0};
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  size_t asked = 0;  // guard mode: the tail band starts at p + asked
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { reset(); }
+  void verify_guards() {
+    std::vector<unsigned char> h(2 * kGuardBytes);
+    unsigned char* raw = static_cast<unsigned char*>(p) - kGuardBytes;
+    if (cudaDeviceSynchronize() != cudaSuccess) return;  // a failed context is reported elsewhere
+    if (cudaMemcpy(h.data(), raw, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    if (cudaMemcpy(h.data() + kGuardBytes, static_cast<unsigned char*>(p) + asked, kGuardBytes,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return;
+    long long bad = 0;
+    for (unsigned char b : h) bad += b != 0xA5;
+    g_guard_bad.fetch_add(bad, std::memory_order_relaxed);
+    g_guard_checked.fetch_add(1, std::memory_order_relaxed);
+  }
   void reset() {
     if (p) {
-      cudaFree(p);
+      if (g_guard_on) {
+        verify_guards();
+        cudaFree(static_cast<unsigned char*>(p) - kGuardBytes);
+      } else {
+        cudaFree(p);
+      }
       g_dbuf_gen.fetch_add(1, std::memory_order_relaxed);
     }
     p = nullptr;
@@ -82,7 +124,17 @@ struct DBuf {
     if (n <= bytes && p) return;
     reset();
     if (n == 0) n = 16;
-    ck(cudaMalloc(&p, n), "cudaMalloc");
+    if (g_guard_on) {
+      unsigned char* raw = nullptr;
+      ck(cudaMalloc(reinterpret_cast<void**>(&raw), n + 2 * kGuardBytes), "cudaMalloc");
+      ck(cudaMemset(raw, 0xA5, kGuardBytes), "cudaMemset");
+      ck(cudaMemset(raw + kGuardBytes + n, 0xA5, kGuardBytes), "cudaMemset");
+      ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+      p = raw + kGuardBytes;
+      asked = n;
+    } else {
+      ck(cudaMalloc(&p, n), "cudaMalloc");
+    }
     g_dbuf_gen.fetch_add(1, std::memory_order_relaxed);
     bytes = n;
   }
@@ -188,12 +240,16 @@ struct Tuning {
   bool no_small = false;  // GCPB_NO_SMALL: no one-launch small-problem path
   bool no_bloom = false;  // GCPB_NO_BLOOM: zero sampler without the Bloom prefilter
   int adam = 1;           // GCPB_ADAM: streaming Adam variant for tables in HBM (0 = off)
-  int fused_bps = 3;      // GCPB_FUSED_BPS: resident fused blocks per SM on the interleaved table
-                          // (C5 fused 3.46 / 2.87 / 2.95 ms at 2 / 3 / 4; 0 = as many as fit)
-  int fused_bps2 = -1;    // GCPB_FUSED_BPS2: the same for the ordered segment's own launch (-1: fused_bps)
+  // Resident fused blocks per SM on the interleaved table (0 = as many as fit):
+  // GCPB_FUSED_BPS for launches of picks only, GCPB_FUSED_BPS2 for launches that
+  // walk an ordered list.  C5, one launch for both: 3.46 / 2.87 / 2.95 ms at
+  // 2 / 3 / 4; split launches (picks, list): step 3.72 ms at (3, 3), 3.87 at
+  // (3, 4), 3.62 at (4, 3), 3.78 at (4, 4), 4.06 at (3, 2).
+  int fused_bps = 0;
+  int fused_bps2 = 3;
   int ord_side = 1;       // GCPB_ORD_SIDE: ordering on the side stream, under the pick half
   void read_env() {
-    if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = atoi(e);
+    if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ORD_SIDE")) ord_side = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS")) fused_bps = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ADAM")) adam = atoi(e);
@@ -773,6 +829,8 @@ FusedArgs<T> base_args(gcpb_ctx* c, const gcpb_loss* loss, uint64_t seed, uint64
   std::memset(&a, 0, sizeof(a));
   a.A = c->A.as<T>();
   a.G = c->Gr.as<T>();
+  a.chk = chk_counters();
+  a.chk_tbl = c->nelem;
   a.nrep = 1;
   a.rep_stride = c->rep_stride;
   a.d = c->d;
@@ -1028,6 +1086,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     a.G = c->AG.as<T>() + c->rp;
     a.pitch = static_cast<int>(2 * c->rp);
     for (int k = 0; k < c->d; ++k) a.off[k] = 2 * c->off[k];
+    a.chk_tbl = 2 * c->nelem - c->rp;
     c->nrep = 1;
     a.nrep = 1;
     c->il_pending = fold;
@@ -1049,6 +1108,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
       if (a.rh > 0) {
         a.hslot = c->hslot.as<uint8_t>();
         a.Ghot = c->Ghot.as<T>();
+        a.chk_ghot = static_cast<int64_t>(c->Ghot.bytes / sizeof(T));
         for (int k = 0; k < c->d; ++k) {
           a.rowbase[k] = c->row_base[k];
           a.hbase[k] = c->hot_base[k];
@@ -1057,7 +1117,8 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     }
   }
   bool used_hot = false;
-  const int bps = il ? c->tune.fused_bps : 0;
+  const bool listed = a.zero_list32 != nullptr;  // the last segment walks an ordered list
+  const int bps = il ? (listed && !c->join_pending ? c->tune.fused_bps2 : c->tune.fused_bps) : 0;
   if (c->join_pending) {
     // the last segment's ordered list is being built on the side stream: the
     // segments before it go first, the join, then the ordered segment
@@ -1074,7 +1135,7 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
       const int64_t t2 = finish_segments(a2);
       bool hot2 = false;
       CK(launch_fused<T>(a2, t2, record, c->stream, c->num_sms, &hot2,
-                         il && c->tune.fused_bps2 >= 0 ? c->tune.fused_bps2 : bps));
+                         il && listed ? c->tune.fused_bps2 : bps));
       used_hot = used_hot || hot2;
     } else {
       CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
@@ -1461,6 +1522,8 @@ struct SortSpec {
   uint64_t range;  // n_0
   uint32_t thr;    // Lemire threshold of range (32-bit draws)
   int shift;
+  unsigned long long* chk;  // checked builds: failure counters, bins of the sort
+  int64_t nbins;
 };
 
 __device__ __forceinline__ uint32_t sort_bin(const SortSpec& sp, uint64_t it, uint64_t t) {
@@ -1494,7 +1557,10 @@ __global__ void __launch_bounds__(256, 4) order_count_kernel(SortSpec sp, uint32
     }
 #pragma unroll
     for (int j = 0; j < kOrdIlp; ++j)
-      if (bin[j] != 0xFFFFFFFFu) atomicAdd(cnt + bin[j], 1u);
+      if (bin[j] != 0xFFFFFFFFu) {
+        GCPB_CHECK(sp.chk, bin[j] < sp.nbins, 10, bin[j]);
+        atomicAdd(cnt + bin[j], 1u);
+      }
   }
 }
 
@@ -1515,7 +1581,10 @@ __global__ void __launch_bounds__(256, 4) order_scatter_kernel(SortSpec sp, uint
     }
 #pragma unroll
     for (int j = 0; j < kOrdIlp; ++j)
-      if (pos[j] != 0xFFFFFFFFu) out[pos[j]] = static_cast<uint32_t>(i + j * nthr);
+      if (pos[j] != 0xFFFFFFFFu) {
+        GCPB_CHECK(sp.chk, pos[j] < sp.n, 11, pos[j]);
+        out[pos[j]] = static_cast<uint32_t>(i + j * nthr);
+      }
   }
 }
 
@@ -1623,6 +1692,8 @@ SortSpec order_spec(const gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int6
   sp.range = a.dims[0];
   sp.thr = a.thr[0];
   sp.shift = c->tune.qshift;  // 64 mode-0 rows per bin by default
+  sp.chk = chk_counters();
+  sp.nbins = order_bins(sp);
   return sp;
 }
 
@@ -1706,6 +1777,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p);
     }
     a.zero_list = c->zero_list.as<uint64_t>();
+    a.chk_zl = static_cast<int64_t>(c->zero_list.bytes / sizeof(uint64_t));
   }
   a.nseg = 0;
   const bool ordered = scatter && !record && est_kind < 0 && c->draw_stream == 0 &&
@@ -1757,6 +1829,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       if (built) {
         a.zero_list32 = c->qorder.out.as<uint32_t>();  // the same draws, in mode-0 row order
         a.zl_base = static_cast<uint64_t>(b0);
+        a.chk_zl = c->qorder.out_cap;
         a.seg[a.nseg++] = make_seg(SEG_ZERO_LIST, TAG_GRAD_SEMI_Q, 0, b1 - b0, wq, 0, p, p);
       } else {
         a.seg[a.nseg++] = make_seg(SEG_DRAW_ZERO, TAG_GRAD_SEMI_Q, b0, b1, wq, 0, p, p);
@@ -3484,6 +3557,26 @@ int gcpb_get_draw_counter(gcpb_ctx* ctx, uint64_t* counter) {
 
 int gcpb_steps_path(const gcpb_ctx* ctx) { return ctx ? ctx->last_steps_path : -1; }
 
+int64_t gcpb_debug_check_failures(int64_t* first_site, int64_t* first_value) {
+#ifdef GCPB_CHECKED
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  if (cudaMemcpyFromSymbol(h, g_chk_dev, sizeof(h)) != cudaSuccess) return -2;
+  if (first_site) *first_site = static_cast<int64_t>(h[1]);
+  if (first_value) *first_value = static_cast<int64_t>(h[2]);
+  return static_cast<int64_t>(h[0]);
+#else
+  if (first_site) *first_site = 0;
+  if (first_value) *first_value = 0;
+  return -1;
+#endif
+}
+
+int64_t gcpb_debug_guard_failures(int64_t* buffers_checked) {
+  if (buffers_checked) *buffers_checked = g_guard_checked.load(std::memory_order_relaxed);
+  return g_guard_on ? g_guard_bad.load(std::memory_order_relaxed) : -1;
+}
+
 int gcpb_run_steps_launches(const gcpb_ctx* ctx, int64_t* kernels) {
   if (!ctx || !kernels) return GCPB_ERR_USAGE;
   *kernels = ctx->last_steps_path == 1 ? 1 : ctx->graph_kernels;
@@ -3935,6 +4028,10 @@ int gcpb_peer_handle(gcpb_ctx* ctx, void* out) {
     b.nelem = ctx->nelem;
     void* base_a = ctx->il_enabled ? ctx->AG.p : ctx->A.p;
     void* base_g = ctx->il_enabled ? ctx->AG.p : ctx->Gr.p;
+    if (g_guard_on) {  // guarded allocations start one band earlier
+      base_a = static_cast<unsigned char*>(base_a) - kGuardBytes;
+      base_g = static_cast<unsigned char*>(base_g) - kGuardBytes;
+    }
     CK(cudaIpcGetMemHandle(&b.ha, base_a));
     CK(cudaIpcGetMemHandle(&b.hg, base_g));
     b.raw_a = reinterpret_cast<uint64_t>(a);

@@ -129,6 +129,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
   if (!s.valid) return;
   const int kind = sg.kind;
   if (kind == SEG_UNIFORM || kind == SEG_DRAW_ZERO || kind == SEG_ZERO_LIST) {
+    if (kind == SEG_ZERO_LIST) GCPB_CHECK(a.chk, t >= 0 && t < a.chk_zl, 1, t);
     const uint64_t tt = (kind == SEG_ZERO_LIST)
                             ? (a.zero_list32 ? a.zl_base + __ldcs(a.zero_list32 + t) : a.zero_list[t])
                             : static_cast<uint64_t>(t);
@@ -216,6 +217,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
       // One aligned record per nonzero: value + coordinates arrive in one
       // 16/32-byte vector load (a single sector for d <= 7 in fp32).
       const int64_t el = static_cast<int64_t>(e) - a.nz_begin;
+      GCPB_CHECK(a.chk, e < a.eta, 2, e);
       constexpr int VWD = sizeof(T) / 4;      // value words
       constexpr int NQ = (VWD + DM + 3) / 4;  // uint4 loads covering value + DM coords
       const uint4* rp = reinterpret_cast<const uint4*>(a.nzrec + el * a.rec_words);
@@ -291,6 +293,13 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
       s.flag = a.g_flag ? a.g_flag[t] : 0;
     }
   }
+#ifdef GCPB_CHECKED
+  if (s.valid) {
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+      if (EXACT || k < d) GCPB_CHECK(a.chk, ik[k] < a.dims[k], 3, ik[k]);
+  }
+#endif
   if (HOT && s.valid) {
     static_assert(!HOT || DM <= 4, "hot-row slots pack 8 bits per mode");
     uint32_t hs = 0;
@@ -308,9 +317,14 @@ __device__ __forceinline__ T* grad_row(const FusedArgs<T>& a, T* Gb, RowOff roff
                                        int k, uint32_t rsel) {
   if (HOT) {
     const uint32_t sl = (hsv >> (8 * k)) & 0xFFu;
-    if (sl != 0xFFu)
+    if (sl != 0xFFu) {
+      GCPB_CHECK(a.chk,
+                 static_cast<int64_t>((a.hbase[k] + sl) * static_cast<uint32_t>(a.rh) + rsel + 1) *
+                         a.rp <= a.chk_ghot && rsel < static_cast<uint32_t>(a.rh),
+                 5, sl);
       return a.Ghot + ((a.hbase[k] + sl) * static_cast<uint32_t>(a.rh) + rsel) *
                           static_cast<uint32_t>(a.rp);
+    }
   }
   return Gb + roff;
 }
@@ -373,6 +387,12 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
     for (int k = 0; k < DM; ++k)
       roff[k] = static_cast<RowOff>(a.off[k]) + static_cast<RowOff>(ii[k]) * static_cast<RowOff>(a.pitch);
+#ifdef GCPB_CHECKED
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+      if (EXACT || k < d)
+        GCPB_CHECK(a.chk, static_cast<int64_t>(roff[k]) + a.nchunks * VW <= a.chk_tbl, 4, roff[k]);
+#endif
     T row[DM][SL];
     T pre[DM][SL];
 #pragma unroll

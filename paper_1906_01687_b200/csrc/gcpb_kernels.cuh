@@ -58,6 +58,25 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 constexpr int kMaxModes = 16;
 constexpr uint64_t kEmptyKey = ~0ull;
 
+// Checked build (-DGCPB_CHECKED, tools/checked_build.sh): index assertions at
+// the gather / scatter sites of the hot path.  A failed check does not trap
+// (that would lose the context): it counts into chk[0] and keeps the first
+// failing site and value in chk[1], chk[2]; gcpb_debug_check_failures reads
+// them and tests/conftest.py asserts zero after every GPU test.
+#ifdef GCPB_CHECKED
+#define GCPB_CHECK(chk, cond, site, val)                                          \
+  do {                                                                            \
+    if ((chk) != nullptr && !(cond)) {                                            \
+      if (atomicAdd((chk), 1ull) == 0ull) {                                       \
+        (chk)[1] = static_cast<unsigned long long>(site);                         \
+        (chk)[2] = static_cast<unsigned long long>(val);                          \
+      }                                                                           \
+    }                                                                             \
+  } while (0)
+#else
+#define GCPB_CHECK(chk, cond, site, val) ((void)0)
+#endif
+
 // Data-access kinds for the tensor value x at a sampled index.
 enum XKind : int {
   X_NONE = 0,
@@ -141,6 +160,11 @@ struct FusedArgs {
   // C5 step, 64 MB, stays in L2 between its scatter and its walk)
   const uint32_t* zero_list32;
   uint64_t zl_base;
+  // checked builds (GCPB_CHECK): failure counters and the extents the indices
+  // are checked against (elements of the factor / gradient table past A and G,
+  // entries of the zero list, elements of Ghot); unused otherwise
+  unsigned long long* chk;
+  int64_t chk_tbl, chk_zl, chk_ghot;
   // optional: SEG_PICK reads its (global) nonzero ordinals from here instead
   // of drawing them (nonzero-sharded ranks: the picks of the global stream
   // that fall in this rank's range, compacted by pick_compact_kernel)
