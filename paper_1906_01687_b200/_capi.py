@@ -157,6 +157,7 @@ SIGNATURES = [
     ("gcpb_set_shard", C.c_int, [ctx_p, C.c_int, C.c_int]),
     ("gcpb_peer_handle", C.c_int, [ctx_p, C.c_void_p]),
     ("gcpb_peer_open", C.c_int, [ctx_p, C.c_char_p, C.c_int]),
+    ("gcpb_peer_close", C.c_int, [ctx_p]),
     ("gcpb_allreduce_grad", C.c_int, [ctx_p]),
     ("gcpb_comm_init_host", C.c_int, [ctx_p, C.c_int, C.c_int, ALLGATHER_FN, ALLREDUCE_FN,
                                       C.c_void_p]),

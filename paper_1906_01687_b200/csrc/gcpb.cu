@@ -248,7 +248,11 @@ struct Tuning {
   int fused_bps = 0;
   int fused_bps2 = 3;
   int ord_side = 1;       // GCPB_ORD_SIDE: ordering on the side stream, under the pick half
+  int side_bps = 3;       // GCPB_SIDE_BPS: fused blocks per SM of the pick launch while the side
+                          // stream works (L2-resident tables; 0 = as many as fit; C3 step 235 / 228 /
+                          // 253 / 342 us at 0 / 3 / 2 / 1)
   void read_env() {
+    if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ORD_SIDE")) ord_side = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS")) fused_bps = std::max(0, atoi(e));
@@ -1127,7 +1131,8 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
       FusedArgs<T> a1 = a;
       a1.nseg = a.nseg - 1;
       const int64_t t1 = finish_segments(a1);
-      CK(launch_fused<T>(a1, t1, record, c->stream, c->num_sms, &used_hot, bps));
+      CK(launch_fused<T>(a1, t1, record, c->stream, c->num_sms, &used_hot,
+                         il ? bps : c->tune.side_bps));
       CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
       FusedArgs<T> a2 = a;
       a2.seg[0] = a.seg[a.nseg - 1];
@@ -1773,6 +1778,25 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       run_zero_sampler_mr(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p,
                           &res.stats);
       zero_mr = true;
+    } else if (zero_mode != ZERO_HOST_CHECK && p > 0 && eta > 0 && c->tune.ord_side != 0 &&
+               c->side_stream != nullptr) {
+      // device-planned batches (no host round trip): the zero sampler runs on
+      // the side stream under the pick segment's launch -- it is issue-bound
+      // (Philox + hashing), the picks are bound by the L2 reductions -- and
+      // run_fused joins before the zero-list segment
+      CK(cudaEventRecord(c->ev_fork, c->stream));
+      CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+      cudaStream_t main_stream = c->stream;
+      c->stream = c->side_stream;
+      try {
+        run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p);
+      } catch (...) {
+        c->stream = main_stream;
+        throw;
+      }
+      c->stream = main_stream;
+      CK(cudaEventRecord(c->ev_join, c->side_stream));
+      c->join_pending = true;
     } else {
       run_zero_sampler(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p);
     }
@@ -4083,6 +4107,17 @@ int gcpb_peer_open(gcpb_ctx* ctx, const void* handles, int nranks) {
       ctx->peer_g[static_cast<size_t>(p)] = static_cast<char*>(mg) + (b.raw_g - b.base_g);
     }
     ctx->peer_ok = nranks > 1;
+  });
+}
+
+int gcpb_peer_close(gcpb_ctx* ctx) {
+  return guard(ctx, [&] {
+    ctx->sync();
+    for (void* pmap : ctx->peer_ipc) cudaIpcCloseMemHandle(pmap);
+    ctx->peer_ipc.clear();
+    ctx->peer_a.clear();
+    ctx->peer_g.clear();
+    ctx->peer_ok = false;
   });
 }
 

@@ -672,6 +672,10 @@ class Engine:
         blob = b"".join(bytes(h) for h in handles)
         self._ck(lib.gcpb_peer_open(self._h, blob, len(handles)))
 
+    def peer_close(self) -> None:
+        """Back to the NCCL all-reduce + replicated Adam exchange (gcpb_peer_close)."""
+        self._ck(lib.gcpb_peer_close(self._h))
+
     def comm_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
         self._ck(lib.gcpb_comm_init(self._h, unique_id, rank, nranks))
 
