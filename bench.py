@@ -213,12 +213,15 @@ ROOFLINE_NOTES = {
     "c3": "factors (512 KB) L2-resident; bound by L2 reductions and the hash probes",
     "c4": "latency-bound: 2e5 samples per step (1.3 tiles per warp)",
     "c5": "random HBM row access (factors 531 MB): factor and gradient rows interleaved in one "
-          "128-byte line so a row gather and its reduction share a DRAM burst, and the "
-          "unrestricted draws walked in mode-0 row order (mode 0 swept instead of gathered); ncu "
-          "DRAM traffic 334 B/sample (B_alg 396; 401 in ordinal order) at 3.8 TB/s, "
-          "long-scoreboard bound (profiles/r01_c5_ordered.md); the random-access "
-          "microbenchmark tops out at 6.0e9 samples/s for the unordered mix (tools/randbw.cu, "
-          "profiles/r01_randbw.md)",
+          "128-byte line so a row gather and its reduction share a DRAM burst; two fused "
+          "launches per step -- the pick half, with the ordering of the unrestricted draws "
+          "(counting sort by mode-0 row block) running under it on a side stream, then the "
+          "unrestricted half walked in mode-0 row order (mode 0 swept instead of gathered); "
+          "kernel_ms spans both launches.  ncu DRAM traffic 327 B/sample (B_alg 396) at "
+          "3.7-3.8 TB/s per launch, long-scoreboard bound "
+          "(profiles/r02_c5_fused_picks.md, r02_c5_fused_list.md): the binding limit is the "
+          "random 128-byte-line access rate of HBM, not its streaming bandwidth "
+          "(tools/randbw.cu, profiles/r01_randbw.md)",
 }
 
 
@@ -464,7 +467,10 @@ def run_ours(args, w):
         fused_total, nl = e.kernel_time()
         e.kernel_timing(False)
         fused_ms = fused_total / max(nl, 1)
-        kernel_name = "fused_grad_kernel (sample+eval+deriv+MTTKRP)"
+        kernel_name = ("fused_grad_kernel (sample+eval+deriv+MTTKRP); stratified and "
+                       "semi-stratified steps launch it twice (pick segment, then the list "
+                       "segment whose list is built on a side stream meanwhile): kernel_ms "
+                       "spans both")
     if dist:
         t = torch.tensor([fused_ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -493,6 +499,17 @@ def run_ours(args, w):
         # DRAM-counter cross-check: the ncu capture's bytes over this run's
         # launch time (ncu times are cold and serialised; the bytes are not)
         roofline["traffic_frac"] = round(traffic / (fused_ms / 1e3) / 1e9 / peak_gbs, 4)
+    if w.name == "c5" and traffic:
+        # Tables in HBM: the binding ceiling is the rate of random 128-byte-line
+        # accesses (fill + 64-byte write-back of the dirty gradient half),
+        # measured by tools/randbw.cu on the same mix without arithmetic
+        # (profiles/r01_randbw.md, "3g+3red il": 6.99e9 samples/s x 3 lines x 192 B)
+        roofline["binding"] = {"limit": "random 128-byte-line HBM access (row gather + reduction "
+                                        "mix, interleaved lines)",
+                               "achieved": round(traffic / (fused_ms / 1e3) / 1e9, 1),
+                               "peak": 4026.0, "unit": "GB/s of DRAM traffic",
+                               "frac": round(traffic / (fused_ms / 1e3) / 1e9 / 4026.0, 3),
+                               "source": "tools/randbw.cu microbenchmark, profiles/r01_randbw.md"}
     if bound == "l2_red":
         # L2-resident factors: the binding ceiling is the L2 vector-reduction
         # rate, measured by tools/bulkred.cu (profiles/r01_bulkred.md: 6.4e7

@@ -247,12 +247,15 @@ struct Tuning {
   // (3, 4), 3.62 at (4, 3), 3.78 at (4, 4), 4.06 at (3, 2).
   int fused_bps = 0;
   int fused_bps2 = 3;
+  int list_hot = 0;       // GCPB_LIST_HOT: hot-row copies also for the list segment's own launch
+                          // (uniform rows: a hot row sees q / n_k reductions, no contention)
   int ord_side = 1;       // GCPB_ORD_SIDE: ordering on the side stream, under the pick half
   int side_bps = 3;       // GCPB_SIDE_BPS: fused blocks per SM of the pick launch while the side
                           // stream works (L2-resident tables; 0 = as many as fit; C3 step 235 / 228 /
                           // 253 / 342 us at 0 / 3 / 2 / 1)
   void read_env() {
     if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
+    if (const char* e = getenv("GCPB_LIST_HOT")) list_hot = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ORD_SIDE")) ord_side = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS")) fused_bps = std::max(0, atoi(e));
@@ -1137,6 +1140,9 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
       FusedArgs<T> a2 = a;
       a2.seg[0] = a.seg[a.nseg - 1];
       a2.nseg = 1;
+      // uniformly drawn rows: straight into the gradient rows (the Adam fold
+      // adds a hot row's copies to its gradient row), no hot-slot lookups
+      if (!c->tune.list_hot) a2.rh = 0;
       const int64_t t2 = finish_segments(a2);
       bool hot2 = false;
       CK(launch_fused<T>(a2, t2, record, c->stream, c->num_sms, &hot2,

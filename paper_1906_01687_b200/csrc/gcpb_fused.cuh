@@ -486,6 +486,103 @@ __device__ __forceinline__ void phase_b(const FusedArgs<T>& a, const SegRegs& sg
   }
 }
 
+// Measurement variant (-DGCPB_PB=2 or 4 through GCPB_NVFLAGS; default build: 1 =
+// off): phase B of the slim hot-path kernels with PB passes per batch -- the
+// row gathers of PB passes are issued before any of their arithmetic and
+// reductions, so a warp keeps PB x DM row loads in flight instead of DM.
+// Kept to reproduce DESIGN.md §5's measurement that the C5 kernel is not
+// short of loads in flight.
+#ifndef GCPB_PB
+#define GCPB_PB 1
+#endif
+template <typename T, int DM, int G, int PB, bool HOT>
+__device__ __forceinline__ void phase_b_batched(const FusedArgs<T>& a, const SegRegs& sg,
+                                                const uint32_t (&ik)[DM], const Drawn<T>& s,
+                                                T* __restrict__ Gb, uint32_t rsel) {
+  constexpr int VW = Vec<T>::W;
+  constexpr int NGRP = 32 / G;
+  constexpr int NPASS = (32 + NGRP - 1) / NGRP;
+  constexpr bool POW2 = (G & (G - 1)) == 0;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int gl = lane % G;
+  const T wseg = static_cast<T>(sg.weight);
+  const int fv = sg.flag;
+  const int cidx = gl < a.nchunks ? gl : a.nchunks - 1;
+  const T cmask = gl < a.nchunks ? static_cast<T>(1) : static_cast<T>(0);
+  const bool owns = gl < a.nchunks;
+#pragma unroll 1
+  for (int p0 = 0; p0 < NPASS; p0 += PB) {
+    bool v[PB];
+    T xv[PB];
+    uint32_t hsv[PB];
+    uint32_t roff[PB][DM];
+    T row[PB][DM][VW];
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      const int pass = p0 + j;
+      const int src = (pass * NGRP + grp) & 31;
+      v[j] = __shfl_sync(FULL, s.valid, src) && pass < NPASS &&
+             (POW2 || (grp < NGRP && pass * NGRP + grp < 32));
+      xv[j] = __shfl_sync(FULL, s.x, src);
+      hsv[j] = HOT ? __shfl_sync(FULL, s.hs, src) : 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < DM; ++k) {
+        roff[j][k] = static_cast<uint32_t>(a.off[k]) +
+                     __shfl_sync(FULL, ik[k], src) * static_cast<uint32_t>(a.pitch);
+        Vec<T> q;
+        load_chunk(a.A + roff[j][k] + cidx * VW, q);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) row[j][k][e] = q.v[e];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      T pre[DM][VW];
+      T mp = static_cast<T>(0);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        T p = row[j][0][e];
+        pre[0][e] = static_cast<T>(1);
+#pragma unroll
+        for (int k = 1; k < DM; ++k) {
+          pre[k][e] = p;
+          p = p * row[j][k][e];
+        }
+        mp += p;
+      }
+      mp *= cmask;
+      if constexpr (POW2) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) mp += __shfl_xor_sync(FULL, mp, o);
+      } else {
+        T tot = static_cast<T>(0);
+#pragma unroll
+        for (int jj = 0; jj < G; ++jj) tot += __shfl_sync(FULL, mp, (grp * G + jj) & 31);
+        mp = tot;
+      }
+      T g = loss_deriv_fast(a.loss, a.delta, xv[j], mp);
+      if (fv) g = g - loss_deriv_fast(a.loss, a.delta, static_cast<T>(0), mp);
+      const T y = wseg * g;
+      const bool act = v[j] && owns;
+      T suf[VW];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) suf[e] = static_cast<T>(1);
+#pragma unroll
+      for (int k = DM - 1; k >= 0; --k) {
+        T out[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          out[e] = y * (pre[k][e] * suf[e]);
+          suf[e] = suf[e] * row[j][k][e];
+        }
+        if (act) red_chunk(grad_row<T, HOT>(a, Gb, roff[j][k], hsv[j], k, rsel) + cidx * VW, out);
+      }
+    }
+  }
+}
+
 template <typename T, int DM, bool EXACT, int G, int VPL, bool REC, int MINB, bool GV = true,
           bool HOT = false, bool OFF64 = false>
 __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T> a,
@@ -521,8 +618,12 @@ __global__ void __launch_bounds__(256, MINB) fused_grad_kernel(const FusedArgs<T
 #pragma unroll
       for (int k = 0; k < DM; ++k) ik2[k] = 0;
     }
-    if (__any_sync(0xffffffffu, s.valid))  // tiles past a device-resident length
-      phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT, OFF64>(a, sg, tile, ik, s, Gb, rsel);
+    if (__any_sync(0xffffffffu, s.valid)) {  // tiles past a device-resident length
+      if constexpr (GCPB_PB > 1 && EXACT && VPL == 1 && !REC && !GV && !OFF64 && DM <= 4)
+        phase_b_batched<T, DM, G, GCPB_PB, HOT>(a, sg, ik, s, Gb, rsel);
+      else
+        phase_b<T, DM, EXACT, G, VPL, REC, GV, HOT, OFF64>(a, sg, tile, ik, s, Gb, rsel);
+    }
 #pragma unroll
     for (int k = 0; k < DM; ++k) ik[k] = ik2[k];
     s = s2;

@@ -279,3 +279,39 @@ def test_ordered_segments_match_ordinal_order(monkeypatch, qshift, dtype):
     g1, m1 = run("1")
     assert O.rel_error(g1, g0) <= tol
     assert O.rel_error(m1, m0) <= tol
+
+
+@pytest.mark.parametrize("strategy", [2, 1])
+def test_side_stream_sampling_matches_main_stream(monkeypatch, strategy):
+    """The ordering of the unrestricted draws (semi-stratified, interleaved
+    table) and the device-planned zero sampler (stratified) run on a side
+    stream under the pick segment's launch, and the fused launch is split at
+    the join.  Same draws, same lists: iterations and the
+    replayed step graph equal the main-stream run, and the split really
+    happened (one more fused launch per step in the captured graph)."""
+    monkeypatch.setenv("GCPB_HOT_T", "4")
+    g = G()
+    rs = np.random.default_rng(9)
+    dims, r = (300, 40, 50), 8
+    coords, vals = _zipf_coords(rs, dims, 3000)
+    F = [rs.uniform(0.1, 1.0, (n, r)) for n in dims]
+    if strategy == 2:
+        sk, lf = g.SamplerKind.semi_stratified(7000, 9000), g.LossFunction.poisson()
+    else:
+        sk, lf = g.SamplerKind.stratified(7000, 9000), g.LossFunction.poisson()
+
+    def run(side):
+        monkeypatch.setenv("GCPB_ORD_SIDE", side)
+        e = _engine(g, monkeypatch, True, dims, r, "f64", coords, vals, F)
+        for it in range(3):
+            e.step(sk, lf, 3, it, 1e-2, lower_bound=0.0)
+        e.run_steps(sk, lf, 3, 3, 4, 1e-2, lower_bound=0.0)
+        launches = e.run_steps_launches()
+        out = _flat(e)
+        e.close()
+        return out, launches
+
+    m0, l0 = run("0")
+    m1, l1 = run("1")
+    assert O.rel_error(m1, m0) <= 1e-10
+    assert l1 == l0 + 4  # 4 replayed steps, each with the fused launch split in two
