@@ -470,6 +470,7 @@ namespace {
 template <typename F>
 int guard(gcpb_ctx* ctx, F&& f) {
   std::string* err = ctx ? &ctx->err : &g_global_err;
+  if (ctx) ctx->join_pending = false;  // no side-stream join survives a call that threw
   try {
     f();
     return GCPB_OK;
