@@ -8,6 +8,7 @@
 // Errors are C++ exceptions internally, mapped at the boundary onto the
 // reference's exception classes (status codes, gcpb_last_error()).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <nccl.h>
 
 #include <unistd.h>
@@ -466,6 +467,15 @@ struct gcpb_ctx {
 };
 
 namespace {
+
+// NVTX range around a C-ABI call (visible in Nsight Systems / ncu --nvtx; a
+// no-op without an attached tool).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <typename F>
 int guard(gcpb_ctx* ctx, F&& f) {
@@ -2988,6 +2998,7 @@ void* gcpb_get_stream(gcpb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stre
 // ---- tensor data -------------------------------------------------------------------
 int gcpb_set_sparse(gcpb_ctx* ctx, int64_t nnz, const int64_t* coords, const double* values) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_set_sparse");
     if (nnz < 0) throw std::invalid_argument("sparse tensor: negative nnz");
     if (nnz > 0 && (!coords || !values)) throw std::invalid_argument("sparse tensor: null buffers");
     if (ctx->wide)
@@ -3109,6 +3120,7 @@ int gcpb_get_sparse(gcpb_ctx* ctx, int64_t* coords_out, double* values_out) {
 
 int gcpb_set_dense(gcpb_ctx* ctx, const double* values, int storage) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_set_dense");
     if (!ctx->total_fits || ctx->total > (uint64_t{1} << 40))
       throw std::invalid_argument("dense tensor too large to materialize");
     const uint64_t n = ctx->total;
@@ -3289,12 +3301,14 @@ int gcpb_value_at(gcpb_ctx* ctx, int64_t n, const int64_t* idx, double* x_out) {
 // ---- factors / gradient / moments -----------------------------------------------------
 int gcpb_set_factors(gcpb_ctx* ctx, int mode, const double* values) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_set_factors");
     ctx->check_mode(mode);
     upload(ctx, ctx->A, mode, values);
   });
 }
 int gcpb_get_factors(gcpb_ctx* ctx, int mode, double* out) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_get_factors");
     ctx->check_mode(mode);
     download(ctx, ctx->A, mode, out);
   });
@@ -3331,6 +3345,7 @@ int gcpb_set_moment(gcpb_ctx* ctx, int which, int mode, const double* values) {
 int gcpb_stoch_grad(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                     uint64_t seed, uint64_t iter, gcpb_stats* stats) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_stoch_grad");
     validate_sampler(sampler);
     validate_loss(loss);
     if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
@@ -3359,6 +3374,7 @@ int gcpb_draw_samples(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_los
                       double* x_out, double* w_out, int32_t* flag_out, double* m_out,
                       double* y_out, int64_t* n_out, gcpb_stats* stats) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_draw_samples");
     validate_sampler(sampler);
     validate_loss(loss);
     if (ctx->tensor_kind == 0) throw std::invalid_argument("no tensor set");
@@ -3443,6 +3459,7 @@ int gcpb_mttkrp_samples(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const doub
 // ---- optimizer -------------------------------------------------------------------------------
 int gcpb_adam_step(gcpb_ctx* ctx, const gcpb_adam* adam) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_adam_step");
     set_adam_params(ctx, adam);
     if (ctx->dtype == GCPB_F32)
       adam_launch<float>(ctx);
@@ -3480,6 +3497,7 @@ int gcpb_set_iterations(gcpb_ctx* ctx, int64_t iterations) {
 int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss, uint64_t seed,
               uint64_t iter, const gcpb_adam* adam) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_step");
     check_step_args(ctx, sampler, loss);
     set_adam_params(ctx, adam);
     ensure_grad_zero(ctx);
@@ -3494,6 +3512,7 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
                    uint64_t seed, uint64_t iter, const gcpb_adam* adam, const double* model_in,
                    double* model_out) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_step_host");
     check_step_args(ctx, sampler, loss);
     // Small problems on page-locked buffers: one cluster launch reads the
     // model from host memory, runs the iteration and writes it back (no
@@ -3535,6 +3554,7 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
 int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter0, int64_t n, const gcpb_adam* adam) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_run_steps");
     check_step_args(ctx, sampler, loss);
     if (n < 0) throw std::invalid_argument("negative step count");
     if (n == 0) return;
@@ -3634,6 +3654,7 @@ int gcpb_synchronize(gcpb_ctx* ctx) {
 
 int gcpb_gradient_full(gcpb_ctx* ctx, const gcpb_loss* loss) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_gradient_full");
     validate_loss(loss);
     if (ctx->dtype == GCPB_F32)
       gradient_full_impl<float>(ctx, loss);
@@ -3645,6 +3666,7 @@ int gcpb_gradient_full(gcpb_ctx* ctx, const gcpb_loss* loss) {
 
 int gcpb_gradient_poisson_implicit(gcpb_ctx* ctx, const gcpb_loss* loss) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_gradient_poisson_implicit");
     validate_loss(loss);
     no_nz_shard(ctx, "gradient_poisson_implicit");
     if (ctx->dtype == GCPB_F32)
@@ -3670,6 +3692,7 @@ int gcpb_bias_variance(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_lo
                        int64_t trials, uint64_t seed, const double* exact, double* bias,
                        double* variance) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_bias_variance");
     check_step_args(ctx, sampler, loss);
     no_nz_shard(ctx, "empirical_bias_variance");
     if (ctx->dtype == GCPB_F32)
@@ -3713,6 +3736,7 @@ int gcpb_fit_gcp_adam(gcpb_ctx* ctx, const gcpb_loss* loss, const gcpb_fit_confi
                       gcpb_trace_record* trace, int64_t trace_cap, int64_t* n_trace,
                       double* final_estimate) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_fit_gcp_adam");
     using clock = std::chrono::steady_clock;
     const auto start = clock::now();
     auto secs = [](clock::time_point a) {
@@ -3891,6 +3915,7 @@ int gcpb_estimator_set(gcpb_ctx* ctx, int64_t n, const int64_t* idx, const doubl
 
 int gcpb_estimator_draw(gcpb_ctx* ctx, int kind, int64_t count, double rho, uint64_t seed) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_estimator_draw");
     if (count < 0) throw std::invalid_argument("estimator: count must be >= 0");
     if (kind != GCPB_EST_UNIFORM && kind != GCPB_EST_STRATIFIED)
       throw std::invalid_argument("unknown estimator kind");
@@ -3966,6 +3991,7 @@ int gcpb_estimator_get(gcpb_ctx* ctx, int64_t* idx_out, double* x_out, double* w
 
 int gcpb_estimate(gcpb_ctx* ctx, const gcpb_loss* loss, double* out) {
   return guard(ctx, [&] {
+    NvtxRange nvtx_("gcpb_estimate");
     validate_loss(loss);
     if (ctx->est_n == 0) {
       *out = 0.0;
