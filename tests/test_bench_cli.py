@@ -30,3 +30,24 @@ def test_gpus_without_torchrun_relaunches_and_fails_without_gpus():
     text = out.stdout + out.stderr
     assert "torch.distributed" in text or "needs 2 GPUs" in text
     assert '"n_gpus"' not in out.stdout  # no JSON line was printed
+
+
+def test_reference_arm_line_contract():
+    """`--impl reference` (the reference's own CPU code, oracle/_ref) prints one
+    JSON line with the arm's keys: same metric/unit/config as ours, impl,
+    cpu_baseline describing the run, e2e repeating the value with zero copies."""
+    import json
+    if not (ROOT / "oracle" / "_ref" / "libgcpref.so").exists():
+        import pytest
+        pytest.skip("oracle/_ref not built")
+    out = _run(["--impl", "reference", "--config", "c1", "--steps", "3", "--warmup", "3"], {})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["unit"] == "samples/s"
+    assert line["higher_is_better"] is True and line["steps"] == 3 and line["warmup"] == 3
+    assert line["config"]["workload"].startswith("C1")
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert line["e2e"] == {"value": line["value"], "unit": "samples/s",
+                           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert line["value"] > 0
