@@ -235,7 +235,8 @@ size_t dense_bytes(int storage, uint64_t n) {
 struct Tuning {
   int il = -1;          // GCPB_IL: interleaved [A | G] table (-1: by size)
   int sortq = -1;       // GCPB_SORTQ: unrestricted draws in mode-0 order (-1: with IL)
-  int qshift = 6;       // GCPB_QSHIFT: log2 mode-0 rows per ordering bin
+  int qshift = 5;       // GCPB_QSHIFT: log2 mode-0 rows per ordering bin (C5 step 3.64 / 3.66 /
+                        // 3.59 / 3.62 / 3.67 / 3.81 ms at 3 / 4 / 5 / 6 / 7 / 8)
   double hot_t = 256.0; // GCPB_HOT_T: reductions per address before a row is privatized
   int replicas = 0;     // GCPB_REPLICAS: forced gradient replica count (0: by load)
   bool no_small = false;  // GCPB_NO_SMALL: no one-launch small-problem path
@@ -1565,7 +1566,10 @@ __device__ __forceinline__ uint32_t sort_bin(const SortSpec& sp, uint64_t it, ui
 // Both passes keep kOrdIlp atomics in flight per thread: they are bound by the
 // L2 atomic round trip, and next to the fused kernel's pick half they get one
 // or two blocks per SM.
-constexpr int kOrdIlp = 8;
+#ifndef GCPB_ORD_ILP
+#define GCPB_ORD_ILP 8
+#endif
+constexpr int kOrdIlp = GCPB_ORD_ILP;
 __global__ void __launch_bounds__(256, 4) order_count_kernel(SortSpec sp, uint32_t* cnt) {
   const uint64_t it = sp.iter + (sp.iter_base ? *sp.iter_base : 0ull);
   const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -1713,7 +1717,7 @@ SortSpec order_spec(const gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int6
   sp.n = b1 - b0;
   sp.range = a.dims[0];
   sp.thr = a.thr[0];
-  sp.shift = c->tune.qshift;  // 64 mode-0 rows per bin by default
+  sp.shift = c->tune.qshift;  // 32 mode-0 rows per bin by default
   sp.chk = chk_counters();
   sp.nbins = order_bins(sp);
   return sp;
