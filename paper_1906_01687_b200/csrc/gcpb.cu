@@ -251,6 +251,9 @@ struct Tuning {
   int fused_bps2 = 3;
   int list_hot = 0;       // GCPB_LIST_HOT: hot-row copies also for the list segment's own launch
                           // (uniform rows: a hot row sees q / n_k reductions, no contention)
+  int ord_bps = 32;       // GCPB_ORD_BPS: blocks per SM of the ordering kernels' grids (short blocks
+                          // hand their SM slots to the pick launch sooner: C5 step 3.79 / 3.62 /
+                          // 3.61 / 3.59 / 3.57 / 3.56 / 3.56 ms at 1 / 2 / 4 / 8 / 16 / 32 / 64)
   int ord_side = 1;       // GCPB_ORD_SIDE: ordering on the side stream, under the pick half
   int side_bps = 3;       // GCPB_SIDE_BPS: fused blocks per SM of the pick launch while the side
                           // stream works (L2-resident tables; 0 = as many as fit; C3 step 235 / 228 /
@@ -260,6 +263,7 @@ struct Tuning {
     if (const char* e = getenv("GCPB_LIST_HOT")) list_hot = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ORD_SIDE")) ord_side = atoi(e);
+    if (const char* e = getenv("GCPB_ORD_BPS")) ord_bps = std::max(1, atoi(e));
     if (const char* e = getenv("GCPB_FUSED_BPS")) fused_bps = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_ADAM")) adam = atoi(e);
     if (const char* e = getenv("GCPB_IL")) il = atoi(e) != 0;
@@ -1693,7 +1697,7 @@ bool order_build(gcpb_ctx* c, OrderBufs& ob, const SortSpec& sp, cudaStream_t st
   uint32_t* cnt = ob.cnt.as<uint32_t>();
   uint32_t* cur = cnt + nbins;
   const int grid = static_cast<int>(std::max<int64_t>(
-      1, std::min<int64_t>((sp.n + 255) / 256, static_cast<int64_t>(c->num_sms) * 8)));
+      1, std::min<int64_t>((sp.n + 255) / 256, static_cast<int64_t>(c->num_sms) * c->tune.ord_bps)));
   CK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nbins) * sizeof(uint32_t), stream));
   order_count_kernel<<<grid, 256, 0, stream>>>(sp, cnt);
   CK(cudaGetLastError());
