@@ -379,7 +379,9 @@ int gcpb_set_shard(gcpb_ctx* ctx, int rank, int nranks);
 int gcpb_peer_handle(gcpb_ctx* ctx, void* out);
 int gcpb_peer_open(gcpb_ctx* ctx, const void* handles, int nranks);
 /* Unmaps the peers' tables: later sharded steps take the NCCL all-reduce +
- * replicated adam_step path again (used when a rank could not map a peer). */
+ * replicated adam_step path again (used when a rank could not map a peer).
+ * After peer steps each row's Adam moments exist only on its owner, so this
+ * is a usage error (std::logic_error) until gcpb_adam_reset. */
 int gcpb_peer_close(gcpb_ctx* ctx);
 int gcpb_allreduce_grad(gcpb_ctx* ctx);
 /* Host-callback communicator, an alternative to NCCL for process groups the

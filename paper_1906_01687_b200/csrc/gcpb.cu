@@ -309,6 +309,9 @@ struct gcpb_ctx {
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool join_pending = false;  // run_fused: wait for ev_join before the last segment
+  // peer steps keep each row's Adam moments on its owner only (ZeRO-1): set by
+  // peer_adam_launch, cleared by gcpb_adam_reset; gcpb_peer_close refuses while set
+  bool moments_sharded = false;
   std::string err;
 
   DBuf A, Gr, B, C, As, Bs, Cs;
@@ -2224,6 +2227,7 @@ void peer_adam_launch(gcpb_ctx* c, int advance_rng) {
               c->C.as<T>(), row0, row1, static_cast<int>(c->rp), cpr_shift,
               static_cast<int>(c->r), c->dst(), advance_rng));
   CK(cudaGetLastError());
+  c->moments_sharded = true;
   if (il) {
     c->a_stale = true;  // the factors live in the tables (AG)
     c->il_pending = false;
@@ -3485,6 +3489,7 @@ int gcpb_adam_reset(gcpb_ctx* ctx) {
     const int64_t zero = 0;
     CK(cudaMemcpyAsync(&ctx->dst()->t, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
     ctx->sync();
+    ctx->moments_sharded = false;
   });
 }
 
@@ -4153,6 +4158,10 @@ int gcpb_peer_open(gcpb_ctx* ctx, const void* handles, int nranks) {
 
 int gcpb_peer_close(gcpb_ctx* ctx) {
   return guard(ctx, [&] {
+    if (ctx->moments_sharded)
+      throw std::logic_error("peer close: the Adam moments are sharded over the ranks after peer "
+                             "steps (each row's moments live on its owner); call gcpb_adam_reset "
+                             "before returning to the replicated adam_step");
     ctx->sync();
     for (void* pmap : ctx->peer_ipc) cudaIpcCloseMemHandle(pmap);
     ctx->peer_ipc.clear();

@@ -221,3 +221,51 @@ def test_multirank_run_steps_with_host_communicator():
     for got in _run_ranks(2, rank_fn):
         for x, y in zip(got, want):
             assert O.rel_error(x, y) <= 1e-12
+
+
+def test_peer_close_returns_to_the_allreduce_path():
+    """gcpb_peer_close before any peer step: the ranks all-reduce the gradient
+    and run the replicated adam_step (the fallback bench.py takes when a rank
+    cannot map a peer), equal to single-rank stepping; after peer steps the
+    Adam moments are sharded over the ranks, so leaving the peer path is a
+    usage error until adam_reset."""
+    import paper_1906_01687_b200.gcp as G
+    dims, r, coords, vals, F = _skewed_problem(45)
+    sk, lf = G.SamplerKind.semi_stratified(1500, 2500), G.LossFunction.poisson()
+    single = G.Engine(dims, r, "f64")
+    single.set_sparse(coords, vals)
+    single.set_factors(F)
+    for it in range(3):
+        single.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+    want = single.factors()
+    nranks = 2
+    hub = Hub(nranks)
+    engines = [None] * nranks
+
+    def make(rank):
+        e = G.Engine(dims, r, "f64")
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.comm_init_host(rank, nranks, lambda v: hub.allgather(rank, v),
+                         lambda a: hub.allreduce(rank, a))
+        engines[rank] = e
+        return e.peer_handle()
+
+    handles = _run_ranks(nranks, make)
+
+    def run(rank):
+        e = engines[rank]
+        e.peer_open(handles)
+        e.peer_close()
+        for it in range(3):
+            e.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+        got = e.factors()
+        e.peer_open(handles)
+        e.step(sk, lf, 9, 3, 1e-2, lower_bound=0.0)
+        with pytest.raises(G.LogicError):
+            e.peer_close()
+        return got
+
+    for got in _run_ranks(nranks, run):
+        for x, y in zip(got, want):
+            assert O.rel_error(x, y) <= 1e-12
