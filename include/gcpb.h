@@ -380,8 +380,10 @@ int gcpb_peer_handle(gcpb_ctx* ctx, void* out);
 int gcpb_peer_open(gcpb_ctx* ctx, const void* handles, int nranks);
 /* Unmaps the peers' tables: later sharded steps take the NCCL all-reduce +
  * replicated adam_step path again (used when a rank could not map a peer).
- * After peer steps each row's Adam moments exist only on its owner, so this
- * is a usage error (std::logic_error) until gcpb_adam_reset. */
+ * After peer steps each row's Adam moments exist only on its owner (rows
+ * gcpb_shard_range(sum_k n_k, rank, nranks) of the concatenated modes;
+ * gcpb_get_moment is current for those rows only), so this is a usage error
+ * (std::logic_error) until gcpb_adam_reset. */
 int gcpb_peer_close(gcpb_ctx* ctx);
 int gcpb_allreduce_grad(gcpb_ctx* ctx);
 /* Host-callback communicator, an alternative to NCCL for process groups the
