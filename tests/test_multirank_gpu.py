@@ -269,3 +269,50 @@ def test_peer_close_returns_to_the_allreduce_path():
     for got in _run_ranks(nranks, run):
         for x, y in zip(got, want):
             assert O.rel_error(x, y) <= 1e-12
+
+
+@pytest.mark.parametrize("il", ["0", "1"])
+def test_peer_step_host_matches_single_rank(monkeypatch, il):
+    """gcpb_step_host on ranks in the peer path (what bench.py's e2e leg runs
+    at N > 1): every rank uploads the same host model, the sharded step runs
+    with the peer-memory exchange, every rank downloads the same updated
+    model -- equal to the single-rank host-model step."""
+    import paper_1906_01687_b200.gcp as G
+    monkeypatch.setenv("GCPB_IL", il)
+    dims, r, coords, vals, F = _skewed_problem(47)
+    sk, lf = G.SamplerKind.semi_stratified(1500, 2500), G.LossFunction.poisson()
+    flat0 = np.concatenate([f.ravel() for f in F])
+
+    def host_steps(e, n):
+        m_in, m_out = flat0.copy(), np.empty_like(flat0)
+        for it in range(n):
+            e.step_host(sk, lf, 9, it, 1e-2, m_in, m_out, lower_bound=0.0)
+            m_in, m_out = m_out, m_in
+        return m_in
+
+    single = G.Engine(dims, r, "f64")
+    single.set_sparse(coords, vals)
+    single.set_factors(F)
+    want = host_steps(single, 3)
+    nranks = 2
+    hub = Hub(nranks)
+    engines = [None] * nranks
+
+    def make(rank):
+        e = G.Engine(dims, r, "f64")
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.comm_init_host(rank, nranks, lambda v: hub.allgather(rank, v),
+                         lambda a: hub.allreduce(rank, a))
+        engines[rank] = e
+        return e.peer_handle()
+
+    handles = _run_ranks(nranks, make)
+
+    def run(rank):
+        e = engines[rank]
+        e.peer_open(handles)
+        return host_steps(e, 3)
+
+    for got in _run_ranks(nranks, run):
+        assert O.rel_error(got, want) <= 1e-12
