@@ -217,11 +217,11 @@ ROOFLINE_NOTES = {
           "launches per step -- the pick half, with the ordering of the unrestricted draws "
           "(counting sort by mode-0 row block) running under it on a side stream, then the "
           "unrestricted half walked in mode-0 row order (mode 0 swept instead of gathered); "
-          "kernel_ms spans both launches.  ncu DRAM traffic 327 B/sample (B_alg 396) at "
-          "3.7-3.8 TB/s per launch, long-scoreboard bound "
-          "(profiles/r02_c5_fused_picks.md, r02_c5_fused_list.md): the binding limit is the "
-          "random 128-byte-line access rate of HBM, not its streaming bandwidth "
-          "(tools/randbw.cu, profiles/r01_randbw.md)",
+          "kernel_ms spans both launches.  ncu DRAM traffic 295 B/sample (B_alg 396), "
+          "long-scoreboard bound (profiles/r02_c5_fused_picks.md, r02_c5_fused_list.md): the "
+          "binding limit is the rate of random DRAM accesses (3.6e10 L2 misses/s whatever the "
+          "request size), not streaming bandwidth (tools/fetchgran.cu, "
+          "profiles/r02_fetchgran.md)",
 }
 
 
@@ -500,16 +500,22 @@ def run_ours(args, w):
         # launch time (ncu times are cold and serialised; the bytes are not)
         roofline["traffic_frac"] = round(traffic / (fused_ms / 1e3) / 1e9 / peak_gbs, 4)
     if w.name == "c5" and traffic:
-        # Tables in HBM: the binding ceiling is the rate of random 128-byte-line
-        # accesses (fill + 64-byte write-back of the dirty gradient half),
-        # measured by tools/randbw.cu on the same mix without arithmetic
-        # (profiles/r01_randbw.md, "3g+3red il": 6.99e9 samples/s x 3 lines x 192 B)
-        roofline["binding"] = {"limit": "random 128-byte-line HBM access (row gather + reduction "
-                                        "mix, interleaved lines)",
-                               "achieved": round(traffic / (fused_ms / 1e3) / 1e9, 1),
-                               "peak": 4026.0, "unit": "GB/s of DRAM traffic",
-                               "frac": round(traffic / (fused_ms / 1e3) / 1e9 / 4026.0, 3),
-                               "source": "tools/randbw.cu microbenchmark, profiles/r01_randbw.md"}
+        # Tables in HBM: the binding ceiling is the rate of DRAM accesses -- L2
+        # line fills (one ~128-byte fetch per miss whatever the request size,
+        # tools/fetchgran.cu: 3.6e10 read misses/s) and write-backs of dirty
+        # gradient halves.  Ceiling for the fused kernel's mix of the two:
+        # tools/randbw.cu "3g+3red il" (row gather + reduction on interleaved
+        # lines, no arithmetic), 6.99e9 samples/s x 3 lines x (fill + write-back)
+        # = 4.19e10 accesses/s.  The access count per step comes from the ncu DRAM
+        # counters of the two fused launches (profiles/ncu_traffic_c5.json).
+        acc = json.loads(prof.read_text()).get("dram_accesses_per_launch")
+        if acc:
+            roofline["binding"] = {"limit": "DRAM accesses (L2 line fills + dirty-line write-backs)",
+                                   "achieved": float("%.4g" % (acc / (fused_ms / 1e3))),
+                                   "peak": 4.19e10, "unit": "accesses/s",
+                                   "frac": round(acc / (fused_ms / 1e3) / 4.19e10, 3),
+                                   "source": "tools/randbw.cu (profiles/r01_randbw.md) and "
+                                             "tools/fetchgran.cu (profiles/r02_fetchgran.md)"}
     if bound == "l2_red":
         # L2-resident factors: the binding ceiling is the L2 vector-reduction
         # rate, measured by tools/bulkred.cu (profiles/r01_bulkred.md: 6.4e7

@@ -225,7 +225,7 @@ __device__ __forceinline__ void phase_a(const FusedArgs<T>& a, const SegRegs& sg
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (q * 4 < a.rec_words) v = __ldg(rp + q);
+        if (q * 4 < a.rec_words) v = ld_record_u4(rp + q);
         wds[q * 4 + 0] = v.x;
         wds[q * 4 + 1] = v.y;
         wds[q * 4 + 2] = v.z;

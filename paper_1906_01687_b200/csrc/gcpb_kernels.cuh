@@ -354,6 +354,18 @@ __device__ __forceinline__ void red_chunk(double* p, const double (&v)[2]) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(v[1]) : "memory");
 }
 
+// One 16-byte word of a nonzero record at a random position of the record
+// table: read-only path, and a 64-byte L2 fetch instead of the default ~128
+// bytes per miss (tools/fetchgran.cu: same miss rate, half the DRAM bytes; a
+// neighbouring record is never wanted).
+__device__ __forceinline__ uint4 ld_record_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // Streaming loads of tensor data that should not displace factor rows in L1.
 __device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
   uint16_t v;
