@@ -66,6 +66,23 @@ void run(const char* name, const uint4* tab, int64_t bytes, uint32_t* sink, int 
          16 * LANES, bps, best, n / (best * 1e-3), n * 16.0 * LANES / (best * 1e-3) / 1e9);
 }
 int main(int argc, char** argv) {
+  if (argc > 1) {  // footprint sweep: fetchgran <GiB> [<GiB> ...] -- 16- and 64-byte loads only
+    uint32_t* sink;
+    cudaMalloc(&sink, 4);
+    for (int i = 1; i < argc; ++i) {
+      const int64_t bytes = static_cast<int64_t>(atof(argv[i]) * (1ll << 30)) / 4096 * 4096;
+      uint4* tab;
+      if (cudaMalloc(&tab, bytes) != cudaSuccess) { printf("cudaMalloc(%s GiB) failed\n", argv[i]); continue; }
+      cudaMemset(tab, 1, bytes);
+      printf("table %s GiB\n", argv[i]);
+      run<0, 1>("ld.nc", tab, bytes, sink, 4);
+      run<4, 1>("ld.L2::64B", tab, bytes, sink, 4);
+      run<0, 4>("ld.nc", tab, bytes, sink, 4);
+      run<0, 8>("ld.nc", tab, bytes, sink, 4);
+      cudaFree(tab);
+    }
+    return 0;
+  }
   const int64_t bytes = 8ll << 30;
   uint4* tab;
   uint32_t* sink;
