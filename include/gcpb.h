@@ -208,13 +208,24 @@ int gcpb_step(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
  * host KruskalModel): model_in (flattened factors, GradientSet order) is
  * copied in before the step and the updated factors copied out to model_out
  * after it (either may be NULL).  One call, one synchronisation; page-locked
- * buffers (cudaHostAlloc / cudaHostRegister) are DMA'd in place, pageable
+ * buffers (cudaHostAlloc / cudaHostRegister) are DMA'd in place (large models
+ * of fp32 engines: narrowed on the host, see gcpb_last_transfer_bytes), pageable
  * ones through the context's pinned staging block.  Small problems (those
  * gcpb_run_steps runs as one cluster kernel) on page-locked in/out buffers
  * take one launch that reads and writes the host model directly. */
 int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,
                    uint64_t seed, uint64_t iter, const gcpb_adam* adam, const double* model_in,
                    double* model_out);
+/* Model bytes the last gcpb_step_host moved over the bus in each direction.
+ * fp32 engines move large (>= 2^22 elements) page-locked fp64 models as fp32:
+ * host threads round chunk after chunk (round-to-nearest-even, the device's own
+ * conversion) into a pinned staging block while the DMA of the previous chunks
+ * runs, and widen the returned chunks the same way, so half the bytes cross
+ * PCIe and the result is bit-identical.  GCPB_NARROW=0 turns it off,
+ * GCPB_HOST_THREADS sets the thread count (default: all cores but two, at
+ * most 32).
+ * No reference counterpart (the reference's model never leaves the host). */
+int gcpb_last_transfer_bytes(const gcpb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* n iterations iter0 .. iter0+n-1 replayed as one CUDA graph (captured once per
  * sampler/loss/seed/n configuration; the draw-stream iteration and Adam's
  * counter advance on the device).  Equivalent to n calls of gcpb_step.  For

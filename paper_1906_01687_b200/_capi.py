@@ -129,6 +129,7 @@ SIGNATURES = [
     ("gcpb_synchronize", C.c_int, [ctx_p]),
     ("gcpb_steps_path", C.c_int, [ctx_p]),
     ("gcpb_run_steps_launches", C.c_int, [ctx_p, C.POINTER(C.c_int64)]),
+    ("gcpb_last_transfer_bytes", C.c_int, [ctx_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("gcpb_debug_guard_failures", C.c_int64, [C.POINTER(C.c_int64)]),
     ("gcpb_debug_check_failures", C.c_int64, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("gcpb_hot_rows", C.c_int, [ctx_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

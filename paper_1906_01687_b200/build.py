@@ -32,7 +32,7 @@ NVFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
     "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
 ]
-SOURCES = ["gcpb.cu", "gcpb_fused_f32.cu", "gcpb_fused_f64.cu", "gcpb_io.cpp"]
+SOURCES = ["gcpb.cu", "gcpb_fused_f32.cu", "gcpb_fused_f64.cu", "gcpb_io.cpp", "gcpb_host.cpp"]
 _FUSED_DEPS = ["philox.cuh", "gcpb_kernels.cuh", "gcpb_fused.cuh"]
 DEPS = {
     "gcpb.cu": ["philox.cuh", "gcpb_kernels.cuh", "gcpb_aux.cuh", "gcpb_gen.cuh",
@@ -40,6 +40,7 @@ DEPS = {
     "gcpb_fused_f32.cu": _FUSED_DEPS,
     "gcpb_fused_f64.cu": _FUSED_DEPS,
     "gcpb_io.cpp": [],
+    "gcpb_host.cpp": [],
 }
 
 

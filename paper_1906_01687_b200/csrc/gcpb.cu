@@ -23,6 +23,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gcpb.h"
@@ -31,6 +32,11 @@
 #include "gcpb_small.cuh"
 #include "gcpb_kernels.cuh"
 #include "rngstream.h"
+
+namespace gcpb {  // gcpb_host.cpp
+void narrow_f64_f32(const double* src, float* dst, size_t n);
+void widen_f32_f64(const float* src, double* dst, size_t n);
+}  // namespace gcpb
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -258,7 +264,13 @@ struct Tuning {
   int side_bps = 3;       // GCPB_SIDE_BPS: fused blocks per SM of the pick launch while the side
                           // stream works (L2-resident tables; 0 = as many as fit; C3 step 235 / 228 /
                           // 253 / 342 us at 0 / 3 / 2 / 1)
+  int host_threads = 0;   // GCPB_HOST_THREADS: threads of the narrowed model transfer (0 = all cores
+                          // but two, at most 32)
+  int narrow = 1;         // GCPB_NARROW: fp32 engines move large page-locked fp64 models as fp32,
+                          // rounded / widened on the host while the DMA runs (0 = fp64 over the bus)
   void read_env() {
+    if (const char* e = getenv("GCPB_HOST_THREADS")) host_threads = std::max(0, atoi(e));
+    if (const char* e = getenv("GCPB_NARROW")) narrow = atoi(e);
     if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_LIST_HOT")) list_hot = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = std::max(0, atoi(e));
@@ -429,6 +441,12 @@ struct gcpb_ctx {
   int64_t graph_kernels = 0;  // kernel nodes of the cached step graph
   DBuf xfer_dev;
   cudaEvent_t xfer_done = nullptr;
+  // narrowed transfers (fp32 engines, page-locked host buffers, large models):
+  // pinned fp32 staging, one event per chunk, bytes moved by the last transfer
+  float* x32_host = nullptr;
+  size_t x32_cap = 0;
+  std::vector<cudaEvent_t> x32_ev;
+  int64_t last_h2d_bytes = 0, last_d2h_bytes = 0;
 
   ~gcpb_ctx() {
     for (auto& pr : tevents) {
@@ -445,6 +463,11 @@ struct gcpb_ctx {
       cudaFreeHost(xfer_host);
     }
     if (xfer_done) cudaEventDestroy(xfer_done);
+    if (x32_host) {
+      cudaStreamSynchronize(stream);
+      cudaFreeHost(x32_host);
+    }
+    for (cudaEvent_t e : x32_ev) cudaEventDestroy(e);
     for (void* pmap : peer_ipc) cudaIpcCloseMemHandle(pmap);
     if (comm) ncclCommDestroy(comm);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -594,12 +617,152 @@ void a_current(gcpb_ctx* c) {
   c->a_stale = false;
 }
 
+// ---- narrowed model transfers (host halves in gcpb_host.cpp) -----------------------
+
+constexpr size_t kNarrowChunk = size_t{1} << 19;  // elements per chunk (2 MB of fp32: short pipeline
+                                                  // fill and drain, still full-rate DMAs)
+constexpr size_t kNarrowMin = size_t{1} << 22;    // smaller transfers go as fp64 in one copy
+
+bool narrow_eligible(const gcpb_ctx* c, size_t n, bool direct) {
+  return direct && c->tune.narrow != 0 && c->dtype == GCPB_F32 && n >= kNarrowMin;
+}
+
+int narrow_threads(const gcpb_ctx* c, size_t nchunks) {
+  // default: all cores but two (the calling thread queues the DMAs; C5 on 16
+  // cores: 41.9 / 38.8 / 34.3 / 33.2 / 31.8 / 32.7 / 33.7 ms per host-buffer step
+  // at 6 / 8 / 10 / 12 / 14 / 15 / 16 threads, 44.4 ms with fp64 over the bus)
+  int t = c->tune.host_threads > 0 ? c->tune.host_threads
+                                   : static_cast<int>(std::thread::hardware_concurrency()) - 2;
+  t = std::max(1, std::min(t, 32));
+  return static_cast<int>(std::min<size_t>(static_cast<size_t>(t), nchunks));
+}
+
+void narrow_reserve(gcpb_ctx* c, size_t n, size_t nchunks, bool dev_stage) {
+  if (!c->xfer_done) CK(cudaEventCreateWithFlags(&c->xfer_done, cudaEventDisableTiming));
+  if (n > c->x32_cap) {
+    if (c->x32_host) {
+      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaFreeHost(c->x32_host));
+      c->x32_host = nullptr;
+    }
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->x32_host), n * sizeof(float)));
+    c->x32_cap = n;
+  }
+  while (c->x32_ev.size() < nchunks) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->x32_ev.push_back(e);
+  }
+  if (dev_stage) c->xfer_dev.alloc(n * sizeof(float));
+}
+
+// Host fp64 rows -> device fp32 rows: worker threads round chunk after chunk
+// into the pinned fp32 staging block, the calling thread queues each chunk's
+// DMA as soon as it is ready.  Unpadded rows (r == rp) land in the table itself.
+void upload_narrow(gcpb_ctx* c, DBuf& buf, int k0, int64_t rows, const double* values) {
+  const size_t n = static_cast<size_t>(rows * c->r);
+  const size_t nchunks = (n + kNarrowChunk - 1) / kNarrowChunk;
+  const bool padded = c->rp != c->r;
+  narrow_reserve(c, n, nchunks, padded);
+  CK(cudaEventSynchronize(c->xfer_done));  // the previous transfer left the staging block
+  float* dev = padded ? c->xfer_dev.as<float>() : buf.as<float>() + c->off[k0];
+  const int nt = narrow_threads(c, nchunks);
+  std::unique_ptr<std::atomic<int>[]> ready(new std::atomic<int>[nchunks]);
+  for (size_t i = 0; i < nchunks; ++i) ready[i].store(0, std::memory_order_relaxed);
+  float* stage = c->x32_host;
+  std::vector<std::thread> pool;
+  pool.reserve(static_cast<size_t>(nt));
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([=, &ready] {
+      for (size_t ch = static_cast<size_t>(t); ch < nchunks; ch += static_cast<size_t>(nt)) {
+        const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
+        gcpb::narrow_f64_f32(values + b, stage + b, e - b);
+        ready[ch].store(1, std::memory_order_release);
+      }
+    });
+  cudaError_t err = cudaSuccess;
+  for (size_t ch = 0; ch < nchunks; ++ch) {
+    while (!ready[ch].load(std::memory_order_acquire))  // leave the cores to the workers
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(dev + b, stage + b, (e - b) * sizeof(float), cudaMemcpyHostToDevice,
+                            c->stream);
+  }
+  for (auto& th : pool) th.join();
+  CK(err);
+  CK(cudaEventRecord(c->xfer_done, c->stream));
+  if (padded) {
+    const int64_t total = rows * c->rp;
+    unpack_rows_kernel<float, float><<<grid_for(total, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+        c->xfer_dev.as<float>(), buf.as<float>() + c->off[k0], total, static_cast<int>(c->r),
+        static_cast<int>(c->rp));
+    CK(cudaGetLastError());
+  }
+  c->last_h2d_bytes += static_cast<int64_t>(n * sizeof(float));
+}
+
+// Device fp32 rows -> host fp64 rows: the chunks' DMAs are queued with an event
+// each; worker threads widen a chunk into the caller's buffer once its event has
+// passed.  Returns with the stream idle.
+void download_narrow(gcpb_ctx* c, const DBuf& buf, int k0, int64_t rows, double* out) {
+  const size_t n = static_cast<size_t>(rows * c->r);
+  const size_t nchunks = (n + kNarrowChunk - 1) / kNarrowChunk;
+  const bool padded = c->rp != c->r;
+  narrow_reserve(c, n, nchunks, padded);
+  CK(cudaEventSynchronize(c->xfer_done));
+  const float* dev = buf.as<float>() + c->off[k0];
+  if (padded) {
+    pack_rows_kernel<float, float><<<grid_for(static_cast<int64_t>(n), 256, c->num_sms, 8), 256, 0,
+                                     c->stream>>>(buf.as<float>() + c->off[k0],
+                                                  c->xfer_dev.as<float>(), static_cast<int64_t>(n),
+                                                  static_cast<int>(c->r), static_cast<int>(c->rp));
+    CK(cudaGetLastError());
+    dev = c->xfer_dev.as<float>();
+  }
+  float* stage = c->x32_host;
+  for (size_t ch = 0; ch < nchunks; ++ch) {
+    const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
+    CK(cudaMemcpyAsync(stage + b, dev + b, (e - b) * sizeof(float), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaEventRecord(c->x32_ev[ch], c->stream));
+  }
+  CK(cudaEventRecord(c->xfer_done, c->stream));
+  const int nt = narrow_threads(c, nchunks);
+  std::atomic<int> failed{0};
+  const int device = c->device;
+  cudaEvent_t* evs = c->x32_ev.data();
+  std::vector<std::thread> pool;
+  pool.reserve(static_cast<size_t>(nt));
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([=, &failed] {
+      cudaSetDevice(device);
+      for (size_t ch = static_cast<size_t>(t); ch < nchunks; ch += static_cast<size_t>(nt)) {
+        if (cudaEventSynchronize(evs[ch]) != cudaSuccess) {
+          failed.store(1);
+          return;
+        }
+        const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
+        gcpb::widen_f32_f64(stage + b, out + b, e - b);
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (failed.load()) CK(cudaStreamSynchronize(c->stream));  // surfaces the stream's error
+  CK(cudaEventSynchronize(c->xfer_done));
+  c->last_d2h_bytes += static_cast<int64_t>(n * sizeof(float));
+}
+
 template <typename T>
 void upload_modes(gcpb_ctx* c, DBuf& buf, int mode, const double* values, bool direct = false) {
   int k0, k1;
   int64_t rows;
   mode_rows(c, mode, &k0, &k1, &rows);
   const size_t n = static_cast<size_t>(rows * c->r);
+  if (narrow_eligible(c, n, direct)) {
+    upload_narrow(c, buf, k0, rows, values);
+    return;
+  }
+  c->last_h2d_bytes += static_cast<int64_t>(n * sizeof(double));
   xfer_reserve(c, n);
   if (direct) {
     CK(cudaMemcpyAsync(c->xfer_dev.p, values, n * sizeof(double), cudaMemcpyHostToDevice,
@@ -624,6 +787,11 @@ void download_modes(gcpb_ctx* c, const DBuf& buf, int mode, double* out, bool di
   int64_t rows;
   mode_rows(c, mode, &k0, &k1, &rows);
   const size_t n = static_cast<size_t>(rows * c->r);
+  if (narrow_eligible(c, n, direct)) {
+    download_narrow(c, buf, k0, rows, out);
+    return;
+  }
+  c->last_d2h_bytes += static_cast<int64_t>(n * sizeof(double));
   xfer_reserve(c, n);
   CK(cudaEventSynchronize(c->xfer_done));
   pack_rows_kernel<T><<<grid_for(static_cast<int64_t>(n), 256, c->num_sms, 8), 256, 0, c->stream>>>(
@@ -3550,6 +3718,7 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
     }
     // pinned buffers are transferred in place: the call synchronises on the
     // download before returning (without model_out, on the stream)
+    ctx->last_h2d_bytes = ctx->last_d2h_bytes = 0;
     if (model_in) upload(ctx, ctx->A, -1, model_in, is_pinned(model_in));
     set_adam_params(ctx, adam);
     ensure_grad_zero(ctx);
@@ -3562,6 +3731,13 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
     else if (model_in)
       CK(cudaStreamSynchronize(ctx->stream));
   });
+}
+
+int gcpb_last_transfer_bytes(const gcpb_ctx* ctx, int64_t* h2d, int64_t* d2h) {
+  if (!ctx || !h2d || !d2h) return GCPB_ERR_USAGE;
+  *h2d = ctx->last_h2d_bytes;
+  *d2h = ctx->last_d2h_bytes;
+  return GCPB_OK;
 }
 
 int gcpb_run_steps(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* loss,

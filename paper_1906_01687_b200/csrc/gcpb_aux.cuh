@@ -1528,8 +1528,8 @@ __global__ void domain_scan_kernel(const V* __restrict__ v, int64_t n, unsigned*
 
 // Factor transfers: unpadded fp64 rows <-> padded device rows (padding
 // columns written as zero, so the "padding stays zero" invariant holds).
-template <typename T>
-__global__ void unpack_rows_kernel(const double* __restrict__ src, T* __restrict__ dst,
+template <typename T, typename S = double>
+__global__ void unpack_rows_kernel(const S* __restrict__ src, T* __restrict__ dst,
                                    int64_t total, int r, int rp) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1539,13 +1539,13 @@ __global__ void unpack_rows_kernel(const double* __restrict__ src, T* __restrict
   }
 }
 
-template <typename T>
-__global__ void pack_rows_kernel(const T* __restrict__ src, double* __restrict__ dst, int64_t n,
+template <typename T, typename S = double>
+__global__ void pack_rows_kernel(const T* __restrict__ src, S* __restrict__ dst, int64_t n,
                                  int r, int rp) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t row = i / r;
-    dst[i] = static_cast<double>(src[row * rp + (i - row * r)]);
+    dst[i] = static_cast<S>(src[row * rp + (i - row * r)]);
   }
 }
 

@@ -515,6 +515,13 @@ class Engine:
         self._ck(lib.gcpb_run_steps_launches(self._h, C.byref(n)))
         return int(n.value)
 
+    def last_transfer_bytes(self) -> tuple:
+        """(h2d, d2h) model bytes the last step_host moved over the bus (fp32
+        engines narrow large page-locked fp64 models on the host)."""
+        a, b = C.c_int64(), C.c_int64()
+        self._ck(lib.gcpb_last_transfer_bytes(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
     @property
     def hot_rows(self) -> tuple:
         """(hot rows selected, copies per hot row used by the last scatter)."""
