@@ -367,34 +367,29 @@ __device__ __forceinline__ uint4 ld_record_u4(const uint4* p) {
 }
 
 // Streaming loads of tensor data that should not displace factor rows in L1.
-#ifdef GCPB_STREAM_ALLOC
-#define GCPB_LDS "ld.global.nc.L2::64B"
-#else
-#define GCPB_LDS "ld.global.nc.L1::no_allocate"
-#endif
 __device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
   uint16_t v;
-  asm volatile(GCPB_LDS ".u8 %0, [%1];" : "=h"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile(GCPB_LDS ".u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ float ld_stream_f32(const float* p) {
   float v;
-  asm volatile(GCPB_LDS ".f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ld_stream_f64(const double* p) {
   double v;
-  asm volatile(GCPB_LDS ".f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const uint64_t* p) {
   ulonglong2 v;
-  asm volatile(GCPB_LDS ".v2.u64 {%0, %1}, [%2];"
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];"
                : "=l"(v.x), "=l"(v.y)
                : "l"(p));
   return v;
