@@ -672,14 +672,19 @@ void upload_narrow(gcpb_ctx* c, DBuf& buf, int k0, int64_t rows, const double* v
   float* stage = c->x32_host;
   std::vector<std::thread> pool;
   pool.reserve(static_cast<size_t>(nt));
-  for (int t = 0; t < nt; ++t)
-    pool.emplace_back([=, &ready] {
-      for (size_t ch = static_cast<size_t>(t); ch < nchunks; ch += static_cast<size_t>(nt)) {
-        const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
-        gcpb::narrow_f64_f32(values + b, stage + b, e - b);
-        ready[ch].store(1, std::memory_order_release);
-      }
-    });
+  try {
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([=, &ready] {
+        for (size_t ch = static_cast<size_t>(t); ch < nchunks; ch += static_cast<size_t>(nt)) {
+          const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
+          gcpb::narrow_f64_f32(values + b, stage + b, e - b);
+          ready[ch].store(1, std::memory_order_release);
+        }
+      });
+  } catch (...) {  // a thread could not be started: its chunks would never arrive
+    for (auto& th : pool) th.join();
+    throw;
+  }
   cudaError_t err = cudaSuccess;
   for (size_t ch = 0; ch < nchunks; ++ch) {
     while (!ready[ch].load(std::memory_order_acquire))  // leave the cores to the workers
@@ -734,18 +739,24 @@ void download_narrow(gcpb_ctx* c, const DBuf& buf, int k0, int64_t rows, double*
   cudaEvent_t* evs = c->x32_ev.data();
   std::vector<std::thread> pool;
   pool.reserve(static_cast<size_t>(nt));
-  for (int t = 0; t < nt; ++t)
-    pool.emplace_back([=, &failed] {
-      cudaSetDevice(device);
-      for (size_t ch = static_cast<size_t>(t); ch < nchunks; ch += static_cast<size_t>(nt)) {
-        if (cudaEventSynchronize(evs[ch]) != cudaSuccess) {
-          failed.store(1);
-          return;
+  try {
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([=, &failed] {
+        cudaSetDevice(device);
+        for (size_t ch = static_cast<size_t>(t); ch < nchunks; ch += static_cast<size_t>(nt)) {
+          if (cudaEventSynchronize(evs[ch]) != cudaSuccess) {
+            failed.store(1);
+            return;
+          }
+          const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
+          gcpb::widen_f32_f64(stage + b, out + b, e - b);
         }
-        const size_t b = ch * kNarrowChunk, e = std::min(n, b + kNarrowChunk);
-        gcpb::widen_f32_f64(stage + b, out + b, e - b);
-      }
-    });
+      });
+  } catch (...) {
+    for (auto& th : pool) th.join();
+    cudaStreamSynchronize(c->stream);  // the staging block is still a DMA target
+    throw;
+  }
   for (auto& th : pool) th.join();
   if (failed.load()) CK(cudaStreamSynchronize(c->stream));  // surfaces the stream's error
   CK(cudaEventSynchronize(c->xfer_done));
