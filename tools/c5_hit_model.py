@@ -10,22 +10,15 @@ from paper_1906_01687_b200 import workloads as WL
 w = WL.get("c5")
 keys, vals = WL.c5_device_data(w)
 del vals
-k = keys.bitwise_xor(torch.tensor(-(2 ** 63), dtype=torch.int64, device=keys.device)) if False else keys
-# keys: u64 linear keys stored as int64 bit patterns (first mode fastest)
+k = keys  # u64 linear keys as int64 bit patterns (first mode fastest; N > 2^63 for C5)
 ps = []
-rem = k.clone()
+rem = k
 n0, n1, n2 = w.dims
-# u64 arithmetic on int64 bit patterns: N < 2^64 but > 2^63, so use float-free split by strides
-# key = i0 + n0*(i1 + n1*i2); i2 = key // (n0*n1) needs unsigned division: do it on the high/low halves
 s01 = n0 * n1
 hi = (rem >> 32) & 0xFFFFFFFF
 lo = rem & 0xFFFFFFFF
-# unsigned key as double-double is overkill; use python ints on a sample? no: exact torch path:
-# q = floor(key / s01) with key = hi*2^32 + lo (both < 2^32, nonnegative)
-q_hi, r_hi = hi // s01, hi % s01          # hi = q_hi*s01 + r_hi  (s01 ~ 8.2e12 > 2^32, so q_hi = 0)
-t = r_hi * (1 << 32) + lo                  # < s01*2^32 ~ 3.5e22: overflows int64 -> split again
-del q_hi, t
-# simpler: i2 from the top bits via float64 estimate, then correct exactly with wrapped int64 arithmetic
+# i2 = key // (n0 * n1) as an unsigned division: a float64 estimate from the two halves,
+# corrected exactly with wrapped int64 arithmetic
 kd = hi.to(torch.float64) * 4294967296.0 + lo.to(torch.float64)
 i2 = torch.floor(kd / float(s01)).to(torch.int64)
 r = rem - i2 * s01                          # wraps mod 2^64 consistently -> exact remainder +- s01
