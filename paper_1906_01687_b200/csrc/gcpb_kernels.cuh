@@ -355,12 +355,14 @@ __device__ __forceinline__ void red_chunk(double* p, const double (&v)[2]) {
 }
 
 // One 16-byte word of a nonzero record at a random position of the record
-// table: read-only path, and a 64-byte L2 fetch instead of the default ~128
-// bytes per miss (tools/fetchgran.cu: same miss rate, half the DRAM bytes; a
-// neighbouring record is never wanted).
+// table: a 64-byte L2 fetch instead of the default ~128 bytes per miss
+// (tools/fetchgran.cu: same miss rate, half the DRAM bytes; a neighbouring
+// record is never wanted), evict-first in L1 and L2 (.cs: a record is used
+// once; C5 step 3.548 -> 3.540 ms; .cv, .lu and evict-first cache policies
+// measured no better than plain .nc).
 __device__ __forceinline__ uint4 ld_record_u4(const uint4* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.cs.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
