@@ -223,7 +223,8 @@ int gcpb_step_host(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss* 
  * runs, and widen the returned chunks the same way, so half the bytes cross
  * PCIe and the result is bit-identical.  GCPB_NARROW=0 turns it off,
  * GCPB_HOST_THREADS sets the thread count (default: all cores but two, at
- * most 32).
+ * most 32), GCPB_NARROW_TAIL the percentage of an upload's rows that cross as
+ * fp64 without a host pass (default 15: the host's rounding is the longer leg).
  * No reference counterpart (the reference's model never leaves the host). */
 int gcpb_last_transfer_bytes(const gcpb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* n iterations iter0 .. iter0+n-1 replayed as one CUDA graph (captured once per

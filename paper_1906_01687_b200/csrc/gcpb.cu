@@ -266,11 +266,14 @@ struct Tuning {
                           // 253 / 342 us at 0 / 3 / 2 / 1)
   int host_threads = 0;   // GCPB_HOST_THREADS: threads of the narrowed model transfer (0 = all cores
                           // but two, at most 32)
+  int narrow_tail = 15;   // GCPB_NARROW_TAIL: percent of a narrowed upload's rows (the last ones) that
+                          // cross as fp64 without a host pass
   int narrow = 1;         // GCPB_NARROW: fp32 engines move large page-locked fp64 models as fp32,
                           // rounded / widened on the host while the DMA runs (0 = fp64 over the bus)
   void read_env() {
     if (const char* e = getenv("GCPB_HOST_THREADS")) host_threads = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_NARROW")) narrow = atoi(e);
+    if (const char* e = getenv("GCPB_NARROW_TAIL")) narrow_tail = atoi(e);
     if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_LIST_HOT")) list_hot = atoi(e);
     if (const char* e = getenv("GCPB_FUSED_BPS2")) fused_bps2 = std::max(0, atoi(e));
@@ -637,35 +640,58 @@ int narrow_threads(const gcpb_ctx* c, size_t nchunks) {
   return static_cast<int>(std::min<size_t>(static_cast<size_t>(t), nchunks));
 }
 
-void narrow_reserve(gcpb_ctx* c, size_t n, size_t nchunks, bool dev_stage) {
+// Staging for a transfer whose first n_head elements cross as fp32 and whose
+// last n_tail elements cross as fp64: pinned fp32 block of n_head, one event
+// per chunk, and a device block holding the fp64 tail followed (padded rows
+// only) by the fp32 head.
+void narrow_reserve(gcpb_ctx* c, size_t n_head, size_t n_tail, size_t nchunks, bool padded) {
   if (!c->xfer_done) CK(cudaEventCreateWithFlags(&c->xfer_done, cudaEventDisableTiming));
-  if (n > c->x32_cap) {
+  if (n_head > c->x32_cap) {
     if (c->x32_host) {
       CK(cudaStreamSynchronize(c->stream));
       CK(cudaFreeHost(c->x32_host));
       c->x32_host = nullptr;
     }
-    CK(cudaMallocHost(reinterpret_cast<void**>(&c->x32_host), n * sizeof(float)));
-    c->x32_cap = n;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->x32_host), n_head * sizeof(float)));
+    c->x32_cap = n_head;
   }
   while (c->x32_ev.size() < nchunks) {
     cudaEvent_t e;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->x32_ev.push_back(e);
   }
-  if (dev_stage) c->xfer_dev.alloc(n * sizeof(float));
+  const size_t bytes = n_tail * sizeof(double) + (padded ? n_head * sizeof(float) : 0);
+  if (bytes) c->xfer_dev.alloc(bytes);
 }
 
-// Host fp64 rows -> device fp32 rows: worker threads round chunk after chunk
-// into the pinned fp32 staging block, the calling thread queues each chunk's
-// DMA as soon as it is ready.  Unpadded rows (r == rp) land in the table itself.
+// Rows that cross as fp64 without a host pass (the last rows of the transfer):
+// the host's rounding, not the DMA, is the longer leg of a narrowed transfer, so
+// a share of the rows goes the old way while the workers handle the rest.
+// Measured on C5 (16 cores, tools/xfer_probe.py): copy-in leg 15.8 / 13.4 / 14.7 ms
+// at 0 / 15 / 30 % (19.9 ms all fp64); the copy-out leg does not gain (12.7 / 13.5 /
+// 14.4 ms, 19.2 ms all fp64), so only uploads take a tail.
+int64_t narrow_tail_rows(const gcpb_ctx* c, int64_t rows, bool upload) {
+  if (!upload) return 0;
+  return rows * std::max(0, std::min(90, c->tune.narrow_tail)) / 100;
+}
+
+// Host fp64 rows -> device fp32 rows.  Head rows: worker threads round chunk
+// after chunk into the pinned fp32 staging block, the calling thread queues each
+// chunk's DMA as soon as it is ready (unpadded rows, r == rp, land in the table
+// itself).  Tail rows: one fp64 DMA, queued first so the bus is busy while the
+// first chunks are being rounded, converted by the unpack kernel.
 void upload_narrow(gcpb_ctx* c, DBuf& buf, int k0, int64_t rows, const double* values) {
-  const size_t n = static_cast<size_t>(rows * c->r);
+  const int64_t rows_tail = narrow_tail_rows(c, rows, true), rows_head = rows - rows_tail;
+  const size_t n = static_cast<size_t>(rows_head * c->r);       // head elements
+  const size_t n_tail = static_cast<size_t>(rows_tail * c->r);
   const size_t nchunks = (n + kNarrowChunk - 1) / kNarrowChunk;
   const bool padded = c->rp != c->r;
-  narrow_reserve(c, n, nchunks, padded);
+  narrow_reserve(c, n, n_tail, nchunks, padded);
   CK(cudaEventSynchronize(c->xfer_done));  // the previous transfer left the staging block
-  float* dev = padded ? c->xfer_dev.as<float>() : buf.as<float>() + c->off[k0];
+  double* dev_tail = c->xfer_dev.as<double>();
+  float* dev_head = reinterpret_cast<float*>(dev_tail + n_tail);  // padded rows only
+  float* table = buf.as<float>() + c->off[k0];
+  float* dev = padded ? dev_head : table;
   const int nt = narrow_threads(c, nchunks);
   std::unique_ptr<std::atomic<int>[]> ready(new std::atomic<int>[nchunks]);
   for (size_t i = 0; i < nchunks; ++i) ready[i].store(0, std::memory_order_relaxed);
@@ -686,6 +712,17 @@ void upload_narrow(gcpb_ctx* c, DBuf& buf, int k0, int64_t rows, const double* v
     throw;
   }
   cudaError_t err = cudaSuccess;
+  if (n_tail) {
+    err = cudaMemcpyAsync(dev_tail, values + n, n_tail * sizeof(double), cudaMemcpyHostToDevice,
+                          c->stream);
+    if (err == cudaSuccess) {
+      const int64_t total = rows_tail * c->rp;
+      unpack_rows_kernel<float, double><<<grid_for(total, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+          dev_tail, table + rows_head * c->rp, total, static_cast<int>(c->r),
+          static_cast<int>(c->rp));
+      err = cudaGetLastError();
+    }
+  }
   for (size_t ch = 0; ch < nchunks; ++ch) {
     while (!ready[ch].load(std::memory_order_acquire))  // leave the cores to the workers
       std::this_thread::sleep_for(std::chrono::microseconds(20));
@@ -697,33 +734,38 @@ void upload_narrow(gcpb_ctx* c, DBuf& buf, int k0, int64_t rows, const double* v
   for (auto& th : pool) th.join();
   CK(err);
   CK(cudaEventRecord(c->xfer_done, c->stream));
-  if (padded) {
-    const int64_t total = rows * c->rp;
+  if (padded && rows_head > 0) {
+    const int64_t total = rows_head * c->rp;
     unpack_rows_kernel<float, float><<<grid_for(total, 256, c->num_sms, 8), 256, 0, c->stream>>>(
-        c->xfer_dev.as<float>(), buf.as<float>() + c->off[k0], total, static_cast<int>(c->r),
-        static_cast<int>(c->rp));
+        dev_head, table, total, static_cast<int>(c->r), static_cast<int>(c->rp));
     CK(cudaGetLastError());
   }
-  c->last_h2d_bytes += static_cast<int64_t>(n * sizeof(float));
+  c->last_h2d_bytes += static_cast<int64_t>(n * sizeof(float) + n_tail * sizeof(double));
 }
 
-// Device fp32 rows -> host fp64 rows: the chunks' DMAs are queued with an event
-// each; worker threads widen a chunk into the caller's buffer once its event has
-// passed.  Returns with the stream idle.
+// Device fp32 rows -> host fp64 rows.  Head rows: the chunks' DMAs are queued
+// with an event each; worker threads widen a chunk into the caller's buffer once
+// its event has passed.  Tail rows: widened on the device and copied as fp64
+// straight into the caller's buffer, queued last (no host pass waits on them).
+// Returns with the stream idle.
 void download_narrow(gcpb_ctx* c, const DBuf& buf, int k0, int64_t rows, double* out) {
-  const size_t n = static_cast<size_t>(rows * c->r);
+  const int64_t rows_tail = narrow_tail_rows(c, rows, false), rows_head = rows - rows_tail;
+  const size_t n = static_cast<size_t>(rows_head * c->r);
+  const size_t n_tail = static_cast<size_t>(rows_tail * c->r);
   const size_t nchunks = (n + kNarrowChunk - 1) / kNarrowChunk;
   const bool padded = c->rp != c->r;
-  narrow_reserve(c, n, nchunks, padded);
+  narrow_reserve(c, n, n_tail, nchunks, padded);
   CK(cudaEventSynchronize(c->xfer_done));
-  const float* dev = buf.as<float>() + c->off[k0];
-  if (padded) {
+  double* dev_tail = c->xfer_dev.as<double>();
+  float* dev_head = reinterpret_cast<float*>(dev_tail + n_tail);
+  const float* table = buf.as<float>() + c->off[k0];
+  const float* dev = table;
+  if (padded && rows_head > 0) {
     pack_rows_kernel<float, float><<<grid_for(static_cast<int64_t>(n), 256, c->num_sms, 8), 256, 0,
-                                     c->stream>>>(buf.as<float>() + c->off[k0],
-                                                  c->xfer_dev.as<float>(), static_cast<int64_t>(n),
+                                     c->stream>>>(table, dev_head, static_cast<int64_t>(n),
                                                   static_cast<int>(c->r), static_cast<int>(c->rp));
     CK(cudaGetLastError());
-    dev = c->xfer_dev.as<float>();
+    dev = dev_head;
   }
   float* stage = c->x32_host;
   for (size_t ch = 0; ch < nchunks; ++ch) {
@@ -731,6 +773,15 @@ void download_narrow(gcpb_ctx* c, const DBuf& buf, int k0, int64_t rows, double*
     CK(cudaMemcpyAsync(stage + b, dev + b, (e - b) * sizeof(float), cudaMemcpyDeviceToHost,
                        c->stream));
     CK(cudaEventRecord(c->x32_ev[ch], c->stream));
+  }
+  if (n_tail) {
+    pack_rows_kernel<float, double><<<grid_for(static_cast<int64_t>(n_tail), 256, c->num_sms, 8),
+                                      256, 0, c->stream>>>(
+        table + rows_head * c->rp, dev_tail, static_cast<int64_t>(n_tail), static_cast<int>(c->r),
+        static_cast<int>(c->rp));
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out + n, dev_tail, n_tail * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
   }
   CK(cudaEventRecord(c->xfer_done, c->stream));
   const int nt = narrow_threads(c, nchunks);
@@ -760,7 +811,7 @@ void download_narrow(gcpb_ctx* c, const DBuf& buf, int k0, int64_t rows, double*
   for (auto& th : pool) th.join();
   if (failed.load()) CK(cudaStreamSynchronize(c->stream));  // surfaces the stream's error
   CK(cudaEventSynchronize(c->xfer_done));
-  c->last_d2h_bytes += static_cast<int64_t>(n * sizeof(float));
+  c->last_d2h_bytes += static_cast<int64_t>(n * sizeof(float) + n_tail * sizeof(double));
 }
 
 template <typename T>

@@ -1,7 +1,7 @@
 """GPU test of the narrowed model transfer (include/gcpb.h,
 gcpb_last_transfer_bytes): an fp32 engine moves a large page-locked fp64 model
 as fp32 — host threads round chunk after chunk under the DMA and widen the
-result — and the host-buffer step (gcpb_step_host, the reference's loop body
+result; a share of the upload's rows crosses as fp64 without a host pass — and the host-buffer step (gcpb_step_host, the reference's loop body
 optimizer.cpp:116-119 on a host KruskalModel) must return bit-identical
 factors to the fp64 transfer (up to the summation order of the step's fp32
 atomics), with half the bytes on the bus."""
@@ -23,8 +23,8 @@ def _problem(rs, dims, nnz):
 
 
 @pytest.mark.parametrize("rank", [16, 18])  # unpadded rows land in the table; 18 -> padded to 20
-@pytest.mark.parametrize("threads", ["3", None])
-def test_narrowed_step_host_is_bit_identical(monkeypatch, rank, threads):
+@pytest.mark.parametrize("threads,tail", [("3", None), (None, "0"), (None, "40")])
+def test_narrowed_step_host_is_bit_identical(monkeypatch, rank, threads, tail):
     import torch
     g = G()
     rs = np.random.default_rng(23)
@@ -42,6 +42,8 @@ def test_narrowed_step_host_is_bit_identical(monkeypatch, rank, threads):
         monkeypatch.setenv("GCPB_NARROW", narrow)
         if threads:
             monkeypatch.setenv("GCPB_HOST_THREADS", threads)
+        if tail:
+            monkeypatch.setenv("GCPB_NARROW_TAIL", tail)
         e = g.Engine(dims, rank, dtype="f32")
         e.set_sparse(coords, vals)
         pin_in = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
@@ -63,8 +65,12 @@ def test_narrowed_step_host_is_bit_identical(monkeypatch, rank, threads):
         dev = np.concatenate([f.ravel() for f in e.factors()])
         assert np.array_equal(dev, pin_out)
         e.close()
+    # the last rows of the upload (15 % by default) cross as fp64 without a host pass
+    rows = sum(dims)
+    rows_tail = rows * int(tail if tail else 15) // 100
+    mixed = ((rows - rows_tail) * 4 + rows_tail * 8) * rank
     assert moved[0] == (n * 8, n * 8)
-    assert moved[1] == (n * 4, n * 4)
+    assert moved[1] == (mixed, n * 4)
     # same steps through both transfers (the fp32 atomics' summation order is
     # the only freedom between two runs)
     assert np.max(np.abs(outs[0] - outs[1])) <= 1e-5 * np.max(np.abs(outs[0]))
