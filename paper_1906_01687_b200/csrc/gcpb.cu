@@ -266,12 +266,15 @@ struct Tuning {
                           // 253 / 342 us at 0 / 3 / 2 / 1)
   int host_threads = 0;   // GCPB_HOST_THREADS: threads of the narrowed model transfer (0 = all cores
                           // but two, at most 32)
+  int pick_side = 1;      // GCPB_PICK_SIDE: nonzero-sharded ranks compact their picks of the global stream on
+                          // the side stream under the ordered list launch (which then goes first)
   int narrow_tail = 15;   // GCPB_NARROW_TAIL: percent of a narrowed upload's rows (the last ones) that
                           // cross as fp64 without a host pass
   int narrow = 1;         // GCPB_NARROW: fp32 engines move large page-locked fp64 models as fp32,
                           // rounded / widened on the host while the DMA runs (0 = fp64 over the bus)
   void read_env() {
     if (const char* e = getenv("GCPB_HOST_THREADS")) host_threads = std::max(0, atoi(e));
+    if (const char* e = getenv("GCPB_PICK_SIDE")) pick_side = atoi(e);
     if (const char* e = getenv("GCPB_NARROW")) narrow = atoi(e);
     if (const char* e = getenv("GCPB_NARROW_TAIL")) narrow_tail = atoi(e);
     if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
@@ -324,6 +327,9 @@ struct gcpb_ctx {
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool join_pending = false;  // run_fused: wait for ev_join before the last segment
+  int join_where = 0;         // 0: before the last segment (its list is built on the side stream);
+                              // 1: before the FIRST segments (their pick list is compacted on the
+                              // side stream), the last segment launched first; 2: before everything
   // peer steps keep each row's Adam moments on its owner only (ZeRO-1): set by
   // peer_adam_launch, cleared by gcpb_adam_reset; gcpb_peer_close refuses while set
   bool moments_sharded = false;
@@ -514,7 +520,10 @@ struct NvtxRange {
 template <typename F>
 int guard(gcpb_ctx* ctx, F&& f) {
   std::string* err = ctx ? &ctx->err : &g_global_err;
-  if (ctx) ctx->join_pending = false;  // no side-stream join survives a call that threw
+  if (ctx) {  // no side-stream join survives a call that threw
+    ctx->join_pending = false;
+    ctx->join_where = 0;
+  }
   try {
     f();
     return GCPB_OK;
@@ -1379,7 +1388,27 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     // the last segment's ordered list is being built on the side stream: the
     // segments before it go first, the join, then the ordered segment
     c->join_pending = false;
-    if (a.nseg >= 2) {
+    const int where = c->join_where;
+    c->join_where = 0;
+    if (a.nseg >= 2 && where == 1) {
+      // the FIRST segments' pick list is being compacted on the side stream: the
+      // ordered last segment goes first, the join, then the segments before it
+      FusedArgs<T> a2 = a;
+      a2.seg[0] = a.seg[a.nseg - 1];
+      a2.nseg = 1;
+      if (!c->tune.list_hot) a2.rh = 0;
+      const int64_t t2 = finish_segments(a2);
+      bool hot2 = false;
+      CK(launch_fused<T>(a2, t2, record, c->stream, c->num_sms, &hot2,
+                         il && listed ? c->tune.fused_bps2 : bps));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+      FusedArgs<T> a1 = a;
+      a1.nseg = a.nseg - 1;
+      const int64_t t1 = finish_segments(a1);
+      CK(launch_fused<T>(a1, t1, record, c->stream, c->num_sms, &used_hot,
+                         il ? c->tune.fused_bps : c->tune.side_bps));
+      used_hot = used_hot || hot2;
+    } else if (a.nseg >= 2 && where == 0) {
       FusedArgs<T> a1 = a;
       a1.nseg = a.nseg - 1;
       const int64_t t1 = finish_segments(a1);
@@ -1733,7 +1762,7 @@ void run_zero_sampler_mr(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint
 // Nonzero-sharded ranks: the picks of the global stream that fall in this
 // rank's nonzero range, compacted into pick_list[0, pick_n) (pick_compact_kernel).
 template <typename T>
-void build_pick_list(gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int64_t p) {
+void build_pick_list(gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int64_t p, int bps = 8) {
   if (c->pick_cap < p) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(c->stream, &cs));
@@ -1760,8 +1789,9 @@ void build_pick_list(gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int64_t p
   ps.ref_flag = a.ref_flag;
   int64_t* cnt = &c->dst()->pick_n;
   CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t), c->stream));
+  const int64_t chunks = (p + 256 * kPickItems - 1) / (256 * kPickItems);
   const int grid = static_cast<int>(
-      std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, static_cast<int64_t>(c->num_sms) * 8)));
+      std::max<int64_t>(1, std::min<int64_t>(chunks, static_cast<int64_t>(c->num_sms) * bps)));
   CK(launch_k(pick_compact_kernel, dim3(grid), dim3(256), 0, c->stream, ps,
               c->pick_list.as<uint64_t>(), cnt));
   CK(cudaGetLastError());
@@ -2064,6 +2094,7 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
   a.nseg = 0;
   const bool ordered = scatter && !record && est_kind < 0 && c->draw_stream == 0 &&
                        order_wanted(c);
+  bool pick_on_side = false;
   if (p > 0) {
     gcpb_shard_range(p, c->rank, c->nranks, &b0, &b1);
     // (walking the picks in COO order measured slower on C5 at every bin
@@ -2072,7 +2103,28 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     if (nz_sharded(c)) {
       // every rank draws the whole global pick stream and keeps its range
       if (record) throw std::invalid_argument("nonzero-sharded ranks record no samples");
-      build_pick_list<T>(c, a, tag_p, p);
+      // With an ordered list segment after the picks, the compaction (Philox-bound:
+      // N x p draws on N ranks) runs on the side stream under that segment's launch
+      // (memory-bound), which run_fused then launches first; the ordering itself
+      // stays on the main stream ahead of it.
+      pick_on_side = ordered && !strat && q > 0 && c->tune.pick_side != 0 &&
+                     c->tune.ord_side != 0 && c->side_stream != nullptr && c->il_enabled;
+      if (pick_on_side) {
+        CK(cudaEventRecord(c->ev_fork, c->stream));
+        CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+        cudaStream_t main_stream = c->stream;
+        c->stream = c->side_stream;
+        try {
+          build_pick_list<T>(c, a, tag_p, p, 1);  // one block per SM beside the list launch
+        } catch (...) {
+          c->stream = main_stream;
+          throw;
+        }
+        c->stream = main_stream;
+        CK(cudaEventRecord(c->ev_join, c->side_stream));
+      } else {
+        build_pick_list<T>(c, a, tag_p, p);
+      }
       a.pick_list = c->pick_list.as<uint64_t>();
       Seg sg = make_seg(SEG_PICK, tag_p, 0, p, eta_over_p, pflag, 0);
       sg.len_dev = &c->dst()->pick_n;
@@ -2095,7 +2147,8 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
         // The ordering depends only on (seed, iteration): with a pick segment
         // ahead of it, it runs on the side stream under that segment's launch
         // and run_fused joins before the ordered segment.
-        const bool side = c->tune.ord_side != 0 && a.nseg == 1 && c->side_stream != nullptr;
+        const bool side = c->tune.ord_side != 0 && a.nseg == 1 && c->side_stream != nullptr &&
+                          !pick_on_side;
         cudaStream_t os = c->stream;
         if (side) {
           CK(cudaEventRecord(c->ev_fork, c->stream));
@@ -2107,6 +2160,10 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
           CK(cudaEventRecord(c->ev_join, c->side_stream));
           c->join_pending = true;
         }
+      }
+      if (pick_on_side) {  // the join now guards the pick segment (first), not the list
+        c->join_pending = true;
+        c->join_where = built ? 1 : 2;  // no ordered list after all: join ahead of one launch
       }
       if (built) {
         a.zero_list32 = c->qorder.out.as<uint32_t>();  // the same draws, in mode-0 row order
