@@ -1442,8 +1442,9 @@ void run_fused(gcpb_ctx* c, FusedArgs<T>& a, bool record, bool fold = false) {
     c->il_gpack = true;
   }
   if (a.scatter && c->nrep > 1 && !fold) {  // fold: Adam sums the replicas itself
-    CK(launch_k(grad_reduce_kernel<T>, dim3(grid_for(c->nelem, 256, c->num_sms, 4)), dim3(256), 0,
-                c->stream, c->Gr.as<T>(), c->Grep.as<T>(), c->nelem, c->nrep, c->rep_stride));
+    const int64_t nchunk = c->nelem / c->vw;
+    CK(launch_k(grad_reduce_kernel<T>, dim3(grid_for(nchunk * 8, 256, c->num_sms, 8)), dim3(256), 0,
+                c->stream, c->Gr.as<T>(), c->Grep.as<T>(), nchunk, c->nrep, c->rep_stride));
   }
   c->hot_pending = 0;
   if (used_hot && fold) {  // the fused Adam folds the hot rows' copies itself

@@ -1237,19 +1237,59 @@ __global__ void ag_unsync_kernel(const T* __restrict__ AG, T* __restrict__ A, in
 }
 
 // G = sum of the nrep privatized gradient replicas; replicas re-zeroed.
+// Eight lanes per 16-byte chunk, each taking every eighth replica: a lane
+// issues all its loads (L2-coherent: the read-then-zero rule above) before the
+// zero stores, then the lanes' partial sums meet in a shuffle tree.  (The
+// element-per-thread loop this replaces walked the replicas one dependent
+// load + store at a time: 115 us for C3's 32 x 512 KB, now a few.)
 template <typename T>
-__global__ void grad_reduce_kernel(T* __restrict__ G, T* __restrict__ reps, int64_t n,
-                                   int nrep, int64_t stride) {
+__global__ void __launch_bounds__(256) grad_reduce_kernel(T* __restrict__ G, T* __restrict__ reps,
+                                                          int64_t nchunks, int nrep,
+                                                          int64_t stride) {
   pdl_begin();
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    T s = static_cast<T>(0);
-    for (int r = 0; r < nrep; ++r) {
-      T* p = reps + r * stride + i;
-      s += *p;
-      *p = static_cast<T>(0);
+  constexpr int VW = Vec<T>::W;
+  constexpr int kLanes = 8, kMaxPer = 4;  // up to 32 replicas per pass
+  const int sub = threadIdx.x & (kLanes - 1);
+  for (int64_t q = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kLanes;
+       q < ((nchunks + 3) & ~int64_t{3});  // whole warps (4 chunks) stay in the shuffles
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x / kLanes) {
+    const bool live = q < nchunks;
+    T acc[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) acc[e] = static_cast<T>(0);
+    for (int r0 = 0; r0 < nrep; r0 += kLanes * kMaxPer) {
+      Vec<T> v[kMaxPer];
+#pragma unroll
+      for (int j = 0; j < kMaxPer; ++j) {
+        const int r = r0 + j * kLanes + sub;
+        if (live && r < nrep) {
+          load_chunk_cg(reps + r * stride + q * VW, v[j]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) v[j].v[e] = static_cast<T>(0);
+        }
+      }
+      Vec<T> z;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) z.v[e] = static_cast<T>(0);
+#pragma unroll
+      for (int j = 0; j < kMaxPer; ++j) {
+        const int r = r0 + j * kLanes + sub;
+        if (live && r < nrep) store_chunk(reps + r * stride + q * VW, z);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc[e] += v[j].v[e];
+      }
     }
-    G[i] = s;
+#pragma unroll
+    for (int o = kLanes / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int e = 0; e < VW; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if (live && sub == 0) {
+      Vec<T> out;
+#pragma unroll
+      for (int e = 0; e < VW; ++e) out.v[e] = acc[e];
+      store_chunk(G + q * VW, out);
+    }
   }
 }
 

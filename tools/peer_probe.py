@@ -11,11 +11,20 @@ import numpy as np
 import paper_1906_01687_b200.gcp as G
 
 R = int(os.environ.get("PROBE_RANKS", "2"))
-dims, r = (4_800_000, 1_700_000, 1_800_000), 16
-rs = np.random.default_rng(1)
-nnz = 200_000
-coords = np.unique(np.stack([rs.integers(0, n, nnz) for n in dims], 1), axis=0)
-vals = np.ones(len(coords))
+CFG = os.environ.get("PROBE_CONFIG", "c5tables")
+if CFG == "c3":  # the whole C3 problem: the multi-rank stratified sampler's kernels
+    from paper_1906_01687_b200 import workloads as WL
+    w = WL.get("c3")
+    dims, r = w.dims, w.rank
+    keys = WL.sparse_keys(w, 1003)
+    coords = np.stack(np.unravel_index(keys.astype(np.int64), dims, order="F"), 1)
+    vals = np.ones(len(coords))
+else:  # C5's table size with a token tensor: the exchange kernel
+    dims, r = (4_800_000, 1_700_000, 1_800_000), 16
+    rs = np.random.default_rng(1)
+    nnz = 200_000
+    coords = np.unique(np.stack([rs.integers(0, n, nnz) for n in dims], 1), axis=0)
+    vals = np.ones(len(coords))
 
 
 class Hub:
@@ -45,6 +54,8 @@ engines, handles = [None] * R, [None] * R
 def make(rank):
     e = G.Engine(dims, r, "f32")
     e.set_sparse(coords, vals)
+    if CFG == "c3":
+        e.set_factors([np.full((n, r), 0.3) for n in dims])
     e.comm_init_host(rank, R, lambda v: hub.allgather(rank, v), lambda a: hub.allreduce(rank, a))
     engines[rank] = e
     handles[rank] = e.peer_handle()
@@ -53,7 +64,10 @@ def make(rank):
 def run(rank):
     e = engines[rank]
     e.peer_open(handles)
-    sk, lf = G.SamplerKind.semi_stratified(100_000 * R, 100_000 * R), G.LossFunction.gaussian()
+    if CFG == "c3":
+        sk, lf = G.SamplerKind.stratified(w.p * R, w.q * R, w.rho), G.LossFunction.bernoulli_odds()
+    else:
+        sk, lf = G.SamplerKind.semi_stratified(100_000 * R, 100_000 * R), G.LossFunction.gaussian()
     for it in range(4):
         e.step(sk, lf, 9, it, 1e-3)
     e.synchronize()
