@@ -2064,8 +2064,29 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
     if (c->nranks > 1) {
       if (record)
         throw std::invalid_argument("multi-rank stratified sampling records no samples");
-      run_zero_sampler_mr(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p,
-                          &res.stats);
+      if (p > 0 && eta > 0 && c->tune.ord_side != 0 && c->side_stream != nullptr) {
+        // as on one rank: the sampler (plan, test, all-gather of the accept counts,
+        // keep, commit per batch) runs on the side stream under the pick segment's
+        // launch; the communicator is used by one stream at a time (fork after the
+        // main stream's last collective, join before its next)
+        CK(cudaEventRecord(c->ev_fork, c->stream));
+        CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+        cudaStream_t main_stream = c->stream;
+        c->stream = c->side_stream;
+        try {
+          run_zero_sampler_mr(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p,
+                              &res.stats);
+        } catch (...) {
+          c->stream = main_stream;
+          throw;
+        }
+        c->stream = main_stream;
+        CK(cudaEventRecord(c->ev_join, c->side_stream));
+        c->join_pending = true;
+      } else {
+        run_zero_sampler_mr(c, q, sk->oversample, seed, iter, iter_base, tag_z, zero_mode, p,
+                            &res.stats);
+      }
       zero_mr = true;
     } else if (zero_mode != ZERO_HOST_CHECK && p > 0 && eta > 0 && c->tune.ord_side != 0 &&
                c->side_stream != nullptr) {
