@@ -16,6 +16,27 @@ if not _LIB_PATH.exists():
         f"gcpb engine library not found at {_LIB_PATH}; build it with "
         "`python -m paper_1906_01687_b200.build` (there is no CPU fallback)")
 
+
+
+def _preload_torch_nccl() -> None:
+    """libgcpb.so links libnccl.so.2; so does torch, which bundles a newer copy
+    and needs its symbols.  The first copy loaded serves the whole process, so
+    when torch's is installed it is loaded first here — importing this package
+    before torch must not leave torch with the system's older library."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        if spec and spec.submodule_search_locations:
+            for d in spec.submodule_search_locations:
+                p = Path(d) / "lib" / "libnccl.so.2"
+                if p.exists():
+                    C.CDLL(str(p), mode=C.RTLD_GLOBAL)
+                    return
+    except (ImportError, OSError, ValueError):
+        pass
+
+
+_preload_torch_nccl()
 lib = C.CDLL(str(_LIB_PATH))
 
 # status codes (gcpb.h)

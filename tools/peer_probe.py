@@ -19,6 +19,13 @@ if CFG == "c3":  # the whole C3 problem: the multi-rank stratified sampler's ker
     keys = WL.sparse_keys(w, 1003)
     coords = np.stack(np.unravel_index(keys.astype(np.int64), dims, order="F"), 1)
     vals = np.ones(len(coords))
+elif CFG == "c5":  # the whole C5 problem (generated on the device, shared by the ranks)
+    import torch
+    from paper_1906_01687_b200 import workloads as WL
+    w = WL.get("c5")
+    dims, r = w.dims, w.rank
+    c5_keys, c5_vals = WL.c5_device_data(w)
+    coords = vals = None
 else:  # C5's table size with a token tensor: the exchange kernel
     dims, r = (4_800_000, 1_700_000, 1_800_000), 16
     rs = np.random.default_rng(1)
@@ -53,7 +60,11 @@ engines, handles = [None] * R, [None] * R
 
 def make(rank):
     e = G.Engine(dims, r, "f32")
-    e.set_sparse(coords, vals)
+    if CFG == "c5":
+        e.set_sparse_device(c5_keys.data_ptr(), c5_vals.data_ptr(), c5_keys.numel(), "f32")
+        e.set_factors([np.full((n, r), 0.05) for n in dims])
+    else:
+        e.set_sparse(coords, vals)
     if CFG == "c3":
         e.set_factors([np.full((n, r), 0.3) for n in dims])
     e.comm_init_host(rank, R, lambda v: hub.allgather(rank, v), lambda a: hub.allreduce(rank, a))
@@ -66,6 +77,8 @@ def run(rank):
     e.peer_open(handles)
     if CFG == "c3":
         sk, lf = G.SamplerKind.stratified(w.p * R, w.q * R, w.rho), G.LossFunction.bernoulli_odds()
+    elif CFG == "c5":
+        sk, lf = G.SamplerKind.semi_stratified(w.p * R, w.q * R), G.LossFunction.gaussian()
     else:
         sk, lf = G.SamplerKind.semi_stratified(100_000 * R, 100_000 * R), G.LossFunction.gaussian()
     for it in range(4):
@@ -73,8 +86,12 @@ def run(rank):
     e.synchronize()
 
 
-for fn in (make, run):
-    ts = [threading.Thread(target=fn, args=(k,)) for k in range(R)]
-    [t.start() for t in ts]
-    [t.join() for t in ts]
+for k in range(R):  # one after the other: the tensor normalisation's working memory
+    make(k)
+if CFG == "c5":
+    del c5_keys, c5_vals
+    torch.cuda.empty_cache()
+ts = [threading.Thread(target=run, args=(k,)) for k in range(R)]
+[t.start() for t in ts]
+[t.join() for t in ts]
 print("peer probe done:", R, "ranks")
