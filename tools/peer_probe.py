@@ -22,7 +22,9 @@ if CFG == "c3":  # the whole C3 problem: the multi-rank stratified sampler's ker
 elif CFG == "c5":  # the whole C5 problem (generated on the device, shared by the ranks)
     import torch
     from paper_1906_01687_b200 import workloads as WL
-    w = WL.get("c5")
+    import dataclasses
+    # a fifth of C5's nonzeros: two ranks' copies of the whole tensor fit beside the generator's
+    w = dataclasses.replace(WL.get("c5"), nnz=int(os.environ.get("PROBE_NNZ", "340000000")))
     dims, r = w.dims, w.rank
     c5_keys, c5_vals = WL.c5_device_data(w)
     coords = vals = None
