@@ -266,8 +266,13 @@ struct Tuning {
                           // 253 / 342 us at 0 / 3 / 2 / 1)
   int host_threads = 0;   // GCPB_HOST_THREADS: threads of the narrowed model transfer (0 = all cores
                           // but two, at most 32)
+  bool lone_rank = false; // GCPB_DEBUG_LONE_RANK: a sharded rank alone on one GPU (timing and capture
+                          // checks, tools/shard_probe.py): rank barriers are skipped and the step
+                          // graph is captured without a communicator; the result is not a valid step
   int pick_side = 1;      // GCPB_PICK_SIDE: nonzero-sharded ranks compact their picks of the global stream on
-                          // the side stream under the ordered list launch (which then goes first)
+                          // the side stream under the ordered list launch (which then goes first);
+                          // 0 = off, 1 = on with 1 (3 from six ranks on) compaction blocks per SM,
+                          // >= 2 = that many blocks per SM
   int narrow_tail = 15;   // GCPB_NARROW_TAIL: percent of a narrowed upload's rows (the last ones) that
                           // cross as fp64 without a host pass
   int narrow = 1;         // GCPB_NARROW: fp32 engines move large page-locked fp64 models as fp32,
@@ -275,6 +280,7 @@ struct Tuning {
   void read_env() {
     if (const char* e = getenv("GCPB_HOST_THREADS")) host_threads = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_PICK_SIDE")) pick_side = atoi(e);
+    lone_rank = getenv("GCPB_DEBUG_LONE_RANK") != nullptr;
     if (const char* e = getenv("GCPB_NARROW")) narrow = atoi(e);
     if (const char* e = getenv("GCPB_NARROW_TAIL")) narrow_tail = atoi(e);
     if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
@@ -2137,7 +2143,11 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
         cudaStream_t main_stream = c->stream;
         c->stream = c->side_stream;
         try {
-          build_pick_list<T>(c, a, tag_p, p, 1);  // one block per SM beside the list launch
+          // blocks per SM beside the list launch (captured C5 step of a lone rank,
+          // tools/lone_rank_probe.py: 3.51 / 3.34 / 4.99 ms at 2 / 4 / 8 ranks with one
+          // block per SM, 3.57 / 3.66 / 4.52 ms with three)
+          const int side_bps = c->tune.pick_side >= 2 ? c->tune.pick_side : (c->nranks >= 6 ? 3 : 1);
+          build_pick_list<T>(c, a, tag_p, p, side_bps);
         } catch (...) {
           c->stream = main_stream;
           throw;
@@ -2498,7 +2508,7 @@ void check_step_args(gcpb_ctx* ctx, const gcpb_sampler* sampler, const gcpb_loss
 // rank's later work starts (NCCL: a one-element all-reduce in stream order,
 // capturable; host communicator: synchronise + an all-gather callback).
 void rank_barrier(gcpb_ctx* c) {
-  if (c->nranks == 1) return;
+  if (c->nranks == 1 || c->tune.lone_rank) return;
   if (c->comm) {
     c->barrier_buf.alloc(sizeof(int64_t));
     nck(ncclAllReduce(c->barrier_buf.p, c->barrier_buf.p, 1, ncclInt64, ncclSum, c->comm,
@@ -2559,7 +2569,8 @@ void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint6
     c->in_step = false;
     int fold = 0;
     if (multi) {
-      if (!has_comm(c)) throw std::logic_error("sharded step without a communicator");
+      if (!has_comm(c) && !c->tune.lone_rank)
+        throw std::logic_error("sharded step without a communicator");
       if (c->peer_ok) {  // reduce-scatter + sharded Adam + all-gather, one kernel
         rank_barrier(c);
         peer_adam_launch<T>(c, iter_base ? 1 : 0);
@@ -2720,7 +2731,7 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
                     uint64_t iter0, int64_t n, const gcpb_adam* adam) {
   set_adam_params(c, adam);
   ensure_grad_zero(c);
-  if (c->nranks > 1 && !c->comm) {
+  if (c->nranks > 1 && !c->comm && !c->tune.lone_rank) {
     // the host communicator cannot be captured in a graph: step eagerly
     for (int64_t k = 0; k < n; ++k)
       step_impl<T>(c, sk, loss, seed, iter0 + static_cast<uint64_t>(k), nullptr, ZERO_HOST_CHECK);
