@@ -316,3 +316,45 @@ def test_peer_step_host_matches_single_rank(monkeypatch, il):
 
     for got in _run_ranks(nranks, run):
         assert O.rel_error(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("nranks,rank", [(2, 1), (8, 3)])
+def test_lone_rank_step_graph_matches_eager_steps(monkeypatch, nranks, rank):
+    """The multi-rank step as gcpb_run_steps captures it (NCCL communicator on
+    real ranks): with GCPB_DEBUG_LONE_RANK a sharded rank alone on the GPU skips
+    the rank barriers and maps every peer to its own table, so the step graph —
+    compaction of the global pick stream on the side stream, ordered list launch
+    first, pick launch, hot fold, peer exchange kernel — is captured and
+    replayed here, and must leave what the same steps leave when issued one by
+    one (the model itself is not a valid multi-rank result)."""
+    import paper_1906_01687_b200.gcp as G
+    monkeypatch.setenv("GCPB_DEBUG_LONE_RANK", "1")
+    monkeypatch.setenv("GCPB_IL", "1")
+    monkeypatch.setenv("GCPB_HOT_T", "4")
+    dims, r, coords, vals, F = _skewed_problem(77)
+    F = [np.asarray(f, np.float32).astype(np.float64) for f in F]
+    sk, lf = G.SamplerKind.semi_stratified(1500 * nranks, 2500 * nranks), G.LossFunction.poisson()
+
+    def run(graph):
+        e = G.Engine(dims, r, "f32")
+        e.set_sparse(coords, vals)
+        e.set_factors(F)
+        e.set_shard(rank, nranks)
+        e.peer_open([e.peer_handle()] * nranks)
+        if graph:
+            e.run_steps(sk, lf, 9, 0, 4, 1e-2, lower_bound=0.0)
+            e.synchronize()
+            assert e.steps_path == "graph" and e.run_steps_launches() > 0
+        else:
+            for it in range(4):
+                e.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
+        out = e.factors()
+        e.adam_reset()
+        e.peer_close()
+        e.close()
+        return out
+
+    got, want = run(True), run(False)
+    assert any(np.abs(x - f).max() > 1e-4 for x, f in zip(got, F))  # the steps moved the model
+    for x, y in zip(got, want):
+        assert O.rel_error(x, y) <= 2e-5
