@@ -266,6 +266,11 @@ struct Tuning {
                           // 253 / 342 us at 0 / 3 / 2 / 1)
   int host_threads = 0;   // GCPB_HOST_THREADS: threads of the narrowed model transfer (0 = all cores
                           // but two, at most 32)
+  int pick_ahead = 0;     // GCPB_PICK_AHEAD: captured multi-rank steps compact the next step's picks
+                          // under the current step's exchange kernel (second pick list).  Off by
+                          // default: it pays only where the exchange leaves the SMs idle (NVLink),
+                          // which one GPU cannot show (lone-rank probe: 4.65 vs 4.67 ms at 8 ranks,
+                          // 3.66 vs 3.48 at 4, the local "exchange" being 0.2 ms of HBM traffic)
   bool lone_rank = false; // GCPB_DEBUG_LONE_RANK: a sharded rank alone on one GPU (timing and capture
                           // checks, tools/shard_probe.py): rank barriers are skipped and the step
                           // graph is captured without a communicator; the result is not a valid step
@@ -281,6 +286,7 @@ struct Tuning {
     if (const char* e = getenv("GCPB_HOST_THREADS")) host_threads = std::max(0, atoi(e));
     if (const char* e = getenv("GCPB_PICK_SIDE")) pick_side = atoi(e);
     lone_rank = getenv("GCPB_DEBUG_LONE_RANK") != nullptr;
+    if (const char* e = getenv("GCPB_PICK_AHEAD")) pick_ahead = atoi(e);
     if (const char* e = getenv("GCPB_NARROW")) narrow = atoi(e);
     if (const char* e = getenv("GCPB_NARROW_TAIL")) narrow_tail = atoi(e);
     if (const char* e = getenv("GCPB_SIDE_BPS")) side_bps = std::max(0, atoi(e));
@@ -383,6 +389,16 @@ struct gcpb_ctx {
   int64_t nz_begin = 0, nz_end = 0;
   DBuf pick_list;           // picks of the global stream in range (pick_compact_kernel)
   int64_t pick_cap = 0;
+  // the next step's picks compacted ahead, under the current step's exchange
+  // (captured multi-rank step graphs): second list, which list the current step
+  // reads, the spec of the last compaction, steps left in the capture
+  DBuf pick_list2;
+  int pick_cur = 0;
+  bool pick_ahead = false;
+  bool pick_spec_valid = false;
+  PickSpec pick_spec;
+  int64_t steps_left = 0;
+  cudaEvent_t ev_ahead = nullptr;
   DBuf mr_counts;           // multi-rank stratified: all-gathered accept counts
   int rec_words = 4;
   DBuf hkeys, hvals;
@@ -485,6 +501,7 @@ struct gcpb_ctx {
     for (cudaEvent_t e : x32_ev) cudaEventDestroy(e);
     for (void* pmap : peer_ipc) cudaIpcCloseMemHandle(pmap);
     if (comm) ncclCommDestroy(comm);
+    if (ev_ahead) cudaEventDestroy(ev_ahead);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side_stream) cudaStreamDestroy(side_stream);
@@ -529,6 +546,8 @@ int guard(gcpb_ctx* ctx, F&& f) {
   if (ctx) {  // no side-stream join survives a call that threw
     ctx->join_pending = false;
     ctx->join_where = 0;
+    ctx->pick_ahead = false;
+    ctx->steps_left = 0;
   }
   try {
     f();
@@ -1766,6 +1785,40 @@ void run_zero_sampler_mr(gcpb_ctx* c, int64_t q, double rho, uint64_t seed, uint
   }
 }
 
+uint64_t* pick_list_of(gcpb_ctx* c, int which) {
+  return which ? c->pick_list2.as<uint64_t>() : c->pick_list.as<uint64_t>();
+}
+int64_t* pick_count_of(gcpb_ctx* c, int which) {
+  return which ? &c->dst()->pick_n2 : &c->dst()->pick_n;
+}
+
+void launch_pick_compact(gcpb_ctx* c, const PickSpec& ps, int which, int bps, cudaStream_t stream) {
+  int64_t* cnt = pick_count_of(c, which);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t), stream));
+  const int64_t chunks = (ps.p + 256 * kPickItems - 1) / (256 * kPickItems);
+  const int grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(chunks, static_cast<int64_t>(c->num_sms) * bps)));
+  CK(launch_k(pick_compact_kernel, dim3(grid), dim3(256), 0, stream, ps, pick_list_of(c, which),
+              cnt));
+  CK(cudaGetLastError());
+}
+
+// Captured multi-rank steps: the NEXT step's picks are compacted into the other
+// list on the side stream while the exchange kernel (NVLink-bound) runs; the
+// iteration they belong to is rng_iter + 1, snapshotted first because the
+// exchange kernel advances rng_iter.  The next step's pick launch joins.
+void pick_compact_ahead(gcpb_ctx* c) {
+  CK(launch_k(iter_next_kernel, dim3(1), dim3(32), 0, c->stream, c->dst()));
+  CK(cudaEventRecord(c->ev_fork, c->stream));
+  CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+  PickSpec ps = c->pick_spec;
+  ps.iter = 0;
+  ps.iter_base = &c->dst()->rng_iter_next;
+  launch_pick_compact(c, ps, c->pick_cur ^ 1, 8, c->side_stream);
+  CK(cudaEventRecord(c->ev_ahead, c->side_stream));
+  c->pick_ahead = true;
+}
+
 // Nonzero-sharded ranks: the picks of the global stream that fall in this
 // rank's nonzero range, compacted into pick_list[0, pick_n) (pick_compact_kernel).
 template <typename T>
@@ -1794,14 +1847,9 @@ void build_pick_list(gcpb_ctx* c, const FusedArgs<T>& a, uint32_t tag, int64_t p
   ps.thr64_eta = a.thr64_eta;
   ps.ref_ctr = a.ref_ctr;
   ps.ref_flag = a.ref_flag;
-  int64_t* cnt = &c->dst()->pick_n;
-  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t), c->stream));
-  const int64_t chunks = (p + 256 * kPickItems - 1) / (256 * kPickItems);
-  const int grid = static_cast<int>(
-      std::max<int64_t>(1, std::min<int64_t>(chunks, static_cast<int64_t>(c->num_sms) * bps)));
-  CK(launch_k(pick_compact_kernel, dim3(grid), dim3(256), 0, c->stream, ps,
-              c->pick_list.as<uint64_t>(), cnt));
-  CK(cudaGetLastError());
+  c->pick_spec = ps;
+  c->pick_spec_valid = !a.refstream;  // RefStream draws follow a counter the steps advance
+  launch_pick_compact(c, ps, c->pick_cur, bps, c->stream);
 }
 
 // ---- unrestricted draws walked in memory order (tables beyond L2) ----------
@@ -2136,8 +2184,16 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       // (memory-bound), which run_fused then launches first; the ordering itself
       // stays on the main stream ahead of it.
       pick_on_side = ordered && !strat && q > 0 && c->tune.pick_side != 0 &&
-                     c->tune.ord_side != 0 && c->side_stream != nullptr && c->il_enabled;
-      if (pick_on_side) {
+                     c->tune.ord_side != 0 && c->side_stream != nullptr && c->il_enabled &&
+                     !c->pick_ahead;
+      if (c->pick_ahead) {
+        // compacted ahead by the previous step of this capture (pick_compact_ahead):
+        // the other list holds this step's picks once the side stream's event passes
+        c->pick_ahead = false;
+        c->pick_cur ^= 1;
+        CK(cudaStreamWaitEvent(c->stream, c->ev_ahead, 0));
+        c->pick_spec_valid = !a.refstream;
+      } else if (pick_on_side) {
         CK(cudaEventRecord(c->ev_fork, c->stream));
         CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
         cudaStream_t main_stream = c->stream;
@@ -2157,9 +2213,9 @@ SampleResult stoch_grad_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_los
       } else {
         build_pick_list<T>(c, a, tag_p, p);
       }
-      a.pick_list = c->pick_list.as<uint64_t>();
+      a.pick_list = pick_list_of(c, c->pick_cur);
       Seg sg = make_seg(SEG_PICK, tag_p, 0, p, eta_over_p, pflag, 0);
-      sg.len_dev = &c->dst()->pick_n;
+      sg.len_dev = pick_count_of(c, c->pick_cur);
       a.seg[a.nseg++] = sg;
     } else {
       a.seg[a.nseg++] = make_seg(SEG_PICK, tag_p, b0, b1, eta_over_p, pflag, 0);
@@ -2572,6 +2628,10 @@ void step_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, uint6
       if (!has_comm(c) && !c->tune.lone_rank)
         throw std::logic_error("sharded step without a communicator");
       if (c->peer_ok) {  // reduce-scatter + sharded Adam + all-gather, one kernel
+        if (iter_base && c->steps_left > 0 && c->tune.pick_ahead != 0 && c->pick_spec_valid &&
+            nz_sharded(c) && c->side_stream != nullptr && c->pick_list2.p)
+          pick_compact_ahead(c);
+        c->pick_spec_valid = false;
         rank_barrier(c);
         peer_adam_launch<T>(c, iter_base ? 1 : 0);
         rank_barrier(c);
@@ -2744,6 +2804,10 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     c->pick_list.alloc(static_cast<size_t>(sk->nonzero_samples) * sizeof(uint64_t));
     c->pick_cap = sk->nonzero_samples;
   }
+  if (nz_sharded(c) && sk->strategy != GCPB_UNIFORM && sk->nonzero_samples > 0 &&
+      c->tune.pick_ahead != 0 && c->peer_ok)  // the next step's picks, compacted ahead
+    c->pick_list2.alloc(static_cast<size_t>(c->pick_cap) * sizeof(uint64_t));
+  c->pick_ahead = false;
   if (sk->strategy == GCPB_STRATIFIED) {
     int64_t q = sk->zero_samples + (c->nnz == 0 ? sk->nonzero_samples : 0);
     if (q > 0) {
@@ -2790,9 +2854,14 @@ void run_steps_impl(gcpb_ctx* c, const gcpb_sampler* sk, const gcpb_loss* loss, 
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     try {
-      for (int64_t k = 0; k < n; ++k)
+      for (int64_t k = 0; k < n; ++k) {
+        c->steps_left = n - 1 - k;
         step_impl<T>(c, sk, loss, seed, 0, &c->dst()->rng_iter, ZERO_CAPTURE);
+      }
+      c->steps_left = 0;
     } catch (...) {
+      c->steps_left = 0;
+      c->pick_ahead = false;
       cudaStreamEndCapture(c->stream, &g);
       if (g) cudaGraphDestroy(g);
       throw;
@@ -3272,6 +3341,7 @@ int gcpb_create(int device, int dtype, int ndims, const int64_t* dims, int64_t r
       CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, hi));
       CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming));
     }
     const size_t bytes = static_cast<size_t>(c->nelem) * c->tsize;
     DBuf* bufs[4] = {&c->A, &c->Gr, &c->B, &c->C};

@@ -37,7 +37,16 @@ struct DevState {
   int64_t zg_kept;   // accepted candidates this rank keeps (its zero-list length)
   int64_t zg_batch;  // global size of the current batch
   int64_t pick_n;    // nonzero-sharded ranks: picks of the global stream in range
+  int64_t pick_n2;   // ... of the second pick list (the next step's picks, compacted ahead)
+  uint64_t rng_iter_next;  // rng_iter + 1, taken before the exchange kernel advances rng_iter
 };
+
+// The next graph-replayed step's iteration, for work queued beside the kernel
+// that advances rng_iter (the next step's pick compaction under the exchange).
+__global__ void iter_next_kernel(DevState* st) {
+  pdl_begin();
+  if (threadIdx.x == 0 && blockIdx.x == 0) st->rng_iter_next = st->rng_iter + 1;
+}
 
 // Contiguous shard [begin, end) of n items for `rank` of `nranks` -- the
 // device twin of gcpb_shard_range (gcpb.cu).

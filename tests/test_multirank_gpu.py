@@ -318,8 +318,9 @@ def test_peer_step_host_matches_single_rank(monkeypatch, il):
         assert O.rel_error(got, want) <= 1e-12
 
 
+@pytest.mark.parametrize("ahead", ["0", "1"])  # the next step's picks compacted under the exchange
 @pytest.mark.parametrize("nranks,rank", [(2, 1), (8, 3)])
-def test_lone_rank_step_graph_matches_eager_steps(monkeypatch, nranks, rank):
+def test_lone_rank_step_graph_matches_eager_steps(monkeypatch, nranks, rank, ahead):
     """The multi-rank step as gcpb_run_steps captures it (NCCL communicator on
     real ranks): with GCPB_DEBUG_LONE_RANK a sharded rank alone on the GPU skips
     the rank barriers and maps every peer to its own table, so the step graph —
@@ -329,11 +330,14 @@ def test_lone_rank_step_graph_matches_eager_steps(monkeypatch, nranks, rank):
     one (the model itself is not a valid multi-rank result)."""
     import paper_1906_01687_b200.gcp as G
     monkeypatch.setenv("GCPB_DEBUG_LONE_RANK", "1")
+    monkeypatch.setenv("GCPB_PICK_AHEAD", ahead)
     monkeypatch.setenv("GCPB_IL", "1")
     monkeypatch.setenv("GCPB_HOT_T", "4")
     dims, r, coords, vals, F = _skewed_problem(77)
     F = [np.asarray(f, np.float32).astype(np.float64) for f in F]
     sk, lf = G.SamplerKind.semi_stratified(1500 * nranks, 2500 * nranks), G.LossFunction.poisson()
+
+    launches = []
 
     def run(graph):
         e = G.Engine(dims, r, "f32")
@@ -345,6 +349,7 @@ def test_lone_rank_step_graph_matches_eager_steps(monkeypatch, nranks, rank):
             e.run_steps(sk, lf, 9, 0, 4, 1e-2, lower_bound=0.0)
             e.synchronize()
             assert e.steps_path == "graph" and e.run_steps_launches() > 0
+            launches.append(e.run_steps_launches())
         else:
             for it in range(4):
                 e.step(sk, lf, 9, it, 1e-2, lower_bound=0.0)
@@ -355,6 +360,8 @@ def test_lone_rank_step_graph_matches_eager_steps(monkeypatch, nranks, rank):
         return out
 
     got, want = run(True), run(False)
+    # 8 kernels per step; compacting ahead adds the iteration snapshot to all but the last
+    assert launches[0] == (4 * 8 + 3 if ahead == "1" else 4 * 8)
     assert any(np.abs(x - f).max() > 1e-4 for x, f in zip(got, F))  # the steps moved the model
     for x, y in zip(got, want):
         assert O.rel_error(x, y) <= 2e-5
